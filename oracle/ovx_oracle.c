@@ -1,0 +1,245 @@
+/*
+ * ovx_oracle.c — plain, slow, obviously-correct CPU oracle for the OVFEM /
+ * TCOVFEM explicit time step (arxiv 2404.13683).
+ *
+ * TEST INFRASTRUCTURE.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code, header or constant generator with the product library
+ * (paper_2404_13683_b200/csrc); the integer element matrix it multiplies is
+ * passed in from oracle/element.py (exact-rational derivation, also oracle).
+ *
+ * Build: gcc -O2 -fPIC -shared -ffp-contract=off -fno-fast-math (see oracle/build.py)
+ * -ffp-contract=off matters: every a*b+c below is two roundings unless fma()
+ * is written explicitly.
+ *
+ * Numbering (PAPER.md L38 voxel grid; reading D1):
+ *   node (ix,iy,iz) -> ix + (nx+1)*(iy + (ny+1)*iz)
+ *   element (ex,ey,ez) -> ex + nx*(ey + ny*ez)
+ * Local node order (reading Q1): (---),(+--),(++-),(-+-),(--+),(+-+),(+++),(-++).
+ * DOF order inside an element vector: 3*local_node + axis.
+ * Node arrays: 3 doubles per node, node-major xyz.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+static const int CX[8] = {0, 1, 1, 0, 0, 1, 1, 0};
+static const int CY[8] = {0, 0, 1, 1, 0, 0, 1, 1};
+static const int CZ[8] = {0, 0, 0, 0, 1, 1, 1, 1};
+
+int64_t oracle_node_id(int64_t nx, int64_t ny, int64_t ix, int64_t iy, int64_t iz) {
+    return ix + (nx + 1) * (iy + (ny + 1) * iz);
+}
+
+/* The 8 global node ids of element e in local order (Fig. 1 / reading Q1). */
+void oracle_element_nodes(int64_t nx, int64_t ny, int64_t e, int64_t out[8]) {
+    int64_t ex = e % nx, ey = (e / nx) % ny, ez = e / (nx * ny);
+    for (int a = 0; a < 8; ++a)
+        out[a] = oracle_node_id(nx, ny, ex + CX[a], ey + CY[a], ez + CZ[a]);
+}
+
+/* Per-node  w_n = dt^2 / m_n,  m_n = sum_{e ∋ n} rho_e ds^3 / 8  (Eq. 6;
+ * reading Q15).  Masses are scattered in element order. */
+void oracle_node_w(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat,
+                   const double *rho, double dt, double *w) {
+    int64_t nn = (nx + 1) * (ny + 1) * (nz + 1), ne = nx * ny * nz;
+    double *m = (double *)calloc((size_t)nn, sizeof(double));
+    double vol8 = ds * ds * ds / 8.0;
+    int64_t nodes[8];
+    for (int64_t e = 0; e < ne; ++e) {
+        double me = rho[mat[e]] * vol8;
+        oracle_element_nodes(nx, ny, e, nodes);
+        for (int a = 0; a < 8; ++a) m[nodes[a]] += me;
+    }
+    for (int64_t n = 0; n < nn; ++n) w[n] = (dt * dt) / m[n];
+    free(m);
+}
+
+/* ---------------------------------------------------------------------------
+ * (i) FP64 path.  f_e = κ ds A_κ u_e + G ds A_G u_e  with A_κ = Kk/256 and
+ * A_G = Kg/384, Kk = K^κ and Kg = K̄^G + 128 I  (DESIGN.md
+ * oracle (i) step 3): the integer matrices are applied first (sequential
+ * sums), then the two scalars.
+ * ------------------------------------------------------------------------- */
+void oracle_element_fp64(const double *ue, double kappa, double G, double ds,
+                         const int32_t *Kk, const int32_t *Kg, double *fe) {
+    double ck = kappa * ds / 256.0, cg = G * ds / 384.0;
+    for (int r = 0; r < 24; ++r) {
+        double a = 0.0, b = 0.0;
+        for (int c = 0; c < 24; ++c) {
+            a = a + (double)Kk[r * 24 + c] * ue[c];
+            b = b + (double)Kg[r * 24 + c] * ue[c];
+        }
+        fe[r] = ck * a + cg * b;
+    }
+}
+
+/* ---------------------------------------------------------------------------
+ * (ii) Integer path (Eqs. 10-17), per element.
+ *   digits == 0 : the paper's b = 2^7, M stages of signed 7-bit slices with a
+ *                 signed top digit; v clamped to ±(2^(7M)-1) (reading Q9).
+ *   digits == 1 : B200 byte slices: v' = v + 2^(7M), u8 digits b_j = byte j of v'
+ *                 (DESIGN.md variant B).  No clamp is needed: v' < 2^64.
+ * a = 2^(7M) (M = 8: a = 2^56, N = 1).
+ * Outputs (any may be NULL): s, v[48], d[nd*48], C[nd*24] (nd = M for the 7-bit
+ * digits, ceil((7M+1)/8) for bytes), y as two int64 halves of the int128
+ * (y = y_hi*2^64 + (uint64)y_lo), fe[24].
+ * Returns 0, or 1 if s is subnormal / non-finite (element treated as zero:
+ * reading Q6').
+ * ------------------------------------------------------------------------- */
+/* Digit expansion of one INT64 value (Eq. 16).
+ *   digits == 0: d_j = (v >> 7(j-1)) & 127 for j < M, top digit d_M = v >> 7(M-1)
+ *                (arithmetic shift), so v = Σ_j 2^{7(j-1)} d_j with d_j ∈ [-128,127]
+ *                (two's-complement 7-bit slices, reading Q10).  Requires |v| < 2^{7M}.
+ *   digits == 1: bytes of v' = v + 2^{7M}: d_j = (v' >> 8(j-1)) & 255, j = 1..ceil((7M+1)/8);
+ *                v = Σ_j 256^{j-1} d_j − 2^{7M} (variant B).  Requires |v| ≤ 2^{7M}+2^6. */
+void oracle_digits(int64_t v, int M, int digits, int32_t *d) {
+    int nbits = 7 * M;
+    if (!digits) {
+        for (int j = 0; j < M; ++j)
+            d[j] = (j < M - 1) ? (int32_t)((v >> (7 * j)) & 127) : (int32_t)(v >> (7 * j));
+    } else {
+        int nd = (nbits + 1 + 7) / 8;
+        uint64_t vp = (uint64_t)(v + ((int64_t)1 << nbits));
+        for (int j = 0; j < nd; ++j) d[j] = (int32_t)((vp >> (8 * j)) & 255u);
+    }
+}
+
+int oracle_element_int8(const double *ue, double kappa, double G, double ds,
+                        const int8_t *K8 /*24x48 row-major*/, int M, int digits,
+                        double *s_out, int64_t *v_out, int32_t *d_out, int64_t *C_out,
+                        int64_t *y_hi, int64_t *y_lo, double *fe) {
+    double cG = (2.0 * G) / (3.0 * kappa);       /* (2/3) G/κ, */
+    double c1 = kappa * ds / 256.0;              /* κ ds / 256, Eq. 9          */
+    double c2 = (256.0 * G) / (3.0 * kappa);     /* (256/3) G/κ, Eq. 9         */
+    int nbits = 7 * M;
+    int64_t A = (int64_t)1 << nbits;             /* a = 2^(7M) as an integer   */
+    double Ad = ldexp(1.0, nbits);
+    int nd = digits ? (nbits + 1 + 7) / 8 : M;
+
+    double ub[48];
+    for (int i = 0; i < 24; ++i) { ub[i] = ue[i]; ub[24 + i] = cG * ue[i]; }
+    /* Eq. 10: s_e = max_i |ū_ei| */
+    double s = 0.0;
+    for (int i = 0; i < 48; ++i) { double t = fabs(ub[i]); if (t > s) s = t; }
+    if (s_out) *s_out = s;
+    int64_t v[48];
+    __int128 y[24];
+    int degenerate = !(s >= 0x1p-1022) || !isfinite(s);
+    if (degenerate) {
+        for (int i = 0; i < 48; ++i) v[i] = 0;
+    } else {
+        double r = 1.0 / s;                      /* reading Q7: one reciprocal  */
+        for (int i = 0; i < 48; ++i) {
+            double x = ub[i] * r;                /* ū_es, Eq. 10                */
+            double t = x * Ad;                   /* exact power-of-two scaling  */
+            v[i] = (int64_t)t;                   /* truncation toward 0, Eq. 12 (Q8) */
+            if (!digits) {                       /* reading Q9 clamp            */
+                if (v[i] > A - 1) v[i] = A - 1;
+                if (v[i] < -(A - 1)) v[i] = -(A - 1);
+            }
+        }
+    }
+    if (v_out) memcpy(v_out, v, sizeof v);
+    for (int r = 0; r < 24; ++r) y[r] = 0;
+    int32_t dall[48][8];
+    for (int k = 0; k < 48; ++k) oracle_digits(v[k], M, digits, dall[k]);
+    for (int j = 0; j < nd; ++j) {
+        int32_t d[48];
+        for (int k = 0; k < 48; ++k) {
+            d[k] = dall[k][j];
+            if (d_out) d_out[j * 48 + k] = d[k];
+        }
+        for (int r = 0; r < 24; ++r) {
+            int64_t c = 0;                       /* Eq. 17: K_e^INT8 · digits_j   */
+            for (int k = 0; k < 48; ++k) c += (int64_t)K8[r * 48 + k] * d[k];
+            if (C_out) C_out[j * 24 + r] = c;
+            __int128 w = digits ? ((__int128)1 << (8 * j)) : ((__int128)1 << (7 * j));
+            y[r] += w * (__int128)c;
+        }
+    }
+    if (digits) {
+        /* K_e^INT8 · (a·1) = a · rowsum; subtract it back:  y = K v' − a K 1 */
+        for (int r = 0; r < 24; ++r) {
+            int64_t rs = 0;
+            for (int k = 0; k < 48; ++k) rs += K8[r * 48 + k];
+            y[r] -= (__int128)A * (__int128)rs;
+        }
+    }
+    double sig = s * ldexp(1.0, -nbits);         /* s_e / a (Eq. 15)              */
+    for (int r = 0; r < 24; ++r) {
+        if (y_hi) y_hi[r] = (int64_t)(y[r] >> 64);
+        if (y_lo) y_lo[r] = (int64_t)(uint64_t)y[r];
+        if (fe) {
+            double Y = degenerate ? 0.0 : (double)y[r];  /* RN(y), one rounding (Q13) */
+            double a = Y * sig;
+            double b = c2 * ue[r];
+            fe[r] = degenerate ? 0.0 : c1 * (a + b);    /* Eq. 9, literal order */
+        }
+    }
+    return degenerate;
+}
+
+/* f = Σ_e scatter(K_e u_e), element order, f zeroed first.
+ * path 0: FP64 (Kk, Kg);  path 1: integer path (K8, M, digits). */
+void oracle_apply_K(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat,
+                    const double *kappa, const double *G, int path,
+                    const int32_t *Kk, const int32_t *Kg, const int8_t *K8, int M, int digits,
+                    const double *u, double *f) {
+    int64_t nn = (nx + 1) * (ny + 1) * (nz + 1), ne = nx * ny * nz;
+    memset(f, 0, sizeof(double) * 3 * (size_t)nn);
+    int64_t nodes[8];
+    double ue[24], fe[24];
+    for (int64_t e = 0; e < ne; ++e) {
+        oracle_element_nodes(nx, ny, e, nodes);
+        for (int a = 0; a < 8; ++a)
+            for (int c = 0; c < 3; ++c) ue[3 * a + c] = u[3 * nodes[a] + c];
+        int m = mat[e];
+        if (path == 0) oracle_element_fp64(ue, kappa[m], G[m], ds, Kk, Kg, fe);
+        else oracle_element_int8(ue, kappa[m], G[m], ds, K8, M, digits,
+                                 NULL, NULL, NULL, NULL, NULL, NULL, fe);
+        for (int a = 0; a < 8; ++a)
+            for (int c = 0; c < 3; ++c) f[3 * nodes[a] + c] += fe[3 * a + c];
+    }
+}
+
+/* Central-difference time stepping (Eq. 3, update L263-L266 with the
+ * sign of Eq. 3: F − K u, reading Q14):
+ *   u^{it+1} = fma(w, F^{it} − f, 2 u^{it} − u^{it−1}),  f = K u^{it},  w = dt²/m
+ * Dirichlet: bit a of dmask[n] set -> component a forced to 0 after the update.
+ * Sources: src_node[k], src_axis[k], amplitude amp[k*n_t + it] (0 beyond n_t).
+ * u and u_prev are advanced in place; *it is incremented per step.
+ * Returns 0, or 3 if a non-finite value appeared (the step index is in *it). */
+int oracle_run(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat,
+               const double *kappa, const double *G, const double *w, const uint8_t *dmask,
+               int path, const int32_t *Kk, const int32_t *Kg, const int8_t *K8, int M, int digits,
+               int nsrc, const int64_t *src_node, const int32_t *src_axis, int64_t n_t,
+               const double *amp, double *u, double *u_prev, int64_t *it, int64_t nsteps) {
+    int64_t nn = (nx + 1) * (ny + 1) * (nz + 1);
+    double *f = (double *)malloc(sizeof(double) * 3 * (size_t)nn);
+    double *F = (double *)calloc(3 * (size_t)nn, sizeof(double));
+    int status = 0;
+    for (int64_t step = 0; step < nsteps; ++step) {
+        oracle_apply_K(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, u, f);
+        for (int k = 0; k < nsrc; ++k)
+            F[3 * src_node[k] + src_axis[k]] += (*it < n_t) ? amp[(int64_t)k * n_t + *it] : 0.0;
+        for (int64_t n = 0; n < nn; ++n) {
+            for (int c = 0; c < 3; ++c) {
+                int64_t i = 3 * n + c;
+                double b = 2.0 * u[i] - u_prev[i];
+                double un = fma(w[n], F[i] - f[i], b);
+                if (dmask && (dmask[n] >> c) & 1) un = 0.0;
+                if (!isfinite(un)) status = 3;
+                u_prev[i] = u[i];
+                u[i] = un;
+            }
+        }
+        for (int k = 0; k < nsrc; ++k) F[3 * src_node[k] + src_axis[k]] = 0.0;
+        *it += 1;
+        if (status) break;
+    }
+    free(f);
+    free(F);
+    return status;
+}

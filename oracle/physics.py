@@ -1,0 +1,53 @@
+"""Closed forms and metrics used to pin the oracle (TEST INFRASTRUCTURE).
+
+* err_metric: PAPER.md L232-L235 (the §3 Err definition).
+* Central-difference recurrence for one eigenmode (Eq. 3): with
+  K φ = λ M φ and u^n = a_n φ,  a_{n+1} = (2 − λ dt²) a_n − a_{n−1}.
+* 1-D lattice dispersion for axis-aligned plane waves on a homogeneous voxel
+  mesh (textbook two-node bar + diagonal mass):  λ = (4 V²/ds²) sin²(k ds/2).
+* Leapfrog energy invariant for Eq. 3 (textbook):
+  E_{n+½} = ½ v_{n+½}ᵀ M v_{n+½} + ½ u_nᵀ K u_{n+1},  v_{n+½} = (u_{n+1} − u_n)/dt.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def err_metric(obs: np.ndarray, ref: np.ndarray) -> float:
+    """Err = (1/n_c) Σ_i Σ_j (u_obs − u_ref)² / Σ_j u_ref²   (channels × steps)."""
+    obs = np.asarray(obs, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    if obs.shape != ref.shape:
+        raise ValueError("channel/step mismatch")
+    den = np.sum(ref * ref, axis=1)
+    if np.any(den == 0):
+        raise ValueError("zero-energy reference channel")
+    return float(np.mean(np.sum((obs - ref) ** 2, axis=1) / den))
+
+
+def lattice_lambda_axis(V: float, k: float, ds: float) -> float:
+    """M⁻¹K eigenvalue of an axis-aligned plane wave with speed V (P: Vp, S: Vs)."""
+    return 4.0 * V * V / (ds * ds) * math.sin(k * ds / 2.0) ** 2
+
+
+def mode_amplitude(lam: float, dt: float, n: int, a0: float = 1.0, am1: float | None = None) -> float:
+    """Closed-form a_n of a_{n+1} = (2 − λdt²) a_n − a_{n−1} (default a_{−1} = a_0)."""
+    if am1 is None:
+        am1 = a0
+    c = 1.0 - lam * dt * dt / 2.0
+    th = math.acos(c)
+    # a_n = A cos nθ + B sin nθ;  A = a0,  a_{-1} = A cos θ − B sin θ
+    B = (a0 * math.cos(th) - am1) / math.sin(th)
+    return a0 * math.cos(n * th) + B * math.sin(n * th)
+
+
+def leapfrog_energy(K, m_diag, u_n, u_np1, dt) -> float:
+    v = (u_np1 - u_n) / dt
+    return 0.5 * float(v @ (m_diag * v)) + 0.5 * float(u_n @ (K @ u_np1))
+
+
+def ricker(t: np.ndarray, f0: float, t0: float) -> np.ndarray:
+    a = (math.pi * f0 * (t - t0)) ** 2
+    return (1.0 - 2.0 * a) * np.exp(-a)
