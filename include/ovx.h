@@ -1,0 +1,141 @@
+/*
+ * ovx.h — C ABI of the B200-native OVFEM / TCOVFEM explicit time step
+ * (arxiv 2404.13683, "Low-ordered Orthogonal Voxel Finite Element with INT8
+ * Tensor Cores for GPU-based Explicit Elastic Wave Propagation Analysis").
+ *
+ * The library computes, per time step, the element-by-element stiffness
+ * product  f = Σ_e K_e^o u_e  of the orthogonal voxel element (Eq. 5,
+ * L66-L69) through the paper's integer form (Eq. 9; Eqs. 10-17,
+ * L112-L146) on tcgen05 kind::i8 tensor cores, or through an FP64 CUDA-core
+ * reference kernel, fused with the diagonal-mass central-difference update
+ * (Eq. 3; update L263-L266 with the sign of Eq. 3).
+ *
+ * Conventions (all entry points)
+ *  - Every function returns ovx_status.  On failure the context keeps a
+ *    message readable with ovx_last_error(); the context stays usable unless
+ *    the status is OVX_ECUDA (sticky device error).
+ *  - ovx_ctx is opaque and not thread-safe: one host thread per context.
+ *  - Host pointers are owned by the caller, read/written only during the call
+ *    and never retained.  *_device variants take device pointers on the
+ *    context's device, valid for the duration of the call.
+ *  - Work is enqueued on the context stream (ovx_set_stream) and is
+ *    asynchronous unless stated; functions returning host data synchronise.
+ *  - Layouts:
+ *      node (ix,iy,iz)     -> ix + (nx+1)*(iy + (ny+1)*iz)
+ *      element (ex,ey,ez)  -> ex + nx*(ey + ny*ez)
+ *      node arrays         3 doubles per node, node-major (x,y,z)
+ *      element materials   uint8 per element (material id)
+ *      Dirichlet mask      uint8 per node, bit a set = component a fixed to 0
+ *      local node order    (---),(+--),(++-),(-+-),(--+),(+-+),(+++),(-++)
+ *                          (Fig. 1 is missing from PAPER.md; reading Q1)
+ */
+#ifndef OVX_H
+#define OVX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ovx_ctx ovx_ctx;
+typedef int ovx_status;
+
+enum {
+    OVX_OK = 0,
+    OVX_EINVAL = 2,     /* rejected input: dims <= 0, ds <= 0, unknown material id, NaN/Inf, size mismatch */
+    OVX_EUNSTABLE = 3,  /* a non-finite displacement appeared (ovx_check_finite) */
+    OVX_ESTATE = 6,     /* call-order violation (e.g. step before setup) */
+    OVX_ECUDA = 7,      /* CUDA runtime error (message has the CUDA error string) */
+    OVX_ENCCL = 8,      /* reserved for the multi-GPU transport */
+    OVX_ENOMEM = 9      /* device allocation failed */
+};
+
+enum {
+    OVX_INT8 = 0,       /* tcgen05 kind::i8 path: Eqs. 10-17 with byte slices (DESIGN.md variant B) */
+    OVX_FP64 = 1        /* FP64 CUDA-core reference: f_e = κ ds A_κ u_e + G ds A_G u_e */
+};
+
+/* ---- lifetime ------------------------------------------------------------ */
+/* Create a context on CUDA device `device` (must be sm_100).  *out is NULL on error. */
+ovx_status ovx_create(int device, ovx_ctx **out);
+ovx_status ovx_destroy(ovx_ctx *ctx);
+/* Last error message of ctx ("" if none).  ctx may be NULL (global message). */
+const char *ovx_last_error(const ovx_ctx *ctx);
+/* Library version string. */
+const char *ovx_version(void);
+/* Order all work of ctx on `stream` (a cudaStream_t of the context's device; NULL = library stream). */
+ovx_status ovx_set_stream(ovx_ctx *ctx, void *stream);
+
+/* ---- model (cubes of side ds on a structured grid; L94: κ, G) -- */
+/* Global element counts and edge length; nx,ny,nz >= 1, ds > 0.  Resets the model. */
+ovx_status ovx_set_grid(ovx_ctx *ctx, int64_t nx, int64_t ny, int64_t nz, double ds);
+/* n <= 256 materials; rho, kappa, G > 0 and finite (host arrays of length n). */
+ovx_status ovx_set_materials(ovx_ctx *ctx, int n, const double *rho, const double *kappa,
+                             const double *G);
+/* Per-element material ids (host, nx*ny*nz bytes); every id < n materials. */
+ovx_status ovx_set_element_materials(ovx_ctx *ctx, const uint8_t *mat);
+/* Per-node Dirichlet mask (host, Nn bytes) or NULL for free surfaces (the default). */
+ovx_status ovx_set_dirichlet(ovx_ctx *ctx, const uint8_t *mask);
+/* Time step dt > 0 (Eq. 3). */
+ovx_status ovx_set_dt(ovx_ctx *ctx, double dt);
+/* Derive K_e^INT8 on the host in exact rational arithmetic,
+ * check that all 1152 entries are integers in [-128,127] (L110; else OVX_EINVAL),
+ * build per-material constants and the per-node w = dt²/m (Eq. 6, m_n = Σ ρ_e ds³/8).
+ * path: OVX_INT8 or OVX_FP64.  stages: M (only 8 is supported by the kernels). */
+ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages);
+/* Copy the library's derived K_e^INT8 (24x48 row-major) to host memory. */
+ovx_status ovx_get_int8_matrix(ovx_ctx *ctx, int8_t *out);
+/* Element-bound stability limit 2/sqrt(max_e λ_max(M_e⁻¹ K_e)) over the materials present. */
+ovx_status ovx_critical_dt(ovx_ctx *ctx, double *dt_elem_bound);
+/* Point sources: component axis[k] of node[k] receives amp[k*n_t + it] at step it (0 after n_t).
+ * n <= 16.  (impulse force at an input point.) */
+ovx_status ovx_set_sources(ovx_ctx *ctx, int n, const int64_t *node, const int32_t *axis,
+                           int64_t n_t, const double *amp);
+
+/* ---- state (u^{it}, u^{it-1}, it) is the complete state: also checkpoint/resume -- */
+ovx_status ovx_set_state(ovx_ctx *ctx, const double *u, const double *u_prev, int64_t it);
+ovx_status ovx_get_state(ovx_ctx *ctx, double *u, double *u_prev, int64_t *it);
+ovx_status ovx_set_state_device(ovx_ctx *ctx, const double *u, const double *u_prev, int64_t it);
+ovx_status ovx_get_state_device(ovx_ctx *ctx, double *u, double *u_prev, int64_t *it);
+
+/* ---- time stepping ------------------------------------------------------- */
+/* Advance n steps: u^{it+1} = fma(w, F^{it} − K u^{it}, 2u^{it} − u^{it−1}), Dirichlet
+ * components forced to 0.  One fused kernel launch per step, asynchronous. */
+ovx_status ovx_step(ovx_ctx *ctx, int64_t n);
+/* Wait for all work on the context stream. */
+ovx_status ovx_sync(ovx_ctx *ctx);
+/* OVX_EUNSTABLE if u^{it} holds a NaN/Inf (synchronises). */
+ovx_status ovx_check_finite(ovx_ctx *ctx);
+
+/* ---- parity hooks -------------------------------------------------------- */
+/* f = K u for one EBE product (same kernel as ovx_step, update disabled).
+ * Host arrays of 3*Nn doubles.  Does not change the state. */
+ovx_status ovx_apply_K(ovx_ctx *ctx, const double *u, double *f);
+ovx_status ovx_apply_K_device(ovx_ctx *ctx, const double *u, double *f);
+/* Bit-level integer-path record for elements [e0, e0+ne) of the product with the host
+ * field u (3*Nn doubles), from the production kernel (INT8 path only):
+ *   s[ne]            Eq. 10 scale s_e = max|ū_e|
+ *   v[ne*48]         INT64 image trunc(2^56 ū_e/s_e)   (Eq. 12, a = 2^56)
+ *   d[ne*8*48]       byte slices of v + 2^56, stage-major (variant B of Eq. 16)
+ *   C[ne*8*24]       per-stage tensor-core products K_e^INT8 · d_j (INT32, Eq. 17)
+ *   y_hi,y_lo[ne*24] y = K_e^INT8 v as a 128-bit integer (y_hi*2^64 + (uint64)y_lo)
+ *   fe[ne*24]        element force f_e (Eq. 9)
+ * Any output pointer may be NULL. */
+ovx_status ovx_debug_element_ints(ovx_ctx *ctx, const double *u, int64_t e0, int64_t ne,
+                                  double *s, int64_t *v, uint8_t *d, int32_t *C,
+                                  int64_t *y_hi, int64_t *y_lo, double *fe);
+/* Per-node w = dt²/m_n (host, Nn doubles). */
+ovx_status ovx_get_node_w(ovx_ctx *ctx, double *w);
+
+/* ---- instrumentation ----------------------------------------------------- */
+/* Device time of the step kernels launched since the last reset, from CUDA events on
+ * the context stream (synchronises); resets the counters if reset != 0. */
+ovx_status ovx_get_timers(ovx_ctx *ctx, double *ms_step, int64_t *launches, int reset);
+/* Number of CTAs / threads / dynamic smem bytes of the step kernel for the current model. */
+ovx_status ovx_get_launch_config(ovx_ctx *ctx, int64_t *ctas, int *threads, int *smem_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OVX_H */

@@ -1,0 +1,63 @@
+// ovx_internal.h — declarations shared by the C-ABI layer (capi.cu) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ovx {
+
+constexpr int kMaxMat = 256;
+constexpr int kMaxSrc = 16;
+
+// Per-material constants, computed on the host in the operation order the
+// oracle's definition fixes (DESIGN.md §Integer path):
+//   cG = (2G)/(3κ)   c1 = κ ds/256   c2 = (256G)/(3κ)     (Eq. 9)
+//   ck = κ ds/256    cg = G ds/384                           (FP64 path: κ ds A_κ + G ds A_G)
+struct MatConst {
+    double cG, c1, c2, ck, cg, rho_vol8;
+};
+
+enum Mode { MODE_STEP = 0, MODE_APPLY = 1, MODE_DEBUG = 2 };
+
+struct StepParams {
+    int64_t nx, ny, nz;
+    const double *u;      // u^{it} (3 per node)
+    double *uo;           // MODE_STEP: in u^{it-1}, out u^{it+1}
+    const double *w;      // dt²/m per node
+    const uint8_t *mat;   // material id per element
+    const uint8_t *dmask; // Dirichlet mask per node (may be null)
+    double *fout;         // MODE_APPLY / MODE_DEBUG: f = K u
+    int nsrc;
+    int64_t src_dof[kMaxSrc];
+    double src_val[kMaxSrc];
+    // tiling
+    int tiles_x, tiles_y, zchunk;
+    // MODE_DEBUG outputs for elements [dbg_e0, dbg_e0 + dbg_ne)
+    int64_t dbg_e0, dbg_ne;
+    double *dbg_s;
+    int64_t *dbg_v;
+    uint8_t *dbg_d;
+    int32_t *dbg_C;
+    int64_t *dbg_yhi, *dbg_ylo;
+    double *dbg_fe;
+};
+
+struct LaunchInfo {
+    int64_t ctas;
+    int threads;
+    int smem;
+};
+
+// kernels.cu
+cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, const double *kk,
+                             const double *kg, cudaStream_t st);
+LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz);
+cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st);
+cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, double dt, double *w,
+                          cudaStream_t st);
+cudaError_t launch_finite_check(const double *u, int64_t n, int *flag, cudaStream_t st);
+
+// element_setup.cpp
+int derive_element_matrices(int8_t *k8, double *Ak, double *Ag);
+double sym_lambda_max(const double *A);
+
+}  // namespace ovx

@@ -1,0 +1,276 @@
+"""Thin ctypes binding of the C ABI in include/ovx.h (argument marshalling only).
+
+Every step of the method runs inside libovx.so (hand-written sm_100a kernels).  There is no
+CPU fallback: if the library cannot be loaded, importing this module's `lib()` raises.
+Method names are the C names without the `ovx_` prefix.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from functools import lru_cache
+
+import numpy as np
+
+from . import build as _build
+
+OVX_OK, OVX_EINVAL, OVX_EUNSTABLE, OVX_ESTATE, OVX_ECUDA, OVX_ENCCL, OVX_ENOMEM = 0, 2, 3, 6, 7, 8, 9
+OVX_INT8, OVX_FP64 = 0, 1
+
+_c = ctypes
+_vp = _c.c_void_p
+_i64 = _c.c_int64
+_int = _c.c_int
+_d = _c.c_double
+
+
+class OvxError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"ovx status {status}: {msg}")
+        self.status = status
+
+
+_SIGS = {
+    "ovx_create": [_int, _c.POINTER(_vp)],
+    "ovx_destroy": [_vp],
+    "ovx_set_stream": [_vp, _vp],
+    "ovx_set_grid": [_vp, _i64, _i64, _i64, _d],
+    "ovx_set_materials": [_vp, _int, _vp, _vp, _vp],
+    "ovx_set_element_materials": [_vp, _vp],
+    "ovx_set_dirichlet": [_vp, _vp],
+    "ovx_set_dt": [_vp, _d],
+    "ovx_setup_elements": [_vp, _int, _int],
+    "ovx_get_int8_matrix": [_vp, _vp],
+    "ovx_critical_dt": [_vp, _vp],
+    "ovx_set_sources": [_vp, _int, _vp, _vp, _i64, _vp],
+    "ovx_set_state": [_vp, _vp, _vp, _i64],
+    "ovx_get_state": [_vp, _vp, _vp, _vp],
+    "ovx_set_state_device": [_vp, _vp, _vp, _i64],
+    "ovx_get_state_device": [_vp, _vp, _vp, _vp],
+    "ovx_step": [_vp, _i64],
+    "ovx_sync": [_vp],
+    "ovx_check_finite": [_vp],
+    "ovx_apply_K": [_vp, _vp, _vp],
+    "ovx_apply_K_device": [_vp, _vp, _vp],
+    "ovx_debug_element_ints": [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "ovx_get_node_w": [_vp, _vp],
+    "ovx_get_timers": [_vp, _vp, _vp, _int],
+    "ovx_get_launch_config": [_vp, _vp, _vp, _vp],
+}
+EXPORTS = tuple(_SIGS) + ("ovx_last_error", "ovx_version")
+
+
+@lru_cache(maxsize=1)
+def lib() -> ctypes.CDLL:
+    """Load (building in-tree if stale) libovx.so; raises if it cannot be loaded."""
+    path = _build.LIB if os.path.exists(_build.LIB) and not _build._stale() else _build.build()
+    L = ctypes.CDLL(path)
+    for name, args in _SIGS.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = _int
+    L.ovx_last_error.argtypes = [_vp]
+    L.ovx_last_error.restype = _c.c_char_p
+    L.ovx_version.argtypes = []
+    L.ovx_version.restype = _c.c_char_p
+    return L
+
+
+def _np_ptr(a: np.ndarray):
+    return a.ctypes.data_as(_vp)
+
+
+def _host(a, dtype) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _dev_ptr(t) -> int:
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous() and t.dtype == torch.float64):
+        raise TypeError("expected a contiguous CUDA float64 tensor")
+    return t.data_ptr()
+
+
+class Ovx:
+    """One context on one GPU.  Methods mirror `ovx_*` of include/ovx.h."""
+
+    def __init__(self, device: int = 0):
+        self._L = lib()
+        h = _vp()
+        self._check(self._L.ovx_create(device, _c.byref(h)), None)
+        self.h = h
+        self.device = device
+        self.nx = self.ny = self.nz = 0
+
+    # -- helpers ---------------------------------------------------------------
+    def _check(self, st: int, h) -> None:
+        if st != OVX_OK:
+            msg = self._L.ovx_last_error(h).decode()
+            raise OvxError(st, msg)
+
+    def _call(self, name: str, *args) -> None:
+        self._check(getattr(self._L, name)(self.h, *args), self.h)
+
+    @property
+    def n_nodes(self) -> int:
+        return (self.nx + 1) * (self.ny + 1) * (self.nz + 1)
+
+    @property
+    def n_elems(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self._L.ovx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- C ABI -------------------------------------------------------------------
+    def set_stream(self, stream) -> None:
+        """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None."""
+        raw = getattr(stream, "cuda_stream", stream)
+        self._call("ovx_set_stream", _vp(raw) if raw else None)
+
+    def set_grid(self, nx: int, ny: int, nz: int, ds: float) -> None:
+        self._call("ovx_set_grid", nx, ny, nz, ds)
+        self.nx, self.ny, self.nz = nx, ny, nz
+
+    def set_materials(self, rho, kappa, G) -> None:
+        r, k, g = _host(rho, np.float64), _host(kappa, np.float64), _host(G, np.float64)
+        self._call("ovx_set_materials", len(r), _np_ptr(r), _np_ptr(k), _np_ptr(g))
+
+    def set_element_materials(self, mat) -> None:
+        m = _host(mat, np.uint8)
+        if m.size != self.n_elems:
+            raise OvxError(OVX_EINVAL, "element material array size mismatch")
+        self._call("ovx_set_element_materials", _np_ptr(m))
+
+    def set_dirichlet(self, mask) -> None:
+        if mask is None:
+            self._call("ovx_set_dirichlet", None)
+            return
+        m = _host(mask, np.uint8)
+        if m.size != self.n_nodes:
+            raise OvxError(OVX_EINVAL, "Dirichlet mask size mismatch")
+        self._call("ovx_set_dirichlet", _np_ptr(m))
+
+    def set_dt(self, dt: float) -> None:
+        self._call("ovx_set_dt", dt)
+
+    def setup_elements(self, path: int = OVX_INT8, stages: int = 8) -> None:
+        self._call("ovx_setup_elements", path, stages)
+
+    def get_int8_matrix(self) -> np.ndarray:
+        out = np.zeros((24, 48), dtype=np.int8)
+        self._call("ovx_get_int8_matrix", _np_ptr(out))
+        return out
+
+    def critical_dt(self) -> float:
+        out = np.zeros(1)
+        self._call("ovx_critical_dt", _np_ptr(out))
+        return float(out[0])
+
+    def set_sources(self, node, axis, amp) -> None:
+        node = _host(node, np.int64)
+        axis = _host(axis, np.int32)
+        amp = _host(amp, np.float64).reshape(len(node), -1) if len(node) else np.zeros((0, 0))
+        self._call("ovx_set_sources", len(node), _np_ptr(node), _np_ptr(axis), amp.shape[1] if len(node) else 0,
+                   _np_ptr(amp))
+
+    def set_state(self, u, u_prev, it: int = 0) -> None:
+        u, up = _host(u, np.float64), _host(u_prev, np.float64)
+        if u.size != 3 * self.n_nodes or up.size != 3 * self.n_nodes:
+            raise OvxError(OVX_EINVAL, "state size mismatch")
+        self._call("ovx_set_state", _np_ptr(u), _np_ptr(up), it)
+
+    def get_state(self):
+        u = np.zeros(3 * self.n_nodes)
+        up = np.zeros(3 * self.n_nodes)
+        it = np.zeros(1, dtype=np.int64)
+        self._call("ovx_get_state", _np_ptr(u), _np_ptr(up), _np_ptr(it))
+        return u, up, int(it[0])
+
+    def set_state_device(self, u, u_prev, it: int = 0) -> None:
+        self._call("ovx_set_state_device", _vp(_dev_ptr(u)), _vp(_dev_ptr(u_prev)), it)
+
+    def get_state_device(self, u, u_prev) -> int:
+        it = np.zeros(1, dtype=np.int64)
+        self._call("ovx_get_state_device", _vp(_dev_ptr(u)), _vp(_dev_ptr(u_prev)), _np_ptr(it))
+        return int(it[0])
+
+    def step(self, n: int = 1) -> None:
+        self._call("ovx_step", n)
+
+    def sync(self) -> None:
+        self._call("ovx_sync")
+
+    def check_finite(self) -> None:
+        self._call("ovx_check_finite")
+
+    def apply_K(self, u) -> np.ndarray:
+        u = _host(u, np.float64)
+        f = np.zeros_like(u)
+        self._call("ovx_apply_K", _np_ptr(u), _np_ptr(f))
+        return f
+
+    def apply_K_device(self, u, f) -> None:
+        self._call("ovx_apply_K_device", _vp(_dev_ptr(u)), _vp(_dev_ptr(f)))
+
+    def debug_element_ints(self, u, e0: int, ne: int) -> dict:
+        u = _host(u, np.float64)
+        s = np.zeros(ne)
+        v = np.zeros((ne, 48), dtype=np.int64)
+        d = np.zeros((ne, 8, 48), dtype=np.uint8)
+        C = np.zeros((ne, 8, 24), dtype=np.int32)
+        yh = np.zeros((ne, 24), dtype=np.int64)
+        yl = np.zeros((ne, 24), dtype=np.int64)
+        fe = np.zeros((ne, 24))
+        self._call("ovx_debug_element_ints", _np_ptr(u), e0, ne, _np_ptr(s), _np_ptr(v), _np_ptr(d), _np_ptr(C),
+                   _np_ptr(yh), _np_ptr(yl), _np_ptr(fe))
+        y = [[(int(h) << 64) + (int(l) & ((1 << 64) - 1)) for h, l in zip(yh[j], yl[j])] for j in range(ne)]
+        return dict(s=s, v=v, d=d, C=C, y=y, fe=fe)
+
+    def debug_element_forces(self, u, e0: int, ne: int) -> np.ndarray:
+        u = _host(u, np.float64)
+        fe = np.zeros((ne, 24))
+        self._call("ovx_debug_element_ints", _np_ptr(u), e0, ne, None, None, None, None, None, None, _np_ptr(fe))
+        return fe
+
+    def get_node_w(self) -> np.ndarray:
+        w = np.zeros(self.n_nodes)
+        self._call("ovx_get_node_w", _np_ptr(w))
+        return w
+
+    def get_timers(self, reset: bool = False):
+        ms = np.zeros(1)
+        n = np.zeros(1, dtype=np.int64)
+        self._call("ovx_get_timers", _np_ptr(ms), _np_ptr(n), 1 if reset else 0)
+        return float(ms[0]), int(n[0])
+
+    def get_launch_config(self):
+        c = np.zeros(1, dtype=np.int64)
+        t = np.zeros(1, dtype=np.int32)
+        s = np.zeros(1, dtype=np.int32)
+        self._call("ovx_get_launch_config", _np_ptr(c), _np_ptr(t), _np_ptr(s))
+        return int(c[0]), int(t[0]), int(s[0])
+
+    # -- convenience ---------------------------------------------------------------
+    def load_model(self, m, path: int = OVX_INT8) -> None:
+        """Upload a workloads.Model-like object (grid, materials, mask, dt, sources) and set up."""
+        self.set_grid(m.nx, m.ny, m.nz, m.ds)
+        self.set_materials(m.rho, m.kappa, m.G)
+        self.set_element_materials(m.mat)
+        self.set_dirichlet(m.dirichlet)
+        self.setup_elements(path, 8)
+        self.set_dt(m.dt)
+        if len(m.src_node):
+            self.set_sources(m.src_node, m.src_axis, m.amp)
+
+
+def version() -> str:
+    return lib().ovx_version().decode()

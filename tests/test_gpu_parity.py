@@ -1,0 +1,204 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars:
+  * integer work (v, byte slices, per-stage tensor-core products C_j, y) — bit-exact;
+  * element forces, global f = K u, node w, and whole trajectories — bit-exact, because the
+    kernel reproduces the oracle's operation order (explicit _rn intrinsics, element-order
+    scatter); the 1e-10 rel-L2 bar of BASELINE.json is checked as well;
+  * full-size (256³) launches: sampled nodes recomputed by the oracle element by element.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ovxmod():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2404_13683_b200 import ovx
+    return ovx
+
+
+def _solver(ovxmod, m, path):
+    s = ovxmod.Ovx(0)
+    s.load_model(m, path)
+    return s
+
+
+PATHS = [("int8", 0), ("fp64", 1)]
+
+
+def _ragged():
+    # spans several tiles in x (31 nodes) and y (3 nodes), two z-chunks (64 planes), ragged tails
+    m = wl.small_random(40, 8, 70, ds=0.01, dt=1e-6)
+    return m
+
+
+def test_node_w_bit_exact(ovxmod):
+    m = _ragged()
+    s = _solver(ovxmod, m, 0)
+    w = s.get_node_w()
+    ref = oracle.node_w(m.nx, m.ny, m.nz, m.ds, m.mat, m.rho, m.dt)
+    assert np.array_equal(w, ref)
+
+
+def test_library_matrix_equals_oracle_matrix(ovxmod):
+    s = ovxmod.Ovx(0)
+    K8, _, _ = oracle.int_matrices()
+    assert np.array_equal(s.get_int8_matrix(), K8)
+
+
+@pytest.mark.parametrize("name,path", PATHS)
+@pytest.mark.parametrize("dims", [(1, 1, 1), (5, 4, 3), (40, 8, 70), (33, 2, 65)])
+def test_apply_K_bit_exact(ovxmod, name, path, dims):
+    m = wl.small_random(*dims, ds=0.01)
+    u = wl.random_field(m)
+    s = _solver(ovxmod, m, path)
+    f = s.apply_K(u)
+    ref = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u,
+                         path=oracle.PATH_INT8 if path == 0 else oracle.PATH_FP64)
+    assert np.array_equal(f, ref), np.abs(f - ref).max()
+
+
+def test_int8_element_records_bit_exact(ovxmod):
+    m = wl.small_random(9, 5, 4, ds=0.01)
+    rng = np.random.default_rng(7)
+    u = wl.random_field(m) * 10.0 ** rng.uniform(-20, 5, size=3 * m.n_nodes)
+    u[::97] = 0.0
+    s = _solver(ovxmod, m, 0)
+    rec = s.debug_element_ints(u, 0, m.n_elems)
+    K8, _, _ = oracle.int_matrices()
+    for e in range(m.n_elems):
+        nodes = oracle.element_nodes(m.nx, m.ny, e)
+        ue = np.concatenate([u[3 * n:3 * n + 3] for n in nodes])
+        mm = m.mat[e]
+        r = oracle.element_int8(ue, m.kappa[mm], m.G[mm], m.ds, 8, oracle.DIGITS_BYTES)
+        assert rec["s"][e] == r["s"]
+        assert np.array_equal(rec["v"][e], r["v"])
+        assert np.array_equal(rec["d"][e].astype(np.int32), r["d"])
+        assert np.array_equal(rec["C"][e].astype(np.int64), r["C"])
+        assert rec["y"][e] == r["y"]
+        assert np.array_equal(rec["fe"][e], r["fe"])
+
+
+def test_int8_edge_inputs(ovxmod):
+    m = wl.small_random(6, 4, 3, ds=0.01)
+    s = _solver(ovxmod, m, 0)
+    z = np.zeros(3 * m.n_nodes)
+    assert np.all(s.apply_K(z) == 0.0)
+    for scale in (1e-310, 1e-300, 1e-290, 1e300):
+        u = wl.random_field(m) * scale
+        ref = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=oracle.PATH_INT8)
+        assert np.array_equal(s.apply_K(u), ref), scale
+    # sign-aligned extremes (the worst case of the two-limb recombination)
+    u = np.sign(wl.random_field(m)) * 3.0
+    ref = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=oracle.PATH_INT8)
+    assert np.array_equal(s.apply_K(u), ref)
+
+
+@pytest.mark.parametrize("name,path", PATHS)
+def test_c1_trajectory_bit_exact(ovxmod, name, path):
+    """C1 (8³ concrete cube, Ricker source, 4 fixed corners), 100 steps."""
+    m = wl.c1_cube(8, steps=100)
+    z = np.zeros(3 * m.n_nodes)
+    s = _solver(ovxmod, m, path)
+    s.set_state(z, z, 0)
+    s.step(100)
+    u, up, it = s.get_state()
+    ru, rup, rit, st = oracle.run(m.as_dict(), z, z, 0, 100,
+                                  path=oracle.PATH_INT8 if path == 0 else oracle.PATH_FP64)
+    assert st == 0 and it == rit == 100
+    assert np.array_equal(u, ru) and np.array_equal(up, rup)
+    assert np.abs(u).max() > 0
+
+
+def test_1000_steps_int8_vs_fp64_oracle(ovxmod):
+    """BASELINE.json bar: INT8 path within 1e-10 rel-L2 of the FP64 oracle after 1000 steps
+    (heterogeneous, ragged grid, source, fixed corners); also bit-exact vs the INT8 oracle."""
+    m = wl.small_random(14, 9, 12, ds=1.0, dt=1e-4)
+    f0 = 25.0
+    wl.point_source(m, 7, 4, 12, 2, f0, 1.2 / f0, 1000, scale=1e6)
+    z = np.zeros(3 * m.n_nodes)
+    s = _solver(ovxmod, m, 0)
+    assert m.dt < s.critical_dt()
+    s.set_state(z, z, 0)
+    s.step(1000)
+    s.check_finite()
+    u, _, _ = s.get_state()
+    ref64, _, _, _ = oracle.run(m.as_dict(), z, z, 0, 1000, path=oracle.PATH_FP64)
+    ref8, _, _, _ = oracle.run(m.as_dict(), z, z, 0, 1000, path=oracle.PATH_INT8)
+    assert np.linalg.norm(u - ref64) <= 1e-10 * np.linalg.norm(ref64)
+    assert np.array_equal(u, ref8)
+
+
+def _node_force_oracle(m, u, ix, iy, iz, path):
+    """f at one node from the oracle's element forces, scattered in element order."""
+    f = np.zeros(3)
+    for dz in (-1, 0):
+        for dy in (-1, 0):
+            for dx in (-1, 0):
+                ex, ey, ez = ix + dx, iy + dy, iz + dz
+                if not (0 <= ex < m.nx and 0 <= ey < m.ny and 0 <= ez < m.nz):
+                    continue
+                e = ex + m.nx * (ey + m.ny * ez)
+                nodes = oracle.element_nodes(m.nx, m.ny, e)
+                ue = np.concatenate([u[3 * n:3 * n + 3] for n in nodes])
+                mm = m.mat[e]
+                fe = (oracle.element_int8(ue, m.kappa[mm], m.G[mm], m.ds)["fe"] if path == 0
+                      else oracle.element_fp64(ue, m.kappa[mm], m.G[mm], m.ds))
+                a = [0, 1, 3, 2, 4, 5, 7, 6][(1 if dx == 0 else 0) + 2 * (1 if dy == 0 else 0) + 4 * (1 if dz == 0 else 0)]
+                # local node a of element e is this node: corner sign + for dx = -1 (node is the +x corner)
+                a = {(1, 1, 1): 6, (0, 1, 1): 7, (1, 0, 1): 5, (0, 0, 1): 4,
+                     (1, 1, 0): 2, (0, 1, 0): 3, (1, 0, 0): 1, (0, 0, 0): 0}[(int(dx == -1), int(dy == -1), int(dz == -1))]
+                f = f + fe[3 * a:3 * a + 3]
+    return f
+
+
+@pytest.mark.parametrize("name,path", PATHS)
+def test_full_size_c2_sampled(ovxmod, name, path):
+    """C2 size (256³, the bench configuration, same launch): sampled nodes vs the oracle."""
+    import torch
+    m = wl.c2_block(256)
+    u = wl.random_field(m)
+    s = _solver(ovxmod, m, path)
+    ut = torch.from_numpy(u).cuda()
+    ft = torch.empty_like(ut)
+    s.apply_K_device(ut, ft)
+    s.sync()
+    f = ft.cpu().numpy()
+    rng = np.random.default_rng(13683)
+    pts = [(0, 0, 0), (256, 256, 256), (31, 3, 64), (30, 2, 63), (255, 1, 128)]
+    pts += [tuple(int(x) for x in rng.integers(0, 257, size=3)) for _ in range(40)]
+    for (ix, iy, iz) in pts:
+        n = ix + 257 * (iy + 257 * iz)
+        ref = _node_force_oracle(m, u, ix, iy, iz, path)
+        assert np.array_equal(f[3 * n:3 * n + 3], ref), (ix, iy, iz)
+
+
+def test_c2_plane_wave_dispersion_on_gpu(ovxmod):
+    """Physics at scale: axis-aligned standing P wave on a 128×32×32 roller box, 1000 steps,
+    against the closed-form lattice recurrence (property that holds at any size)."""
+    from oracle import physics
+    m = wl.c2_block(32)
+    m.nx, m.ny, m.nz = 128, 32, 32
+    m.mat = np.zeros(m.nx * m.ny * m.nz, np.uint8)
+    m.dirichlet = wl.roller_mask(m.nx, m.ny, m.nz)
+    u0 = wl.standing_wave(m, mvec=(16, 0, 0), U=(1.0, 0.0, 0.0))
+    k = math.pi * 16 / (m.nx * m.ds)
+    V = math.sqrt((m.kappa[0] + 4 * m.G[0] / 3) / m.rho[0])
+    lam = physics.lattice_lambda_axis(V, k, m.ds)
+    for path in (0, 1):
+        s = _solver(ovxmod, m, path)
+        s.set_state(u0, u0, 0)
+        s.step(1000)
+        u, _, _ = s.get_state()
+        a = physics.mode_amplitude(lam, m.dt, 1000)
+        assert np.abs(u - a * u0).max() <= 1e-10 * np.abs(u0).max()
