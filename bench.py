@@ -151,7 +151,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ovx", choices=["ovx", "reference"])
-    ap.add_argument("--path", default="int8", choices=["int8", "fp64"])
+    ap.add_argument("--path", default="int8", choices=["int8", "fp64", "fp64_dense"])
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -162,7 +162,7 @@ def main() -> None:
 
     import torch
     import torch.distributed as dist
-    from paper_2404_13683_b200 import Ovx, OVX_INT8, OVX_FP64
+    from paper_2404_13683_b200 import Ovx, OVX_INT8, OVX_FP64, OVX_FP64_DENSE
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -172,7 +172,7 @@ def main() -> None:
         dist.init_process_group("nccl")
 
     m, u0 = _workload(args.n)
-    path = OVX_INT8 if args.path == "int8" else OVX_FP64
+    path = {"int8": OVX_INT8, "fp64": OVX_FP64, "fp64_dense": OVX_FP64_DENSE}[args.path]
     stream = torch.cuda.Stream()
     s = Ovx(local)
     s.set_stream(stream)
@@ -244,7 +244,7 @@ def main() -> None:
     out = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if path == OVX_FP64 else "u8xs8->s32 + f64",
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32 + f64" if path == OVX_INT8 else "f64",
         "data": "synthetic (seeded; C2 roller box with a standing P wave)",
         "config": {"workload": f"C2: {args.n}^3 homogeneous block (kappa=5/3, G=1, rho=1, ds=1), rollers",
                    "path": args.path, "elements": E, "nodes": m.n_nodes,

@@ -53,7 +53,10 @@ enum {
 
 enum {
     OVX_INT8 = 0,       /* tcgen05 kind::i8 path: Eqs. 10-17 with byte slices (DESIGN.md variant B) */
-    OVX_FP64 = 1        /* FP64 CUDA-core reference: f_e = κ ds A_κ u_e + G ds A_G u_e */
+    OVX_FP64 = 1,       /* FP64 CUDA-core reference, factored form of Eq. 5 (Walsh-Hadamard of the
+                           corner values, ≈180 FP64 ops/element); equal to K_e^o u_e up to rounding */
+    OVX_FP64_DENSE = 2  /* FP64, literal dense form f_e = (κds/256)(K^κ u_e) + (Gds/384)((K̄^G+128I)u_e)
+                           with sequential sums: bit-identical to the oracle's FP64 definition */
 };
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -82,7 +85,7 @@ ovx_status ovx_set_dt(ovx_ctx *ctx, double dt);
 /* Derive K_e^INT8 on the host in exact rational arithmetic,
  * check that all 1152 entries are integers in [-128,127] (L110; else OVX_EINVAL),
  * build per-material constants and the per-node w = dt²/m (Eq. 6, m_n = Σ ρ_e ds³/8).
- * path: OVX_INT8 or OVX_FP64.  stages: M (only 8 is supported by the kernels). */
+ * path: OVX_INT8, OVX_FP64 or OVX_FP64_DENSE.  stages: M (only 8 is supported by the kernels). */
 ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages);
 /* Copy the library's derived K_e^INT8 (24x48 row-major) to host memory. */
 ovx_status ovx_get_int8_matrix(ovx_ctx *ctx, int8_t *out);

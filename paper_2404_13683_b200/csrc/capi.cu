@@ -267,7 +267,8 @@ ovx_status ovx_set_dt(ovx_ctx *ctx, double dt) {
 ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
     if (!ctx->have_grid || !ctx->have_emat) return fail(ctx, OVX_ESTATE, "set grid and element materials first");
-    if (path != OVX_INT8 && path != OVX_FP64) return fail(ctx, OVX_EINVAL, "path must be OVX_INT8 or OVX_FP64");
+    if (path != OVX_INT8 && path != OVX_FP64 && path != OVX_FP64_DENSE)
+        return fail(ctx, OVX_EINVAL, "path must be OVX_INT8, OVX_FP64 or OVX_FP64_DENSE");
     if (stages != 8) return fail(ctx, OVX_EINVAL, "only M = 8 stages is implemented");
     if (derive_element_matrices(ctx->k8, ctx->Ak, ctx->Ag) != 0)
         return fail(ctx, OVX_EINVAL, "K_e^INT8 derivation produced a non-INT8 entry (PAPER.md L110 violated)");
@@ -288,6 +289,14 @@ ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
         c.ck = k * ds / 256.0;
         c.cg = g * ds / 384.0;
         c.rho_vol8 = ctx->rho[m] * vol8;
+        const double lam = k - 2.0 * g / 3.0, s0 = ds / 16.0, s1 = s0 * 0.75, s2 = s1 * 0.75;
+        c.L0 = s0 * lam;
+        c.M0 = s0 * g;
+        c.M0x2 = 2.0 * c.M0;
+        c.L1 = s1 * lam;
+        c.M1 = s1 * g;
+        c.M1x3 = 3.0 * c.M1;
+        c.C2 = s2 * lam + 4.0 * (s2 * g);
     }
     ctx->path = path;
     ctx->stages = stages;
@@ -496,7 +505,7 @@ ovx_status ovx_debug_element_ints(ovx_ctx *ctx, const double *u, int64_t e0, int
     if (s) return s;
     // one device block for everything
     const size_t bs = 8 * ne, bv = 8 * ne * 48, bd = ne * 384, bC = 4 * ne * 192, by = 8 * ne * 24, bf = 8 * ne * 24;
-    const size_t bu = 8 * n3, total = bu * 2 + bs + bv + bd + bC + 2 * by + bf + 64 * 8;
+    const size_t bu = 8 * n3, total = bu * 2 + bs + bv + bd + bC + 2 * by + bf + 16 * 256;
     uint8_t *blk = nullptr;
     if (cudaMalloc(&blk, total) != cudaSuccess) {
         cudaGetLastError();

@@ -31,48 +31,61 @@ __constant__ int8_t c_K8[1152];
 
 namespace {
 
-constexpr int TX = 31, TY = 3;            // owned node columns per tile
-constexpr int EX = TX + 1, EY = TY + 1;   // element columns computed per layer
-constexpr int NE = EX * EY;               // 128 elements = MMA M
-constexpr int PX = TX + 2, PY = TY + 2;   // node columns of a u plane held in smem
-constexpr int NT = 128;                   // threads per CTA
-constexpr int PLANE_D = PX * PY * 3;      // doubles per u plane
-constexpr int NOWN = TX * TY;             // owned nodes per plane
-constexpr int FPL = NOWN * 3;             // doubles per force accumulation plane
+constexpr int EX = 32;                    // element columns per layer (x)
+constexpr int TX = EX - 1;                // owned node columns (x)
+constexpr int PX = TX + 2;                // node columns of a u plane held in smem (x)
+template <int EY> struct Tile {
+    static constexpr int TY = EY - 1;          // owned node rows (y)
+    static constexpr int NE = EX * EY;         // elements per layer = threads per CTA
+    static constexpr int PY = TY + 2;          // node rows of a u plane in smem
+    static constexpr int PLANE_D = PX * PY * 3;
+    static constexpr int NOWN = TX * TY;
+    static constexpr int FPL = NOWN * 3;
+};
+constexpr int EY_I8 = 4;                  // INT8 path: 128 elements = MMA M
+constexpr int EY_F64 = 8;                 // FP64 paths: 256 elements per layer
 constexpr int KB = 96;                    // K bytes per A row / B row (48 values × 2 bytes)
 constexpr int ROWGRP = 8 * KB;            // bytes per 8-row core-matrix group (6 chunks × 128)
-constexpr int A_BYTES = NE * KB;          // one half-word array
+constexpr int A_BYTES = 128 * KB;         // one half-word array (M = 128 rows)
 constexpr int B_ROWS = 48;                // N = 24 outputs × 2 byte positions
 constexpr int B_BYTES = B_ROWS * KB;
 constexpr int TMEM_COLS = 256;            // 4 accumulators of 48 columns at 64-column pitch
 constexpr uint32_t IDESC = ptx::idesc_i8(128, 48);
 
+template <int EY>
 struct SmemF64 {
-    double up[2][PLANE_D];
-    double fe[24][NE];
-    double facc[2][FPL];
+    using T = Tile<EY>;
+    double up[2][T::PLANE_D];
+    double fe[24][T::NE];
+    double facc[2][T::FPL];
 };
 
 struct SmemI8 {
+    using T = Tile<EY_I8>;
     alignas(1024) uint8_t A[4][A_BYTES];
     alignas(128) uint8_t B[B_BYTES];
-    double up[2][PLANE_D];
-    double fe[24][NE];
-    double facc[2][FPL];
-    double sig[NE];
-    int deg[NE];
+    double up[2][T::PLANE_D];
+    double fe[24][T::NE];
+    double facc[2][T::FPL];
+    double sig[T::NE];
+    int deg[T::NE];
     uint64_t mbar;
     uint32_t tmem;
 };
 
 template <int PATH>
-using Smem = typename std::conditional<PATH == OVX_INT8, SmemI8, SmemF64>::type;
+struct PathCfg {
+    static constexpr int EY = PATH == OVX_INT8 ? EY_I8 : EY_F64;
+    using T = Tile<EY>;
+    using Smem = typename std::conditional<PATH == OVX_INT8, SmemI8, SmemF64<EY>>::type;
+};
 
 // Load node plane iz of u (tile-local columns [X0-1, X0+TX] × [Y0-1, Y0+TY]) into smem.
+template <int EY>
 __device__ __forceinline__ void load_plane(double *dst, const double *__restrict__ u, const StepParams &p,
                                            int64_t X0, int64_t Y0, int64_t iz) {
     const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
-    for (int idx = threadIdx.x; idx < PLANE_D; idx += NT) {
+    for (int idx = threadIdx.x; idx < Tile<EY>::PLANE_D; idx += Tile<EY>::NE) {
         int py = idx / (PX * 3);
         int rem = idx - py * (PX * 3);
         int px = rem / 3, c = rem - px * 3;
@@ -84,6 +97,7 @@ __device__ __forceinline__ void load_plane(double *dst, const double *__restrict
 }
 
 // Gather u_e (local node order of reading Q1) of tile-local element (lx, ly) from the two planes.
+template <int PY>
 __device__ __forceinline__ void gather(double (&ue)[24], const double *lo, const double *hi, int lx, int ly) {
     const int cx[4] = {0, 1, 1, 0}, cy[4] = {0, 0, 1, 1};
 #pragma unroll
@@ -95,10 +109,94 @@ __device__ __forceinline__ void gather(double (&ue)[24], const double *lo, const
     }
 }
 
+// ---- factored FP64 element force (OVX_FP64) -----------------------------------
+// K_e^o u_e = Σ_β B_βᵀ c B_β u_e / g_β (Eq. 5) evaluated through the 3-D Walsh-Hadamard
+// transform of the corner values: with h_c[S] = Σ_α Π_{j∈S} r̄_j^α u_c^α, the mode-β strain is
+// (ds²/4)2^{-|β|} h_c[{i}∪β] (reading Q3), and f_c^α = Σ_S Π_{j∈S} r̄_j^α F_c[S] with
+// F_c[S] = (ds/16) Σ (3/4)^{|β|} τ_β[c][i].  ≈180 FP64 operations instead of 1152 FMAs;
+// equal to K_e^o u_e in exact arithmetic (rounding differs from the dense order).
+__device__ __forceinline__ void wht8(double (&v)[8]) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const int st = 1 << j;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if (!(b & st)) {
+                const double a = v[b], c = v[b | st];
+                v[b] = a + c;
+                v[b | st] = c - a;
+            }
+    }
+}
+__device__ __forceinline__ void iwht8(double (&v)[8]) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const int st = 1 << j;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if (!(b & st)) {
+                const double a = v[b], c = v[b | st];
+                v[b] = a - c;
+                v[b | st] = a + c;
+            }
+    }
+}
+__device__ __forceinline__ void element_force_wht(const double (&ue)[24], const MatConst &m, double (&fe)[24]) {
+    constexpr int BORD[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // local node -> bit index x | y<<1 | z<<2
+    double h[3][8];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) h[c][BORD[a]] = ue[3 * a + c];
+        wht8(h[c]);
+    }
+    double F[3][8];
+    F[0][0] = F[1][0] = F[2][0] = 0.0;
+    // β = ∅ : full gradient h_c[{i}]
+    const double lt0 = m.L0 * (h[0][1] + h[1][2] + h[2][4]);
+    F[0][1] = fma(m.M0x2, h[0][1], lt0);
+    F[1][2] = fma(m.M0x2, h[1][2], lt0);
+    F[2][4] = fma(m.M0x2, h[2][4], lt0);
+    const double sxy = m.M0 * (h[0][2] + h[1][1]);
+    const double syz = m.M0 * (h[1][4] + h[2][2]);
+    const double szx = m.M0 * (h[2][1] + h[0][4]);
+    F[0][2] = sxy; F[1][1] = sxy;
+    F[1][4] = syz; F[2][2] = syz;
+    F[2][1] = szx; F[0][4] = szx;
+    // |β| = 1
+    const double ltx = m.L1 * (h[1][3] + h[2][5]);
+    const double lty = m.L1 * (h[0][3] + h[2][6]);
+    const double ltz = m.L1 * (h[0][5] + h[1][6]);
+    F[0][3] = fma(m.M1x3, h[0][3], lty);
+    F[1][3] = fma(m.M1x3, h[1][3], ltx);
+    F[0][5] = fma(m.M1x3, h[0][5], ltz);
+    F[2][5] = fma(m.M1x3, h[2][5], ltx);
+    F[1][6] = fma(m.M1x3, h[1][6], ltz);
+    F[2][6] = fma(m.M1x3, h[2][6], lty);
+    const double pp = h[2][3], qq = h[1][5], rr = h[0][6], tt = pp + qq + rr;
+    F[2][3] = m.M1 * (tt + pp);
+    F[1][5] = m.M1 * (tt + qq);
+    F[0][6] = m.M1 * (tt + rr);
+    // |β| = 2
+    F[0][7] = m.C2 * h[0][7];
+    F[1][7] = m.C2 * h[1][7];
+    F[2][7] = m.C2 * h[2][7];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        iwht8(F[c]);
+#pragma unroll
+        for (int a = 0; a < 8; ++a) fe[3 * a + c] = F[c][BORD[a]];
+    }
+}
+
 template <int PATH, int MODE>
-__global__ void __launch_bounds__(NT) step_kernel(const StepParams p) {
+__global__ void __launch_bounds__(PathCfg<PATH>::T::NE) step_kernel(const StepParams p) {
+    using Cfg = PathCfg<PATH>;
+    using T = typename Cfg::T;
+    constexpr int EY = Cfg::EY;
+    constexpr int NT = T::NE, TY = T::TY, PY = T::PY, NOWN = T::NOWN, FPL = T::FPL;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    Smem<PATH> &S = *reinterpret_cast<Smem<PATH> *>(smem_raw);
+    typename Cfg::Smem &S = *reinterpret_cast<typename Cfg::Smem *>(smem_raw);
     const int t = threadIdx.x;
     const int warp = t >> 5;
 
@@ -139,8 +237,8 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepParams p) {
     for (int64_t L = Z0 - 1; L < Z1; ++L) {
         const bool layer_ok = (L >= 0 && L < p.nz);
         if (layer_ok) {
-            if (L == Lfirst) load_plane(S.up[L & 1], p.u, p, X0, Y0, L);
-            load_plane(S.up[(L + 1) & 1], p.u, p, X0, Y0, L + 1);
+            if (L == Lfirst) load_plane<EY>(S.up[L & 1], p.u, p, X0, Y0, L);
+            load_plane<EY>(S.up[(L + 1) & 1], p.u, p, X0, Y0, L + 1);
             __syncthreads();
             const double *plo = S.up[L & 1], *phi = S.up[(L + 1) & 1];
             const int m = ein ? (int)__ldg(p.mat + ex + p.nx * (ey + p.ny * L)) : 0;
@@ -150,8 +248,17 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepParams p) {
             const bool dbg = dbg_w && dj >= 0 && dj < p.dbg_ne;
 
             if constexpr (PATH == OVX_FP64) {
+                double ue[24], fe[24];
+                gather<PY>(ue, plo, phi, lx, ly);
+                element_force_wht(ue, c_mat[m], fe);
+#pragma unroll
+                for (int r = 0; r < 24; ++r) {
+                    S.fe[r][t] = ein ? fe[r] : 0.0;
+                    if (MODE == MODE_DEBUG && dbg && p.dbg_fe) p.dbg_fe[dj * 24 + r] = fe[r];
+                }
+            } else if constexpr (PATH == OVX_FP64_DENSE) {
                 double ue[24];
-                gather(ue, plo, phi, lx, ly);
+                gather<PY>(ue, plo, phi, lx, ly);
                 const double ck = c_mat[m].ck, cg = c_mat[m].cg;
 #pragma unroll 1
                 for (int r = 0; r < 24; ++r) {
@@ -168,7 +275,7 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepParams p) {
             } else {
                 // ---- Eqs. 10-16 on CUDA cores: scale, INT64 image, byte slices -> A operand ----
                 double ue[24];
-                gather(ue, plo, phi, lx, ly);
+                gather<PY>(ue, plo, phi, lx, ly);
                 const double cG = c_mat[m].cG;
                 double amax = 0.0;
 #pragma unroll
@@ -177,7 +284,7 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepParams p) {
                 const double s = fmax(amax, __dmul_rn(cG, amax));
                 const bool deg = !ein || !(s >= 0x1p-1022) || isinf(s);
                 const bool fast = s >= 0x1p-960;
-                const double r = 1.0 / s;                       // RN(1/s_e), reading Q7
+                const double r = 1.0 / s;                          // RN(1/s_e), reading Q7
                 const double R = fast ? __dmul_rn(r, 0x1p56) : r;  // exact power-of-two scaling
 #pragma unroll
                 for (int ch = 0; ch < 6; ++ch) {
@@ -187,7 +294,7 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepParams p) {
                         const int k = ch * 8 + q;
                         const double ub = k < 24 ? ue[k] : __dmul_rn(cG, ue[k - 24]);
                         const double tt = fast ? __dmul_rn(ub, R) : __dmul_rn(__dmul_rn(ub, r), 0x1p56);
-                        const long long v = deg ? 0ll : __double2ll_rz(tt);   // truncation toward 0 (Q8)
+                        const long long v = deg ? 0ll : __double2ll_rz(tt);  // truncation toward 0 (Q8)
                         const unsigned long long vp = (unsigned long long)v + (1ull << 56);
                         lo[q] = (uint32_t)vp;
                         hi[q] = (uint32_t)(vp >> 32);
@@ -198,7 +305,7 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepParams p) {
                                 for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = (uint8_t)(vp >> (8 * j));
                         }
                     }
-                    // half-word arrays: array p holds bytes (2p, 2p+1) of v' for every k
+                    // half-word arrays: array pa holds bytes (2pa, 2pa+1) of v' for every k
                     const uint32_t off = (uint32_t)((t >> 3) * ROWGRP + ch * 128 + (t & 7) * 16);
 #pragma unroll
                     for (int pa = 0; pa < 4; ++pa) {
@@ -269,7 +376,6 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepParams p) {
                             if (p.dbg_C)
 #pragma unroll
                                 for (int j = 0; j < 8; ++j) p.dbg_C[dj * 192 + j * 24 + i] = C[j];
-                            // y as int128: hi*2^32 + lo
                             __int128 y = (__int128)hi * ((__int128)1 << 32) + (__int128)lo;
                             if (p.dbg_yhi) p.dbg_yhi[dj * 24 + i] = (long long)(y >> 64);
                             if (p.dbg_ylo) p.dbg_ylo[dj * 24 + i] = (long long)(unsigned long long)y;
@@ -354,14 +460,21 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepParams p) {
 template <int PATH, int MODE>
 cudaError_t launch_t(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
-    const int smem = (int)sizeof(Smem<PATH>);
+    const int smem = (int)sizeof(typename PathCfg<PATH>::Smem);
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(step_kernel<PATH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_kernel<PATH, MODE><<<(unsigned)ctas, NT, smem, st>>>(p);
+    step_kernel<PATH, MODE><<<(unsigned)ctas, PathCfg<PATH>::T::NE, smem, st>>>(p);
     return cudaGetLastError();
+}
+
+template <int PATH>
+cudaError_t launch_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
+    if (mode == MODE_STEP) return launch_t<PATH, MODE_STEP>(p, ctas, st);
+    if (mode == MODE_APPLY) return launch_t<PATH, MODE_APPLY>(p, ctas, st);
+    return launch_t<PATH, MODE_DEBUG>(p, ctas, st);
 }
 
 __global__ void node_w_kernel(int64_t nx, int64_t ny, int64_t nz, const uint8_t *__restrict__ mat, double dt,
@@ -387,6 +500,20 @@ __global__ void finite_kernel(const double *__restrict__ u, int64_t n, int *flag
         if (!isfinite(u[i])) *flag = 1;
 }
 
+constexpr int kZChunk = 64;
+
+template <int PATH>
+LaunchInfo info_t(int64_t nx, int64_t ny, int64_t nz) {
+    using T = typename PathCfg<PATH>::T;
+    LaunchInfo li;
+    const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + T::TY - 1) / T::TY;
+    const int64_t tz = (nz + 1 + kZChunk - 1) / kZChunk;
+    li.ctas = tx * ty * tz;
+    li.threads = T::NE;
+    li.smem = (int)sizeof(typename PathCfg<PATH>::Smem);
+    return li;
+}
+
 }  // namespace
 
 cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, const double *kk, const double *kg,
@@ -400,30 +527,21 @@ cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, c
 }
 
 LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
-    LaunchInfo li;
-    const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + TY - 1) / TY;
-    const int64_t zchunk = 64;
-    const int64_t tz = (nz + 1 + zchunk - 1) / zchunk;
-    li.ctas = tx * ty * tz;
-    li.threads = NT;
-    li.smem = path == OVX_INT8 ? (int)sizeof(SmemI8) : (int)sizeof(SmemF64);
-    return li;
+    if (path == OVX_INT8) return info_t<OVX_INT8>(nx, ny, nz);
+    if (path == OVX_FP64) return info_t<OVX_FP64>(nx, ny, nz);
+    return info_t<OVX_FP64_DENSE>(nx, ny, nz);
 }
 
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
+    const int ty = path == OVX_INT8 ? Tile<EY_I8>::TY : Tile<EY_F64>::TY;
     p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
-    p.tiles_y = (int)((p.ny + 1 + TY - 1) / TY);
-    p.zchunk = 64;
+    p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
+    p.zchunk = kZChunk;
     const int64_t tz = (p.nz + 1 + p.zchunk - 1) / p.zchunk;
     const int64_t ctas = (int64_t)p.tiles_x * p.tiles_y * tz;
-    if (path == OVX_INT8) {
-        if (mode == MODE_STEP) return launch_t<OVX_INT8, MODE_STEP>(p, ctas, st);
-        if (mode == MODE_APPLY) return launch_t<OVX_INT8, MODE_APPLY>(p, ctas, st);
-        return launch_t<OVX_INT8, MODE_DEBUG>(p, ctas, st);
-    }
-    if (mode == MODE_STEP) return launch_t<OVX_FP64, MODE_STEP>(p, ctas, st);
-    if (mode == MODE_APPLY) return launch_t<OVX_FP64, MODE_APPLY>(p, ctas, st);
-    return launch_t<OVX_FP64, MODE_DEBUG>(p, ctas, st);
+    if (path == OVX_INT8) return launch_mode<OVX_INT8>(mode, p, ctas, st);
+    if (path == OVX_FP64) return launch_mode<OVX_FP64>(mode, p, ctas, st);
+    return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);
 }
 
 cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, double dt, double *w,

@@ -12,8 +12,10 @@ constexpr int kMaxSrc = 16;
 // oracle's definition fixes (DESIGN.md §Integer path):
 //   cG = (2G)/(3κ)   c1 = κ ds/256   c2 = (256G)/(3κ)     (Eq. 9)
 //   ck = κ ds/256    cg = G ds/384                           (FP64 path: κ ds A_κ + G ds A_G)
+//   L0..C2: factored FP64 path, (ds/16)(3/4)^k λ and μ, λ = κ − 2G/3, μ = G
 struct MatConst {
     double cG, c1, c2, ck, cg, rho_vol8;
+    double L0, M0, M0x2, L1, M1, M1x3, C2;
 };
 
 enum Mode { MODE_STEP = 0, MODE_APPLY = 1, MODE_DEBUG = 2 };

@@ -33,7 +33,15 @@ def _solver(ovxmod, m, path):
     return s
 
 
-PATHS = [("int8", 0), ("fp64", 1)]
+PATHS = [("int8", 0), ("fp64", 1), ("fp64_dense", 2)]
+EXACT = {0: True, 1: False, 2: True}          # factored FP64 differs from the dense order by rounding
+ORACLE_PATH = {0: oracle.PATH_INT8, 1: oracle.PATH_FP64, 2: oracle.PATH_FP64}
+
+
+def _close(a, ref, path, rel=1e-13):
+    if EXACT[path]:
+        return np.array_equal(a, ref)
+    return np.linalg.norm(a - ref) <= rel * np.linalg.norm(ref)
 
 
 def _ragged():
@@ -63,9 +71,12 @@ def test_apply_K_bit_exact(ovxmod, name, path, dims):
     u = wl.random_field(m)
     s = _solver(ovxmod, m, path)
     f = s.apply_K(u)
-    ref = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u,
-                         path=oracle.PATH_INT8 if path == 0 else oracle.PATH_FP64)
-    assert np.array_equal(f, ref), np.abs(f - ref).max()
+    ref = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=ORACLE_PATH[path])
+    assert _close(f, ref, path), np.abs(f - ref).max()
+    if not EXACT[path]:   # per-node bound: a few ulps of the node's |K||u| scale
+        scale = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, np.abs(m.kappa), np.abs(m.G), np.abs(u),
+                               path=oracle.PATH_FP64)
+        assert np.all(np.abs(f - ref) <= 64 * 2.0 ** -52 * np.abs(scale) + 1e-300)
 
 
 def test_int8_element_records_bit_exact(ovxmod):
@@ -113,10 +124,9 @@ def test_c1_trajectory_bit_exact(ovxmod, name, path):
     s.set_state(z, z, 0)
     s.step(100)
     u, up, it = s.get_state()
-    ru, rup, rit, st = oracle.run(m.as_dict(), z, z, 0, 100,
-                                  path=oracle.PATH_INT8 if path == 0 else oracle.PATH_FP64)
+    ru, rup, rit, st = oracle.run(m.as_dict(), z, z, 0, 100, path=ORACLE_PATH[path])
     assert st == 0 and it == rit == 100
-    assert np.array_equal(u, ru) and np.array_equal(up, rup)
+    assert _close(u, ru, path, 1e-12) and _close(up, rup, path, 1e-12)
     assert np.abs(u).max() > 0
 
 
@@ -137,6 +147,11 @@ def test_1000_steps_int8_vs_fp64_oracle(ovxmod):
     ref8, _, _, _ = oracle.run(m.as_dict(), z, z, 0, 1000, path=oracle.PATH_INT8)
     assert np.linalg.norm(u - ref64) <= 1e-10 * np.linalg.norm(ref64)
     assert np.array_equal(u, ref8)
+    s64 = _solver(ovxmod, m, 1)
+    s64.set_state(z, z, 0)
+    s64.step(1000)
+    u64, _, _ = s64.get_state()
+    assert np.linalg.norm(u64 - ref64) <= 1e-10 * np.linalg.norm(ref64)
 
 
 def _node_force_oracle(m, u, ix, iy, iz, path):
@@ -154,7 +169,6 @@ def _node_force_oracle(m, u, ix, iy, iz, path):
                 mm = m.mat[e]
                 fe = (oracle.element_int8(ue, m.kappa[mm], m.G[mm], m.ds)["fe"] if path == 0
                       else oracle.element_fp64(ue, m.kappa[mm], m.G[mm], m.ds))
-                a = [0, 1, 3, 2, 4, 5, 7, 6][(1 if dx == 0 else 0) + 2 * (1 if dy == 0 else 0) + 4 * (1 if dz == 0 else 0)]
                 # local node a of element e is this node: corner sign + for dx = -1 (node is the +x corner)
                 a = {(1, 1, 1): 6, (0, 1, 1): 7, (1, 0, 1): 5, (0, 0, 1): 4,
                      (1, 1, 0): 2, (0, 1, 0): 3, (1, 0, 0): 1, (0, 0, 0): 0}[(int(dx == -1), int(dy == -1), int(dz == -1))]
@@ -180,7 +194,10 @@ def test_full_size_c2_sampled(ovxmod, name, path):
     for (ix, iy, iz) in pts:
         n = ix + 257 * (iy + 257 * iz)
         ref = _node_force_oracle(m, u, ix, iy, iz, path)
-        assert np.array_equal(f[3 * n:3 * n + 3], ref), (ix, iy, iz)
+        if EXACT[path]:
+            assert np.array_equal(f[3 * n:3 * n + 3], ref), (ix, iy, iz)
+        else:
+            assert np.abs(f[3 * n:3 * n + 3] - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max()), (ix, iy, iz)
 
 
 def test_c2_plane_wave_dispersion_on_gpu(ovxmod):
@@ -195,7 +212,7 @@ def test_c2_plane_wave_dispersion_on_gpu(ovxmod):
     k = math.pi * 16 / (m.nx * m.ds)
     V = math.sqrt((m.kappa[0] + 4 * m.G[0] / 3) / m.rho[0])
     lam = physics.lattice_lambda_axis(V, k, m.ds)
-    for path in (0, 1):
+    for path in (0, 1, 2):
         s = _solver(ovxmod, m, path)
         s.set_state(u0, u0, 0)
         s.step(1000)

@@ -23,11 +23,11 @@ __global__ void kern(const double *in, unsigned long long *out, long long *cyc) 
     long long t0 = clock64();
     for (int it = 0; it < ITERS; ++it) {
         if (OP == 0) {  // F2I.S64.F64.TRUNC
-#define S(i) asm volatile("cvt.rzi.s64.f64 %0, %1;" : "=l"(l[i]) : "d"(d[i]));
+#define S(i) asm volatile("cvt.rzi.s64.f64 %0, %1;\n\tcvt.rn.f64.s64 %1, %0;" : "=l"(l[i]), "+d"(d[i]));
             BODY8(S)
 #undef S
         } else if (OP == 1) {  // I2F.F64.S64
-#define S(i) asm volatile("cvt.rn.f64.s64 %0, %1;" : "=d"(d[i]) : "l"(l[i]));
+#define S(i) asm volatile("cvt.rn.f64.s64 %0, %1;\n\tadd.s64 %1, %1, 1;" : "=d"(d[i]), "+l"(l[i]));
             BODY8(S)
 #undef S
         } else if (OP == 2) {  // PRMT
@@ -47,7 +47,7 @@ __global__ void kern(const double *in, unsigned long long *out, long long *cyc) 
             BODY8(S)
 #undef S
         } else if (OP == 6) {  // I2F.F64.S32
-#define S(i) asm volatile("cvt.rn.f64.s32 %0, %1;" : "=d"(d[i]) : "r"(u[i]));
+#define S(i) asm volatile("cvt.rn.f64.s32 %0, %1;\n\tcvt.rzi.s32.f64 %1, %0;" : "=d"(d[i]), "+r"(u[i]));
             BODY8(S)
 #undef S
         } else if (OP == 7) {  // FP64 max (fmax)
@@ -91,13 +91,13 @@ int main() {
     cudaMemcpy(in, h, sizeof h, cudaMemcpyHostToDevice);
     cudaMalloc(&out, sizeof(unsigned long long) * sms * 1024);
     cudaMalloc(&cyc, sizeof(long long) * sms);
-    run<0>("F2I.S64.F64", in, out, cyc, sms);
-    run<1>("I2F.F64.S64", in, out, cyc, sms);
+    run<0>("F2I.S64.F64+I2F.F64.S64 pair", in, out, cyc, sms);
+    run<1>("I2F.F64.S64+IADD64", in, out, cyc, sms);
     run<2>("PRMT", in, out, cyc, sms);
     run<3>("DFMA", in, out, cyc, sms);
     run<4>("IMAD.WIDE", in, out, cyc, sms);
     run<5>("IADD", in, out, cyc, sms);
-    run<6>("I2F.F64.S32", in, out, cyc, sms);
+    run<6>("I2F.F64.S32+F2I.S32.F64 pair", in, out, cyc, sms);
     run<7>("DMNMX(max.f64)", in, out, cyc, sms);
     printf("{\"sms\": %d}\n", sms);
     return 0;
