@@ -189,284 +189,18 @@ __device__ __forceinline__ void element_force_wht(const double (&ue)[24], const 
     }
 }
 
-template <int PATH, int MODE>
-__global__ void __launch_bounds__(PathCfg<PATH>::T::NE) step_kernel(const StepParams p) {
-    using Cfg = PathCfg<PATH>;
-    using T = typename Cfg::T;
-    constexpr int EY = Cfg::EY;
-    constexpr int NT = T::NE, TY = T::TY, PY = T::PY, NOWN = T::NOWN, FPL = T::FPL;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    typename Cfg::Smem &S = *reinterpret_cast<typename Cfg::Smem *>(smem_raw);
-    const int t = threadIdx.x;
-    const int warp = t >> 5;
-
-    int bid = blockIdx.x;
-    const int tx = bid % p.tiles_x;
-    bid /= p.tiles_x;
-    const int ty = bid % p.tiles_y;
-    const int tz = bid / p.tiles_y;
-    const int64_t X0 = (int64_t)tx * TX, Y0 = (int64_t)ty * TY;
-    const int64_t Z0 = (int64_t)tz * p.zchunk;
-    const int64_t Z1 = min(Z0 + (int64_t)p.zchunk, p.nz + 1);
-    const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
-
-    const int lx = t % EX, ly = t / EX;
-    const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
-    const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
-
-    uint32_t phase = 0;
-    if constexpr (PATH == OVX_INT8) {
-        // Resident B operand: B[n = 2i+b'][kb = 2k+b] = K_e^INT8[i][k]·δ(b,b'), K-major core matrices.
-        for (int idx = t; idx < B_BYTES; idx += NT) {
-            int grp = idx / ROWGRP, rem = idx - grp * ROWGRP;
-            int chunk = rem >> 7;
-            rem &= 127;
-            int n = grp * 8 + (rem >> 4), kb = chunk * 16 + (rem & 15);
-            S.B[idx] = ((kb & 1) == (n & 1)) ? (uint8_t)c_K8[(n >> 1) * 48 + (kb >> 1)] : (uint8_t)0;
-        }
-        if (warp == 0) ptx::tmem_alloc<TMEM_COLS>(&S.tmem);
-        if (t == 0) ptx::mbar_init(&S.mbar, 1);
-        ptx::fence_proxy_async_smem();
-        ptx::tc_fence_before();
-    }
-    for (int i = t; i < 2 * FPL; i += NT) (&S.facc[0][0])[i] = 0.0;
-    __syncthreads();
-    if constexpr (PATH == OVX_INT8) ptx::tc_fence_after();
-
-    const int64_t Lfirst = max(Z0 - 1, (int64_t)0);
-    for (int64_t L = Z0 - 1; L < Z1; ++L) {
-        const bool layer_ok = (L >= 0 && L < p.nz);
-        if (layer_ok) {
-            if (L == Lfirst) load_plane<EY>(S.up[L & 1], p.u, p, X0, Y0, L);
-            load_plane<EY>(S.up[(L + 1) & 1], p.u, p, X0, Y0, L + 1);
-            __syncthreads();
-            const double *plo = S.up[L & 1], *phi = S.up[(L + 1) & 1];
-            const int m = ein ? (int)__ldg(p.mat + ex + p.nx * (ey + p.ny * L)) : 0;
-            const bool dbg_w = (MODE == MODE_DEBUG) && ein && lx < TX && ly < TY && (L + 1 >= Z0) && (L + 1 < Z1);
-            const int64_t eid = ex + p.nx * (ey + p.ny * L);
-            const int64_t dj = eid - p.dbg_e0;
-            const bool dbg = dbg_w && dj >= 0 && dj < p.dbg_ne;
-
-            if constexpr (PATH == OVX_FP64) {
-                double ue[24], fe[24];
-                gather<PY>(ue, plo, phi, lx, ly);
-                element_force_wht(ue, c_mat[m], fe);
-#pragma unroll
-                for (int r = 0; r < 24; ++r) {
-                    S.fe[r][t] = ein ? fe[r] : 0.0;
-                    if (MODE == MODE_DEBUG && dbg && p.dbg_fe) p.dbg_fe[dj * 24 + r] = fe[r];
-                }
-            } else if constexpr (PATH == OVX_FP64_DENSE) {
-                double ue[24];
-                gather<PY>(ue, plo, phi, lx, ly);
-                const double ck = c_mat[m].ck, cg = c_mat[m].cg;
-#pragma unroll 1
-                for (int r = 0; r < 24; ++r) {
-                    double a = 0.0, b = 0.0;
-#pragma unroll
-                    for (int c = 0; c < 24; ++c) {
-                        a = __dadd_rn(a, __dmul_rn(c_Kk[r * 24 + c], ue[c]));
-                        b = __dadd_rn(b, __dmul_rn(c_Kg[r * 24 + c], ue[c]));
-                    }
-                    double f = __dadd_rn(__dmul_rn(ck, a), __dmul_rn(cg, b));
-                    S.fe[r][t] = ein ? f : 0.0;
-                    if (MODE == MODE_DEBUG && dbg && p.dbg_fe) p.dbg_fe[dj * 24 + r] = f;
-                }
-            } else {
-                // ---- Eqs. 10-16 on CUDA cores: scale, INT64 image, byte slices -> A operand ----
-                double ue[24];
-                gather<PY>(ue, plo, phi, lx, ly);
-                const double cG = c_mat[m].cG;
-                double amax = 0.0;
-#pragma unroll
-                for (int i = 0; i < 24; ++i) amax = fmax(amax, fabs(ue[i]));
-                // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)  (RN is monotone, cG > 0)
-                const double s = fmax(amax, __dmul_rn(cG, amax));
-                const bool deg = !ein || !(s >= 0x1p-1022) || isinf(s);
-                const bool fast = s >= 0x1p-960;
-                const double r = 1.0 / s;                          // RN(1/s_e), reading Q7
-                const double R = fast ? __dmul_rn(r, 0x1p56) : r;  // exact power-of-two scaling
-#pragma unroll
-                for (int ch = 0; ch < 6; ++ch) {
-                    uint32_t lo[8], hi[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int k = ch * 8 + q;
-                        const double ub = k < 24 ? ue[k] : __dmul_rn(cG, ue[k - 24]);
-                        const double tt = fast ? __dmul_rn(ub, R) : __dmul_rn(__dmul_rn(ub, r), 0x1p56);
-                        const long long v = deg ? 0ll : __double2ll_rz(tt);  // truncation toward 0 (Q8)
-                        const unsigned long long vp = (unsigned long long)v + (1ull << 56);
-                        lo[q] = (uint32_t)vp;
-                        hi[q] = (uint32_t)(vp >> 32);
-                        if (MODE == MODE_DEBUG && dbg) {
-                            if (p.dbg_v) p.dbg_v[dj * 48 + k] = v;
-                            if (p.dbg_d)
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = (uint8_t)(vp >> (8 * j));
-                        }
-                    }
-                    // half-word arrays: array pa holds bytes (2pa, 2pa+1) of v' for every k
-                    const uint32_t off = (uint32_t)((t >> 3) * ROWGRP + ch * 128 + (t & 7) * 16);
-#pragma unroll
-                    for (int pa = 0; pa < 4; ++pa) {
-                        const uint32_t *src = pa < 2 ? lo : hi;
-                        const uint32_t sel = (pa & 1) ? 0x7632u : 0x5410u;
-                        uint4 wv;
-                        wv.x = __byte_perm(src[0], src[1], sel);
-                        wv.y = __byte_perm(src[2], src[3], sel);
-                        wv.z = __byte_perm(src[4], src[5], sel);
-                        wv.w = __byte_perm(src[6], src[7], sel);
-                        *reinterpret_cast<uint4 *>(&S.A[pa][off]) = wv;
-                    }
-                }
-                S.sig[t] = __dmul_rn(s, 0x1p-56);
-                S.deg[t] = deg;
-#pragma unroll
-                for (int i = 0; i < 24; ++i) S.fe[i][t] = ue[i];  // parked for the epilogue (c2·u_e)
-                if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
-
-                // ---- Eq. 17 on tensor cores: 4 arrays × 3 K-steps of M128 N48 K32 ----
-                ptx::fence_proxy_async_smem();
-                __syncthreads();
-                if (t == 0) {
-                    ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(&S.A[0][0]), b0 = ptx::smem_u32(&S.B[0]);
-#pragma unroll
-                    for (int pa = 0; pa < 4; ++pa)
-#pragma unroll
-                        for (int ks = 0; ks < 3; ++ks) {
-                            uint64_t ad = ptx::smem_desc(a0 + pa * A_BYTES + ks * 256, 128, ROWGRP);
-                            uint64_t bd = ptx::smem_desc(b0 + ks * 256, 128, ROWGRP);
-                            ptx::mma_i8(S.tmem + pa * 64, ad, bd, IDESC, ks > 0 ? 1u : 0u);
-                        }
-                    ptx::mma_commit(&S.mbar);
-                }
-                ptx::mbar_wait(&S.mbar, phase);
-                phase ^= 1;
-                ptx::tc_fence_after();
-
-                // ---- epilogue: exact recombination + Eq. 9 scalars ----
-                const double c1 = c_mat[m].c1, c2 = c_mat[m].c2;
-                const double sig = S.sig[t];
-                const uint32_t tbase = S.tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-                for (int cc = 0; cc < 3; ++cc) {
-                    uint32_t R0[16], R1[16], R2[16], R3[16];
-                    ptx::tmem_ld16(tbase + 0 + cc * 16, R0);
-                    ptx::tmem_ld16(tbase + 64 + cc * 16, R1);
-                    ptx::tmem_ld16(tbase + 128 + cc * 16, R2);
-                    ptx::tmem_ld16(tbase + 192 + cc * 16, R3);
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int i = cc * 8 + q;
-                        const int32_t C[8] = {(int32_t)R0[2 * q], (int32_t)R0[2 * q + 1], (int32_t)R1[2 * q],
-                                              (int32_t)R1[2 * q + 1], (int32_t)R2[2 * q], (int32_t)R2[2 * q + 1],
-                                              (int32_t)R3[2 * q], (int32_t)R3[2 * q + 1]};
-                        const int32_t L0 = C[0] + 256 * C[1], L1 = C[2] + 256 * C[3];
-                        const int32_t L2 = C[4] + 256 * C[5], L3 = C[6] + 256 * C[7];
-                        // y = Σ_j 256^j C'_j + 2^63 = lo + 2^32 hi  (K_e^INT8·1 = −128 per row)
-                        const long long lo = (long long)L0 + (long long)L1 * 65536ll;
-                        const long long hi = (long long)L2 + (long long)L3 * 65536ll + (1ll << 31);
-                        const double Y = __fma_rn(__ll2double_rn(hi), 0x1p32, __ll2double_rn(lo));  // RN(y)
-                        const double f = __dmul_rn(c1, __dadd_rn(__dmul_rn(Y, sig), __dmul_rn(c2, S.fe[i][t])));
-                        const bool dg = S.deg[t];
-                        S.fe[i][t] = dg ? 0.0 : f;
-                        if (MODE == MODE_DEBUG && dbg) {
-                            if (p.dbg_C)
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) p.dbg_C[dj * 192 + j * 24 + i] = C[j];
-                            __int128 y = (__int128)hi * ((__int128)1 << 32) + (__int128)lo;
-                            if (p.dbg_yhi) p.dbg_yhi[dj * 24 + i] = (long long)(y >> 64);
-                            if (p.dbg_ylo) p.dbg_ylo[dj * 24 + i] = (long long)(unsigned long long)y;
-                            if (p.dbg_fe) p.dbg_fe[dj * 24 + i] = dg ? 0.0 : f;
-                        }
-                    }
-                }
-                ptx::tc_fence_before();
-            }
-            __syncthreads();
-
-            // ---- scatter in global element order into the two force planes ----
-            if (t < NOWN) {
-                const int nxl = t % TX, nyl = t / TX;
-                const int e00 = nxl + EX * nyl, e10 = e00 + 1, e01 = e00 + EX, e11 = e01 + 1;
-                if (L >= Z0) {  // bottom corners of layer L -> plane L
-                    double *fa = &S.facc[L & 1][t * 3];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        double f = fa[c];
-                        f = __dadd_rn(f, S.fe[3 * 2 + c][e00]);
-                        f = __dadd_rn(f, S.fe[3 * 3 + c][e10]);
-                        f = __dadd_rn(f, S.fe[3 * 1 + c][e01]);
-                        f = __dadd_rn(f, S.fe[3 * 0 + c][e11]);
-                        fa[c] = f;
-                    }
-                }
-                if (L + 1 < Z1) {  // top corners of layer L -> plane L+1
-                    double *fa = &S.facc[(L + 1) & 1][t * 3];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        double f = fa[c];
-                        f = __dadd_rn(f, S.fe[3 * 6 + c][e00]);
-                        f = __dadd_rn(f, S.fe[3 * 7 + c][e10]);
-                        f = __dadd_rn(f, S.fe[3 * 5 + c][e01]);
-                        f = __dadd_rn(f, S.fe[3 * 4 + c][e11]);
-                        fa[c] = f;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        // ---- plane L is complete: update (or emit f) ----
-        if (L >= Z0 && L <= p.nz) {
-            if (t < NOWN) {
-                const int nxl = t % TX, nyl = t / TX;
-                const int64_t ix = X0 + nxl, iy = Y0 + nyl;
-                double *fa = &S.facc[L & 1][t * 3];
-                if (ix < NX1 && iy < NY1) {
-                    const int64_t n = ix + NX1 * (iy + NY1 * L);
-                    const double *up = &S.up[L & 1][((nyl + 1) * PX + (nxl + 1)) * 3];
-                    if (MODE == MODE_STEP) {
-                        const double wn = __ldg(p.w + n);
-                        const uint8_t dm = p.dmask ? __ldg(p.dmask + n) : (uint8_t)0;
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            const int64_t dof = 3 * n + c;
-                            double F = 0.0;
-                            for (int k = 0; k < p.nsrc; ++k)
-                                if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
-                            const double b = __dsub_rn(__dmul_rn(2.0, up[c]), p.uo[dof]);
-                            double un = __fma_rn(wn, __dsub_rn(F, fa[c]), b);
-                            if ((dm >> c) & 1) un = 0.0;
-                            p.uo[dof] = un;
-                        }
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) p.fout[3 * n + c] = fa[c];
-                    }
-                }
-                fa[0] = fa[1] = fa[2] = 0.0;
-            }
-            __syncthreads();
-        }
-    }
-    if constexpr (PATH == OVX_INT8) {
-        ptx::tc_fence_after();
-        if (warp == 0) ptx::tmem_dealloc<TMEM_COLS>(S.tmem);
-    }
-}
+#include "step_v1.cuh"
 
 template <int PATH, int MODE>
 cudaError_t launch_t(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
-    const int smem = (int)sizeof(typename PathCfg<PATH>::Smem);
+    const int smem = (int)sizeof(SmemV1<PATH>);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_kernel<PATH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_v1<PATH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_kernel<PATH, MODE><<<(unsigned)ctas, PathCfg<PATH>::T::NE, smem, st>>>(p);
+    step_v1<PATH, MODE><<<(unsigned)ctas, V1<PATH>::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -504,13 +238,13 @@ constexpr int kZChunk = 64;
 
 template <int PATH>
 LaunchInfo info_t(int64_t nx, int64_t ny, int64_t nz) {
-    using T = typename PathCfg<PATH>::T;
+    using C = V1<PATH>;
     LaunchInfo li;
-    const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + T::TY - 1) / T::TY;
+    const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + C::TY - 1) / C::TY;
     const int64_t tz = (nz + 1 + kZChunk - 1) / kZChunk;
     li.ctas = tx * ty * tz;
-    li.threads = T::NE;
-    li.smem = (int)sizeof(typename PathCfg<PATH>::Smem);
+    li.threads = C::NT;
+    li.smem = (int)sizeof(SmemV1<PATH>);
     return li;
 }
 
@@ -533,7 +267,7 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
 }
 
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
-    const int ty = path == OVX_INT8 ? Tile<EY_I8>::TY : Tile<EY_F64>::TY;
+    const int ty = V1<OVX_INT8>::TY;   // same tile height for every path
     p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
     p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
     p.zchunk = kZChunk;

@@ -1,0 +1,393 @@
+// step_v1.cuh — the fused time-step kernel (included by kernels.cu inside ovx::{anon}).
+//
+// CTA = 32×8 elements per layer (one halo ring recomputed by the neighbour tiles: owned
+// nodes 31×7, element-work redundancy 256/217 = 1.18), marching in z over a chunk of node
+// planes.  Per layer L:
+//   (1) prefetch node plane L+2 of u^{it} and the update operands of plane L (u^{it-1}, w, mask)
+//       into registers — their latency hides under (2);
+//   (2) element forces of layer L (path-specific) -> smem fe[24][256];
+//   (3) scatter in global element order into two smem force planes; plane L is then complete
+//       and is updated in place (Eq. 3 / L263-L266 with the sign of Eq. 3);
+//   (4) park the prefetched plane in the 3-slot smem ring.
+// INT8 path: 512 threads, two per element (u-half / G-half of ū_e, bottom / top output nodes),
+// two M=128 tcgen05.mma.kind::i8 tiles per layer into TMEM (2 × 4 arrays × N48, 64-col pitch).
+
+template <int PATH>
+struct V1 {
+    static constexpr int EY = 8;
+    static constexpr int NE = EX * EY;                 // 256 elements per layer
+    static constexpr int TPE = PATH == OVX_INT8 ? 2 : 1;
+    static constexpr int NT = NE * TPE;                // threads
+    static constexpr int TY = EY - 1;                  // 7 owned node rows
+    static constexpr int PY = EY + 1;                  // 9 node rows per smem plane
+    static constexpr int NOWN = TX * TY;               // 217 owned nodes per plane
+    static constexpr int PLANE = PX * PY * 3;          // 891 doubles per plane
+    static constexpr int PF = (PLANE + NT - 1) / NT;   // prefetched doubles per thread
+    static constexpr int MINB = PATH == OVX_INT8 ? 1 : 2;
+};
+
+struct SmemV1F64 {
+    double up[3][V1<OVX_FP64>::PLANE];
+    double fe[24][256];
+    double facc[2][V1<OVX_FP64>::NOWN * 3];
+};
+
+constexpr int A1_PITCH = 784;   // bytes per 8-row core-matrix group (768 + 16: bank spread)
+constexpr int A1_BYTES = 16 * A1_PITCH;  // one half-word array of 128 rows
+
+struct SmemV1I8 {
+    union {
+        uint8_t A[2][4][A1_BYTES];   // [M-tile][half-word array], K-major canonical layout
+        double fe[24][256];          // aliases M-tile 0's arrays (dead after its MMAs complete)
+    } u;
+    alignas(128) uint8_t B[6 * A1_PITCH];
+    double up[3][V1<OVX_INT8>::PLANE];
+    double facc[2][V1<OVX_INT8>::NOWN * 3];
+    double amax[2][256];
+    uint64_t mbar[2];
+    uint32_t tmem;
+};
+static_assert(sizeof(double) * 24 * 256 <= 4 * A1_BYTES, "fe must alias inside M-tile 0's A arrays");
+
+template <int PATH>
+using SmemV1 = typename std::conditional<PATH == OVX_INT8, SmemV1I8, SmemV1F64>::type;
+
+__device__ __forceinline__ double (*fe_of(SmemV1I8 &S))[256] { return S.u.fe; }
+__device__ __forceinline__ double (*fe_of(SmemV1F64 &S))[256] { return S.fe; }
+
+template <int PATH>
+__device__ __forceinline__ void v1_load_plane_sync(double *dst, const StepParams &p, int64_t X0, int64_t Y0,
+                                                   int64_t iz) {
+    using C = V1<PATH>;
+    const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
+    for (int idx = threadIdx.x; idx < C::PLANE; idx += C::NT) {
+        const int py = idx / (PX * 3);
+        const int rem = idx - py * (PX * 3);
+        const int px = rem / 3, c = rem - px * 3;
+        const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
+        double v = 0.0;
+        if (iz <= p.nz && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1) v = __ldg(p.u + 3 * (ix + NX1 * (iy + NY1 * iz)) + c);
+        dst[idx] = v;
+    }
+}
+
+template <int PATH, int MODE>
+__global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const StepParams p) {
+    using C = V1<PATH>;
+    constexpr int NT = C::NT, TY = C::TY, NOWN = C::NOWN, PLANE = C::PLANE, PF = C::PF;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    SmemV1<PATH> &S = *reinterpret_cast<SmemV1<PATH> *>(smem_raw);
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+
+    int bid = blockIdx.x;
+    const int tx = bid % p.tiles_x;
+    bid /= p.tiles_x;
+    const int ty = bid % p.tiles_y;
+    const int tz = bid / p.tiles_y;
+    const int64_t X0 = (int64_t)tx * TX, Y0 = (int64_t)ty * TY;
+    const int64_t Z0 = (int64_t)tz * p.zchunk;
+    const int64_t Z1 = min(Z0 + (int64_t)p.zchunk, p.nz + 1);
+    const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
+
+    // element (and half) handled by this thread
+    int el, half = 0, mt = 0, row = 0;
+    if constexpr (PATH == OVX_INT8) {
+        const int g = warp >> 2;          // 0..3: (M-tile, half)
+        row = (warp & 3) * 32 + lane;     // TMEM lane = MMA row
+        mt = g >> 1;
+        half = g & 1;                     // 0: u-part of ū_e, outputs of nodes 0-3; 1: G-part, nodes 4-7
+        el = mt * 128 + row;
+    } else {
+        el = t;
+    }
+    const int lx = el % EX, ly = el / EX;
+    const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
+    const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
+
+    // does any point source fall on this tile's owned columns?
+    bool has_src = false;
+    if (MODE == MODE_STEP)
+        for (int k = 0; k < p.nsrc; ++k) {
+            const int64_t n = p.src_dof[k] / 3;
+            const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+            has_src |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
+        }
+
+    uint32_t phase = 0;
+    if constexpr (PATH == OVX_INT8) {
+        // resident B operand: B[n = 2i+b'][kb = 2k+b] = K_e^INT8[i][k]·δ(b,b')
+        for (int idx = t; idx < 48 * 96; idx += NT) {
+            const int n = idx / 96, kb = idx - n * 96;
+            const int off = (n >> 3) * A1_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
+            S.B[off] = ((kb & 1) == (n & 1)) ? (uint8_t)c_K8[(n >> 1) * 48 + (kb >> 1)] : (uint8_t)0;
+        }
+        if (warp == 0) ptx::tmem_alloc<512>(&S.tmem);
+        if (t == 0) {
+            ptx::mbar_init(&S.mbar[0], 1);
+            ptx::mbar_init(&S.mbar[1], 1);
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+    }
+    for (int i = t; i < 2 * NOWN * 3; i += NT) (&S.facc[0][0])[i] = 0.0;
+    const int64_t Lfirst = max(Z0 - 1, (int64_t)0);
+    v1_load_plane_sync<PATH>(S.up[Lfirst % 3], p, X0, Y0, Lfirst);
+    v1_load_plane_sync<PATH>(S.up[(Lfirst + 1) % 3], p, X0, Y0, Lfirst + 1);
+    __syncthreads();
+    if constexpr (PATH == OVX_INT8) ptx::tc_fence_after();
+
+    for (int64_t L = Z0 - 1; L < Z1; ++L) {
+        const bool layer_ok = (L >= 0 && L < p.nz);
+        const bool plane_done = (L >= Z0 && L <= p.nz);
+        // ---- (1) prefetch: plane L+2 (needed by layer L+1) and the update operands of plane L ----
+        const int64_t pz = L + 2;
+        const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < p.nz);
+        double pfv[PF];
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+            const int idx = t + j * NT;
+            pfv[j] = 0.0;
+            if (pf && idx < PLANE) {
+                const int py = idx / (PX * 3);
+                const int rem = idx - py * (PX * 3);
+                const int px = rem / 3, c = rem - px * 3;
+                const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
+                if (ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1) pfv[j] = __ldg(p.u + 3 * (ix + NX1 * (iy + NY1 * pz)) + c);
+            }
+        }
+        const int nxl = t % TX, nyl = t / TX;
+        const int64_t uix = X0 + nxl, uiy = Y0 + nyl;
+        const bool upd = plane_done && t < NOWN && uix < NX1 && uiy < NY1;
+        const int64_t un_id = uix + NX1 * (uiy + NY1 * L);
+        double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;
+        uint8_t dm = 0;
+        if (MODE == MODE_STEP && upd) {
+            upv[0] = p.uo[3 * un_id];
+            upv[1] = p.uo[3 * un_id + 1];
+            upv[2] = p.uo[3 * un_id + 2];
+            wn = __ldg(p.w + un_id);
+            dm = p.dmask ? __ldg(p.dmask + un_id) : (uint8_t)0;
+        }
+
+        // ---- (2) element forces of layer L ----
+        if (layer_ok) {
+            const double *plo = S.up[L % 3], *phi = S.up[(L + 1) % 3];
+            const int m = ein ? (int)__ldg(p.mat + ex + p.nx * (ey + p.ny * L)) : 0;
+            const int64_t eid = ex + p.nx * (ey + p.ny * L);
+            const int64_t dj = eid - p.dbg_e0;
+            const bool dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
+                             dj >= 0 && dj < p.dbg_ne;
+            double ue[24];
+            gather<C::PY>(ue, plo, phi, lx, ly);
+            if constexpr (PATH == OVX_FP64) {
+                double fe[24];
+                element_force_wht(ue, c_mat[m], fe);
+#pragma unroll
+                for (int r = 0; r < 24; ++r) {
+                    S.fe[r][el] = ein ? fe[r] : 0.0;
+                    if (MODE == MODE_DEBUG && dbg && p.dbg_fe) p.dbg_fe[dj * 24 + r] = fe[r];
+                }
+            } else if constexpr (PATH == OVX_FP64_DENSE) {
+                const double ck = c_mat[m].ck, cg = c_mat[m].cg;
+#pragma unroll 1
+                for (int r = 0; r < 24; ++r) {
+                    double a = 0.0, b = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 24; ++c) {
+                        a = __dadd_rn(a, __dmul_rn(c_Kk[r * 24 + c], ue[c]));
+                        b = __dadd_rn(b, __dmul_rn(c_Kg[r * 24 + c], ue[c]));
+                    }
+                    const double f = __dadd_rn(__dmul_rn(ck, a), __dmul_rn(cg, b));
+                    S.fe[r][el] = ein ? f : 0.0;
+                    if (MODE == MODE_DEBUG && dbg && p.dbg_fe) p.dbg_fe[dj * 24 + r] = f;
+                }
+            } else {
+                // ---- Eqs. 10-16: s_e, INT64 image, byte slices -> A operand (this thread: 24 of 48) ----
+                const double cG = c_mat[m].cG;
+                double hm = 0.0;
+#pragma unroll
+                for (int i = 0; i < 12; ++i) hm = fmax(hm, fabs(half ? ue[12 + i] : ue[i]));
+                S.amax[half][el] = hm;
+                asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
+                const double amax = fmax(S.amax[0][el], S.amax[1][el]);
+                // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)  (RN is monotone, cG > 0)
+                const double s = fmax(amax, __dmul_rn(cG, amax));
+                const bool deg = !ein || !(s >= 0x1p-1022) || isinf(s);
+                const bool fast = s >= 0x1p-960;
+                const double r = 1.0 / s;                          // RN(1/s_e), reading Q7
+                const double R = fast ? __dmul_rn(r, 0x1p56) : r;  // exact power-of-two scaling
+                uint8_t *Ab = &S.u.A[mt][0][0];
+                const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    uint32_t lo[8], hi[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int i = ch * 8 + q;          // index into u_e
+                        const int k = 24 * half + i;       // index into ū_e
+                        const double ub = half ? __dmul_rn(cG, ue[i]) : ue[i];
+                        const double tt = fast ? __dmul_rn(ub, R) : __dmul_rn(__dmul_rn(ub, r), 0x1p56);
+                        const long long v = deg ? 0ll : __double2ll_rz(tt);  // truncation toward 0 (Q8)
+                        const unsigned long long vp = (unsigned long long)v + (1ull << 56);
+                        lo[q] = (uint32_t)vp;
+                        hi[q] = (uint32_t)(vp >> 32);
+                        if (MODE == MODE_DEBUG && dbg) {
+                            if (p.dbg_v) p.dbg_v[dj * 48 + k] = v;
+                            if (p.dbg_d)
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = (uint8_t)(vp >> (8 * j));
+                        }
+                    }
+                    const uint32_t off = rowoff + (uint32_t)(3 * half + ch) * 128;
+#pragma unroll
+                    for (int pa = 0; pa < 4; ++pa) {
+                        const uint32_t *src = pa < 2 ? lo : hi;
+                        const uint32_t sel = (pa & 1) ? 0x7632u : 0x5410u;
+                        uint4 wv;
+                        wv.x = __byte_perm(src[0], src[1], sel);
+                        wv.y = __byte_perm(src[2], src[3], sel);
+                        wv.z = __byte_perm(src[4], src[5], sel);
+                        wv.w = __byte_perm(src[6], src[7], sel);
+                        *reinterpret_cast<uint4 *>(Ab + pa * A1_BYTES + off) = wv;
+                    }
+                }
+                if (MODE == MODE_DEBUG && dbg && half == 0 && p.dbg_s) p.dbg_s[dj] = s;
+
+                // ---- Eq. 17: 2 M-tiles × 4 arrays × 3 K-steps of M128 N48 K32 ----
+                ptx::fence_proxy_async_smem();
+                __syncthreads();
+                if (t == 0) {
+                    ptx::tc_fence_after();
+                    const uint32_t b0 = ptx::smem_u32(&S.B[0]);
+#pragma unroll
+                    for (int mm = 0; mm < 2; ++mm) {
+                        const uint32_t a0 = ptx::smem_u32(&S.u.A[mm][0][0]);
+#pragma unroll
+                        for (int pa = 0; pa < 4; ++pa)
+#pragma unroll
+                            for (int ks = 0; ks < 3; ++ks) {
+                                const uint64_t ad = ptx::smem_desc(a0 + pa * A1_BYTES + ks * 256, 128, A1_PITCH);
+                                const uint64_t bd = ptx::smem_desc(b0 + ks * 256, 128, A1_PITCH);
+                                ptx::mma_i8(S.tmem + mm * 256 + pa * 64, ad, bd, IDESC, ks > 0 ? 1u : 0u);
+                            }
+                        ptx::mma_commit(&S.mbar[mm]);
+                    }
+                }
+                ptx::mbar_wait(&S.mbar[mt], phase);
+                phase ^= 1;
+                ptx::tc_fence_after();
+
+                // ---- epilogue: 12 outputs (nodes 4·half .. 4·half+3): exact recombination + Eq. 9 ----
+                const double c1 = c_mat[m].c1, c2 = c_mat[m].c2;
+                const double sig = __dmul_rn(s, 0x1p-56);
+                const uint32_t tb = S.tmem + ((uint32_t)((warp & 3) * 32) << 16) + mt * 256 + half * 24;
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {           // 4 outputs per round (8 columns per array)
+                    uint32_t R0[8], R1[8], R2[8], R3[8];
+                    ptx::tmem_ld8(tb + 0 + cc * 8, R0);
+                    ptx::tmem_ld8(tb + 64 + cc * 8, R1);
+                    ptx::tmem_ld8(tb + 128 + cc * 8, R2);
+                    ptx::tmem_ld8(tb + 192 + cc * 8, R3);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int i = 12 * half + cc * 4 + q;
+                        const int32_t Cj[8] = {(int32_t)R0[2 * q], (int32_t)R0[2 * q + 1], (int32_t)R1[2 * q],
+                                               (int32_t)R1[2 * q + 1], (int32_t)R2[2 * q], (int32_t)R2[2 * q + 1],
+                                               (int32_t)R3[2 * q], (int32_t)R3[2 * q + 1]};
+                        const int32_t L0 = Cj[0] + 256 * Cj[1], L1 = Cj[2] + 256 * Cj[3];
+                        const int32_t L2 = Cj[4] + 256 * Cj[5], L3 = Cj[6] + 256 * Cj[7];
+                        // y = Σ_j 256^j C'_j + 2^63 = lo + 2^32 hi; both limbs < 2^44 -> exact via the
+                        // 1.5·2^52 magic (no 64-bit I2F), one rounding in the final fma = RN(y)
+                        const long long lo = (long long)L0 + (long long)L1 * 65536ll;
+                        const long long hi = (long long)L2 + (long long)L3 * 65536ll;
+                        const double dlo = __longlong_as_double(lo + 0x4338000000000000ll) - 0x1.8p52;
+                        const double dhi = __longlong_as_double(hi + 0x4338000000000000ll) - (0x1.8p52 - 0x1p31);
+                        const double Y = __fma_rn(dhi, 0x1p32, dlo);
+                        const double ui = half ? ue[12 + cc * 4 + q] : ue[cc * 4 + q];
+                        const double f = __dmul_rn(c1, __dadd_rn(__dmul_rn(Y, sig), __dmul_rn(c2, ui)));
+                        if (MODE == MODE_DEBUG && dbg) {
+                            if (p.dbg_C)
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) p.dbg_C[dj * 192 + j * 24 + i] = Cj[j];
+                            const __int128 y = ((__int128)hi + ((__int128)1 << 31)) * ((__int128)1 << 32) + (__int128)lo;
+                            if (p.dbg_yhi) p.dbg_yhi[dj * 24 + i] = (long long)(y >> 64);
+                            if (p.dbg_ylo) p.dbg_ylo[dj * 24 + i] = (long long)(unsigned long long)y;
+                            if (p.dbg_fe) p.dbg_fe[dj * 24 + i] = deg ? 0.0 : f;
+                        }
+                        // fe aliases M-tile 0's A: written only after this M-tile's MMAs completed
+                        S.u.fe[i][el] = deg ? 0.0 : f;
+                    }
+                }
+                ptx::tc_fence_before();
+            }
+        }
+        __syncthreads();
+
+        // ---- (3) scatter (global element order) + update of the completed plane L ----
+        if (t < NOWN) {
+            double(*fe)[256] = fe_of(S);
+            const int e00 = nxl + EX * nyl, e10 = e00 + 1, e01 = e00 + EX, e11 = e01 + 1;
+            double *fl = &S.facc[L & 1][t * 3];
+            double *fh = &S.facc[(L + 1) & 1][t * 3];
+            if (layer_ok && L >= Z0) {     // bottom corners of layer L -> plane L
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double f = fl[c];
+                    f = __dadd_rn(f, fe[3 * 2 + c][e00]);
+                    f = __dadd_rn(f, fe[3 * 3 + c][e10]);
+                    f = __dadd_rn(f, fe[3 * 1 + c][e01]);
+                    f = __dadd_rn(f, fe[3 * 0 + c][e11]);
+                    fl[c] = f;
+                }
+            }
+            if (layer_ok && L + 1 < Z1) {  // top corners of layer L -> plane L+1
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double f = fh[c];
+                    f = __dadd_rn(f, fe[3 * 6 + c][e00]);
+                    f = __dadd_rn(f, fe[3 * 7 + c][e10]);
+                    f = __dadd_rn(f, fe[3 * 5 + c][e01]);
+                    f = __dadd_rn(f, fe[3 * 4 + c][e11]);
+                    fh[c] = f;
+                }
+            }
+            if (upd) {
+                const double *up = &S.up[L % 3][((nyl + 1) * PX + (nxl + 1)) * 3];
+                if (MODE == MODE_STEP) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const int64_t dof = 3 * un_id + c;
+                        double F = 0.0;
+                        if (has_src)
+                            for (int k = 0; k < p.nsrc; ++k)
+                                if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
+                        const double b = __dsub_rn(__dmul_rn(2.0, up[c]), upv[c]);
+                        double un = __fma_rn(wn, __dsub_rn(F, fl[c]), b);
+                        if ((dm >> c) & 1) un = 0.0;
+                        p.uo[dof] = un;
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) p.fout[3 * un_id + c] = fl[c];
+                }
+            }
+            if (plane_done) fl[0] = fl[1] = fl[2] = 0.0;
+        }
+        // ---- (4) park the prefetched plane L+2 (slot of plane L-1, no longer read) ----
+        if (pf) {
+            double *dst = S.up[pz % 3];
+#pragma unroll
+            for (int j = 0; j < PF; ++j) {
+                const int idx = t + j * NT;
+                if (idx < PLANE) dst[idx] = pfv[j];
+            }
+        }
+        __syncthreads();
+    }
+    if constexpr (PATH == OVX_INT8) {
+        ptx::tc_fence_after();
+        if (warp == 0) ptx::tmem_dealloc<512>(S.tmem);
+    }
+}
