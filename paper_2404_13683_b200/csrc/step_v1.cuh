@@ -205,9 +205,17 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             } else {
                 // ---- Eqs. 10-16: s_e, INT64 image, byte slices -> A operand (this thread: 24 of 48) ----
                 const double cG = c_mat[m].cG;
+                double uo[12];   // u of this thread's output nodes (4·half .. 4·half+3)
+                if (half) {
+#pragma unroll
+                    for (int i = 0; i < 12; ++i) uo[i] = ue[12 + i];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 12; ++i) uo[i] = ue[i];
+                }
                 double hm = 0.0;
 #pragma unroll
-                for (int i = 0; i < 12; ++i) hm = fmax(hm, fabs(half ? ue[12 + i] : ue[i]));
+                for (int i = 0; i < 12; ++i) hm = fmax(hm, fabs(uo[i]));
                 S.amax[half][el] = hm;
                 asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
                 const double amax = fmax(S.amax[0][el], S.amax[1][el]);
@@ -219,6 +227,12 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                 const double R = fast ? __dmul_rn(r, 0x1p56) : r;  // exact power-of-two scaling
                 uint8_t *Ab = &S.u.A[mt][0][0];
                 const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
+                // ū_e for this half: u_e (half 0) or RN(cG·u_e) (half 1); half is warp-uniform
+                if (half) {
+#pragma unroll
+                    for (int i = 0; i < 24; ++i) ue[i] = __dmul_rn(cG, ue[i]);
+                }
+                const bool straight = fast && !deg;   // all but degenerate / tiny-s elements
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
                     uint32_t lo[8], hi[8];
@@ -226,9 +240,12 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                     for (int q = 0; q < 8; ++q) {
                         const int i = ch * 8 + q;          // index into u_e
                         const int k = 24 * half + i;       // index into ū_e
-                        const double ub = half ? __dmul_rn(cG, ue[i]) : ue[i];
-                        const double tt = fast ? __dmul_rn(ub, R) : __dmul_rn(__dmul_rn(ub, r), 0x1p56);
-                        const long long v = deg ? 0ll : __double2ll_rz(tt);  // truncation toward 0 (Q8)
+                        long long v;
+                        if (straight) {
+                            v = __double2ll_rz(__dmul_rn(ue[i], R));      // truncation toward 0 (Q8)
+                        } else {
+                            v = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ue[i], r), 0x1p56));
+                        }
                         const unsigned long long vp = (unsigned long long)v + (1ull << 56);
                         lo[q] = (uint32_t)vp;
                         hi[q] = (uint32_t)(vp >> 32);
@@ -305,7 +322,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                         const double dlo = __longlong_as_double(lo + 0x4338000000000000ll) - 0x1.8p52;
                         const double dhi = __longlong_as_double(hi + 0x4338000000000000ll) - (0x1.8p52 - 0x1p31);
                         const double Y = __fma_rn(dhi, 0x1p32, dlo);
-                        const double ui = half ? ue[12 + cc * 4 + q] : ue[cc * 4 + q];
+                        const double ui = uo[cc * 4 + q];
                         const double f = __dmul_rn(c1, __dadd_rn(__dmul_rn(Y, sig), __dmul_rn(c2, ui)));
                         if (MODE == MODE_DEBUG && dbg) {
                             if (p.dbg_C)
