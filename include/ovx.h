@@ -73,7 +73,7 @@ ovx_status ovx_set_stream(ovx_ctx *ctx, void *stream);
 /* ---- model (cubes of side ds on a structured grid; L94: κ, G) -- */
 /* Global element counts and edge length; nx,ny,nz >= 1, ds > 0.  Resets the model. */
 ovx_status ovx_set_grid(ovx_ctx *ctx, int64_t nx, int64_t ny, int64_t nz, double ds);
-/* n <= 256 materials; rho, kappa, G > 0 and finite (host arrays of length n). */
+/* n <= 255 materials; rho, kappa, G > 0 and finite (host arrays of length n). */
 ovx_status ovx_set_materials(ovx_ctx *ctx, int n, const double *rho, const double *kappa,
                              const double *G);
 /* Per-element material ids (host, nx*ny*nz bytes); every id < n materials. */

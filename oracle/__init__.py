@@ -80,6 +80,7 @@ def int_matrices():
 
 PATH_FP64, PATH_INT8 = 0, 1
 DIGITS_PAPER, DIGITS_BYTES = 0, 1
+DIGITS_BYTES_FOLD = 3      # byte slices + Eq. 9 diagonal term in the integer product (variant D)
 
 
 def element_nodes(nx: int, ny: int, e: int) -> np.ndarray:
@@ -113,11 +114,11 @@ def element_fp64(ue, kappa, G, ds) -> np.ndarray:
     return fe
 
 
-def element_int8(ue, kappa, G, ds, M: int = 8, digits: int = DIGITS_BYTES) -> dict:
+def element_int8(ue, kappa, G, ds, M: int = 8, digits: int = DIGITS_BYTES_FOLD) -> dict:
     """Bit-level integer path for one element; returns s, v, d, C, y (python ints), fe."""
     K8, _, _ = int_matrices()
     ue = np.ascontiguousarray(ue, dtype=np.float64)
-    nd = (7 * M + 1 + 7) // 8 if digits else M
+    nd = (7 * M + 1 + 7) // 8 if (digits & 1) else M
     s = np.zeros(1)
     v = np.zeros(48, dtype=np.int64)
     d = np.zeros(nd * 48, dtype=np.int32)
@@ -133,7 +134,7 @@ def element_int8(ue, kappa, G, ds, M: int = 8, digits: int = DIGITS_BYTES) -> di
                 degenerate=bool(deg))
 
 
-def apply_K(nx, ny, nz, ds, mat, kappa, G, u, path=PATH_FP64, M=8, digits=DIGITS_BYTES) -> np.ndarray:
+def apply_K(nx, ny, nz, ds, mat, kappa, G, u, path=PATH_FP64, M=8, digits=DIGITS_BYTES_FOLD) -> np.ndarray:
     K8, Kk, Kg = int_matrices()
     mat = np.ascontiguousarray(mat, dtype=np.uint8)
     kappa = np.ascontiguousarray(kappa, dtype=np.float64)
@@ -146,7 +147,7 @@ def apply_K(nx, ny, nz, ds, mat, kappa, G, u, path=PATH_FP64, M=8, digits=DIGITS
     return f
 
 
-def run(model, u, u_prev, it: int, nsteps: int, path=PATH_FP64, M=8, digits=DIGITS_BYTES):
+def run(model, u, u_prev, it: int, nsteps: int, path=PATH_FP64, M=8, digits=DIGITS_BYTES_FOLD):
     """Advance (u, u_prev, it) by nsteps with the model dict produced by workloads.
 
     model keys: nx, ny, nz, ds, mat (uint8 per element), rho/kappa/G (per material),

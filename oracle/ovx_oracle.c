@@ -110,6 +110,11 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
                         const int8_t *K8 /*24x48 row-major*/, int M, int digits,
                         double *s_out, int64_t *v_out, int32_t *d_out, int64_t *C_out,
                         int64_t *y_hi, int64_t *y_lo, double *fe) {
+    /* digits bit 1 ("fold", DESIGN.md variant D): the Eq. 9 diagonal term (256/3)(G/κ)u_e =
+     * 128·ū_{e,G} is taken in the integer domain, y_D = K_D v with K_D = [K^κ | K̄^G + 128 I]
+     * (= [256 A_κ | 384 A_G]), and f_e = RN(c1s·RN(y_D)), c1s = RN(c1·RN(s_e·2^-56)). */
+    const int fold = (digits >> 1) & 1;
+    digits &= 1;
     double cG = (2.0 * G) / (3.0 * kappa);       /* (2/3) G/κ, */
     double c1 = kappa * ds / 256.0;              /* κ ds / 256, Eq. 9          */
     double c2 = (256.0 * G) / (3.0 * kappa);     /* (256/3) G/κ, Eq. 9         */
@@ -154,6 +159,7 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
         for (int r = 0; r < 24; ++r) {
             int64_t c = 0;                       /* Eq. 17: K_e^INT8 · digits_j   */
             for (int k = 0; k < 48; ++k) c += (int64_t)K8[r * 48 + k] * d[k];
+            if (fold) c += 128 * (int64_t)d[24 + r];   /* + 128 I on the G block */
             if (C_out) C_out[j * 24 + r] = c;
             __int128 w = digits ? ((__int128)1 << (8 * j)) : ((__int128)1 << (7 * j));
             y[r] += w * (__int128)c;
@@ -162,7 +168,7 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
     if (digits) {
         /* K_e^INT8 · (a·1) = a · rowsum; subtract it back:  y = K v' − a K 1 */
         for (int r = 0; r < 24; ++r) {
-            int64_t rs = 0;
+            int64_t rs = fold ? 128 : 0;
             for (int k = 0; k < 48; ++k) rs += K8[r * 48 + k];
             y[r] -= (__int128)A * (__int128)rs;
         }
@@ -173,9 +179,13 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
         if (y_lo) y_lo[r] = (int64_t)(uint64_t)y[r];
         if (fe) {
             double Y = degenerate ? 0.0 : (double)y[r];  /* RN(y), one rounding (Q13) */
-            double a = Y * sig;
-            double b = c2 * ue[r];
-            fe[r] = degenerate ? 0.0 : c1 * (a + b);    /* Eq. 9, literal order */
+            if (fold) {
+                fe[r] = degenerate ? 0.0 : (c1 * sig) * Y;
+            } else {
+                double a = Y * sig;
+                double b = c2 * ue[r];
+                fe[r] = degenerate ? 0.0 : c1 * (a + b);    /* Eq. 9, literal order */
+            }
         }
     }
     return degenerate;

@@ -207,7 +207,7 @@ ovx_status ovx_set_grid(ovx_ctx *ctx, int64_t nx, int64_t ny, int64_t nz, double
 
 ovx_status ovx_set_materials(ovx_ctx *ctx, int n, const double *rho, const double *kappa, const double *G) {
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
-    if (n < 1 || n > kMaxMat || !rho || !kappa || !G) return fail(ctx, OVX_EINVAL, "need 1..256 materials");
+    if (n < 1 || n > kMaxMat - 1 || !rho || !kappa || !G) return fail(ctx, OVX_EINVAL, "need 1..255 materials");
     for (int i = 0; i < n; ++i)
         if (!(rho[i] > 0) || !(kappa[i] > 0) || !(G[i] > 0) || !std::isfinite(rho[i]) || !std::isfinite(kappa[i]) ||
             !std::isfinite(G[i]))

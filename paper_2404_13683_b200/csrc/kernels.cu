@@ -254,6 +254,10 @@ cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, c
                              cudaStream_t st) {
     cudaError_t e;
     if ((e = cudaMemcpyToSymbolAsync(c_mat, mats, sizeof(MatConst) * nmat, 0, cudaMemcpyHostToDevice, st))) return e;
+    static const MatConst zero = {};   // reserved zero material: elements outside the domain
+    if ((e = cudaMemcpyToSymbolAsync(c_mat, &zero, sizeof(MatConst), sizeof(MatConst) * kZeroMat,
+                                     cudaMemcpyHostToDevice, st)))
+        return e;
     if ((e = cudaMemcpyToSymbolAsync(c_K8, k8, 1152, 0, cudaMemcpyHostToDevice, st))) return e;
     if ((e = cudaMemcpyToSymbolAsync(c_Kk, kk, 576 * 8, 0, cudaMemcpyHostToDevice, st))) return e;
     if ((e = cudaMemcpyToSymbolAsync(c_Kg, kg, 576 * 8, 0, cudaMemcpyHostToDevice, st))) return e;

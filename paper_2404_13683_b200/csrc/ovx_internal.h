@@ -5,7 +5,8 @@
 
 namespace ovx {
 
-constexpr int kMaxMat = 256;
+constexpr int kMaxMat = 256;   // constant-table size; id 255 is the reserved zero material
+constexpr int kZeroMat = kMaxMat - 1;
 constexpr int kMaxSrc = 16;
 
 // Per-material constants, computed on the host in the operation order the

@@ -11,6 +11,9 @@
 //   (4) park the prefetched plane in the 3-slot smem ring.
 // INT8 path: 512 threads, two per element (u-half / G-half of ū_e, bottom / top output nodes),
 // two M=128 tcgen05.mma.kind::i8 tiles per layer into TMEM (2 × 4 arrays × N48, 64-col pitch).
+// The Eq. 9 diagonal term is folded into the integer product (DESIGN.md variant D): per array
+// 3 K-steps against B = −K_e^INT8 ⊗ I_2 plus 2 K-steps of the G bytes against −128·I ⊗ I_2, so
+// D = −(K_e^INT8 v + 128 v_G) byte-stage by byte-stage, and f_e = RN(c1 s_e 2^-56)·RN(y).
 
 template <int PATH>
 struct V1 {
@@ -32,15 +35,21 @@ struct SmemV1F64 {
     double facc[2][V1<OVX_FP64>::NOWN * 3];
 };
 
-constexpr int A1_PITCH = 784;   // bytes per 8-row core-matrix group (768 + 16: bank spread)
-constexpr int A1_BYTES = 16 * A1_PITCH;  // one half-word array of 128 rows
+// A operand row (one element, one half-word array): 7 chunks of 16 B — chunks 0-2 the u bytes,
+// 3-5 the G bytes, 6 zero (K padding of the identity block's second K-step).
+constexpr int A1_CHUNKS = 7;
+constexpr int A1_PITCH = A1_CHUNKS * 128 + 16;   // bytes per 8-row core-matrix group (+16: bank spread)
+constexpr int A1_BYTES = 16 * A1_PITCH;          // one half-word array of 128 rows
+constexpr int B1_PITCH = 6 * 128;                // main B: 48 rows × 96 K-bytes
+constexpr int BI_PITCH = 2 * 128;                // identity blocks: 48 rows × 32 K-bytes
 
 struct SmemV1I8 {
     union {
         uint8_t A[2][4][A1_BYTES];   // [M-tile][half-word array], K-major canonical layout
         double fe[24][256];          // aliases M-tile 0's arrays (dead after its MMAs complete)
     } u;
-    alignas(128) uint8_t B[6 * A1_PITCH];
+    alignas(128) uint8_t B[6 * B1_PITCH];
+    alignas(128) uint8_t BI[2][6 * BI_PITCH];
     double up[3][V1<OVX_INT8>::PLANE];
     double facc[2][V1<OVX_INT8>::NOWN * 3];
     double amax[2][256];
@@ -89,6 +98,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
     const int64_t Z0 = (int64_t)tz * p.zchunk;
     const int64_t Z1 = min(Z0 + (int64_t)p.zchunk, p.nz + 1);
     const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
+    const int64_t PSTRIDE = NX1 * NY1;        // nodes per plane
 
     // element (and half) handled by this thread
     int el, half = 0, mt = 0, row = 0;
@@ -104,6 +114,27 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
     const int lx = el % EX, ly = el / EX;
     const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
     const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
+    const uint8_t *matcol = p.mat + (ein ? ex + p.nx * ey : 0);   // + nx*ny*L per layer
+    const int64_t mstride = p.nx * p.ny;
+
+    // loop-invariant prefetch sources of this thread (offsets within a plane of u)
+    int64_t pfoff[PF];
+    bool pfok[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+        const int idx = t + j * NT;
+        const int py = idx / (PX * 3);
+        const int rem = idx - py * (PX * 3);
+        const int px = rem / 3, c = rem - px * 3;
+        const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
+        pfok[j] = idx < PLANE && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1;
+        pfoff[j] = pfok[j] ? 3 * (ix + NX1 * iy) + c : 0;
+    }
+    // update role: owned node (nxl, nyl) of the tile
+    const int nxl = t % TX, nyl = t / TX;
+    const int64_t uix = X0 + nxl, uiy = Y0 + nyl;
+    const bool own = t < NOWN && uix < NX1 && uiy < NY1;
+    const int64_t ucol = own ? uix + NX1 * uiy : 0;
 
     // does any point source fall on this tile's owned columns?
     bool has_src = false;
@@ -116,11 +147,25 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
 
     uint32_t phase = 0;
     if constexpr (PATH == OVX_INT8) {
-        // resident B operand: B[n = 2i+b'][kb = 2k+b] = K_e^INT8[i][k]·δ(b,b')
+        // resident B operands: B[n = 2i+b'][kb = 2k+b] = −K_e^INT8[i][k]·δ(b,b');
+        // BI[s][n][kb] = −128·δ(k, i − 16 s)·δ(b,b') on the G bytes (k = G index within the K-step)
         for (int idx = t; idx < 48 * 96; idx += NT) {
             const int n = idx / 96, kb = idx - n * 96;
-            const int off = (n >> 3) * A1_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
-            S.B[off] = ((kb & 1) == (n & 1)) ? (uint8_t)c_K8[(n >> 1) * 48 + (kb >> 1)] : (uint8_t)0;
+            const int off = (n >> 3) * B1_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
+            S.B[off] = ((kb & 1) == (n & 1)) ? (uint8_t)(-(int)c_K8[(n >> 1) * 48 + (kb >> 1)]) : (uint8_t)0;
+        }
+        for (int idx = t; idx < 2 * 48 * 32; idx += NT) {
+            const int s2 = idx / (48 * 32), r2 = idx - s2 * 48 * 32;
+            const int n = r2 / 32, kb = r2 - n * 32;
+            const int off = (n >> 3) * BI_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
+            const int k = 16 * s2 + (kb >> 1);
+            S.BI[s2][off] = ((kb & 1) == (n & 1) && k == (n >> 1)) ? (uint8_t)0x80 : (uint8_t)0;
+        }
+        // zero the K-padding chunk of every A row (never written afterwards)
+        for (int idx = t; idx < 2 * 4 * 128; idx += NT) {
+            const int a = idx >> 7, r = idx & 127;
+            *reinterpret_cast<uint4 *>(&S.u.A[a >> 2][a & 3][(r >> 3) * A1_PITCH + 6 * 128 + (r & 7) * 16]) =
+                make_uint4(0, 0, 0, 0);
         }
         if (warp == 0) ptx::tmem_alloc<512>(&S.tmem);
         if (t == 0) {
@@ -144,22 +189,11 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
         const int64_t pz = L + 2;
         const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < p.nz);
         double pfv[PF];
+        const double *uplane = p.u + 3 * PSTRIDE * pz;
 #pragma unroll
-        for (int j = 0; j < PF; ++j) {
-            const int idx = t + j * NT;
-            pfv[j] = 0.0;
-            if (pf && idx < PLANE) {
-                const int py = idx / (PX * 3);
-                const int rem = idx - py * (PX * 3);
-                const int px = rem / 3, c = rem - px * 3;
-                const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
-                if (ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1) pfv[j] = __ldg(p.u + 3 * (ix + NX1 * (iy + NY1 * pz)) + c);
-            }
-        }
-        const int nxl = t % TX, nyl = t / TX;
-        const int64_t uix = X0 + nxl, uiy = Y0 + nyl;
-        const bool upd = plane_done && t < NOWN && uix < NX1 && uiy < NY1;
-        const int64_t un_id = uix + NX1 * (uiy + NY1 * L);
+        for (int j = 0; j < PF; ++j) pfv[j] = (pf && pfok[j]) ? __ldg(uplane + pfoff[j]) : 0.0;
+        const bool upd = plane_done && own;
+        const int64_t un_id = ucol + PSTRIDE * L;
         double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;
         uint8_t dm = 0;
         if (MODE == MODE_STEP && upd) {
@@ -173,7 +207,8 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
         // ---- (2) element forces of layer L ----
         if (layer_ok) {
             const double *plo = S.up[L % 3], *phi = S.up[(L + 1) % 3];
-            const int m = ein ? (int)__ldg(p.mat + ex + p.nx * (ey + p.ny * L)) : 0;
+            // material of this element; elements outside the domain use the reserved zero material
+            const int m = ein ? (int)__ldg(matcol + mstride * L) : kZeroMat;
             const int64_t eid = ex + p.nx * (ey + p.ny * L);
             const int64_t dj = eid - p.dbg_e0;
             const bool dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
@@ -182,10 +217,10 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             gather<C::PY>(ue, plo, phi, lx, ly);
             if constexpr (PATH == OVX_FP64) {
                 double fe[24];
-                element_force_wht(ue, c_mat[m], fe);
+                element_force_wht(ue, c_mat[m], fe);   // zero material -> fe = 0 exactly
 #pragma unroll
                 for (int r = 0; r < 24; ++r) {
-                    S.fe[r][el] = ein ? fe[r] : 0.0;
+                    S.fe[r][el] = fe[r];
                     if (MODE == MODE_DEBUG && dbg && p.dbg_fe) p.dbg_fe[dj * 24 + r] = fe[r];
                 }
             } else if constexpr (PATH == OVX_FP64_DENSE) {
@@ -205,58 +240,55 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             } else {
                 // ---- Eqs. 10-16: s_e, INT64 image, byte slices -> A operand (this thread: 24 of 48) ----
                 const double cG = c_mat[m].cG;
-                double uo[12];   // u of this thread's output nodes (4·half .. 4·half+3)
+                double hm = 0.0;
                 if (half) {
 #pragma unroll
-                    for (int i = 0; i < 12; ++i) uo[i] = ue[12 + i];
+                    for (int i = 12; i < 24; ++i) hm = fmax(hm, fabs(ue[i]));
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 12; ++i) uo[i] = ue[i];
+                    for (int i = 0; i < 12; ++i) hm = fmax(hm, fabs(ue[i]));
                 }
-                double hm = 0.0;
-#pragma unroll
-                for (int i = 0; i < 12; ++i) hm = fmax(hm, fabs(uo[i]));
                 S.amax[half][el] = hm;
                 asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
                 const double amax = fmax(S.amax[0][el], S.amax[1][el]);
                 // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)  (RN is monotone, cG > 0)
                 const double s = fmax(amax, __dmul_rn(cG, amax));
                 const bool deg = !ein || !(s >= 0x1p-1022) || isinf(s);
-                const bool fast = s >= 0x1p-960;
-                const double r = 1.0 / s;                          // RN(1/s_e), reading Q7
-                const double R = fast ? __dmul_rn(r, 0x1p56) : r;  // exact power-of-two scaling
                 uint8_t *Ab = &S.u.A[mt][0][0];
-                const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
+                const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16) + (uint32_t)(3 * half) * 128;
                 // ū_e for this half: u_e (half 0) or RN(cG·u_e) (half 1); half is warp-uniform
                 if (half) {
 #pragma unroll
                     for (int i = 0; i < 24; ++i) ue[i] = __dmul_rn(cG, ue[i]);
                 }
-                const bool straight = fast && !deg;   // all but degenerate / tiny-s elements
+                long long v[24];
+                if (!deg && s >= 0x1p-960) {
+                    const double R = __dmul_rn(1.0 / s, 0x1p56);   // RN(1/s_e)·2^56, exact scaling (Q7)
+#pragma unroll
+                    for (int i = 0; i < 24; ++i) v[i] = __double2ll_rz(__dmul_rn(ue[i], R));  // trunc (Q8)
+                } else {
+                    const double r = 1.0 / s;
+#pragma unroll
+                    for (int i = 0; i < 24; ++i)
+                        v[i] = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ue[i], r), 0x1p56));
+                }
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
                     uint32_t lo[8], hi[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const int i = ch * 8 + q;          // index into u_e
-                        const int k = 24 * half + i;       // index into ū_e
-                        long long v;
-                        if (straight) {
-                            v = __double2ll_rz(__dmul_rn(ue[i], R));      // truncation toward 0 (Q8)
-                        } else {
-                            v = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ue[i], r), 0x1p56));
-                        }
-                        const unsigned long long vp = (unsigned long long)v + (1ull << 56);
+                        const unsigned long long vp = (unsigned long long)v[ch * 8 + q] + (1ull << 56);
                         lo[q] = (uint32_t)vp;
                         hi[q] = (uint32_t)(vp >> 32);
                         if (MODE == MODE_DEBUG && dbg) {
-                            if (p.dbg_v) p.dbg_v[dj * 48 + k] = v;
+                            const int k = 24 * half + ch * 8 + q;
+                            if (p.dbg_v) p.dbg_v[dj * 48 + k] = v[ch * 8 + q];
                             if (p.dbg_d)
 #pragma unroll
                                 for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = (uint8_t)(vp >> (8 * j));
                         }
                     }
-                    const uint32_t off = rowoff + (uint32_t)(3 * half + ch) * 128;
+                    const uint32_t off = rowoff + (uint32_t)ch * 128;
 #pragma unroll
                     for (int pa = 0; pa < 4; ++pa) {
                         const uint32_t *src = pa < 2 ? lo : hi;
@@ -271,23 +303,29 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                 }
                 if (MODE == MODE_DEBUG && dbg && half == 0 && p.dbg_s) p.dbg_s[dj] = s;
 
-                // ---- Eq. 17: 2 M-tiles × 4 arrays × 3 K-steps of M128 N48 K32 ----
+                // ---- Eq. 17 (+ folded diagonal): 2 M-tiles × 4 arrays × (3 + 2) K-steps, M128 N48 K32 ----
                 ptx::fence_proxy_async_smem();
                 __syncthreads();
                 if (t == 0) {
                     ptx::tc_fence_after();
                     const uint32_t b0 = ptx::smem_u32(&S.B[0]);
+                    const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
 #pragma unroll
                     for (int mm = 0; mm < 2; ++mm) {
                         const uint32_t a0 = ptx::smem_u32(&S.u.A[mm][0][0]);
 #pragma unroll
-                        for (int pa = 0; pa < 4; ++pa)
+                        for (int pa = 0; pa < 4; ++pa) {
+                            const uint32_t ab = a0 + pa * A1_BYTES;
+                            const uint32_t d = S.tmem + mm * 256 + pa * 64;
 #pragma unroll
-                            for (int ks = 0; ks < 3; ++ks) {
-                                const uint64_t ad = ptx::smem_desc(a0 + pa * A1_BYTES + ks * 256, 128, A1_PITCH);
-                                const uint64_t bd = ptx::smem_desc(b0 + ks * 256, 128, A1_PITCH);
-                                ptx::mma_i8(S.tmem + mm * 256 + pa * 64, ad, bd, IDESC, ks > 0 ? 1u : 0u);
-                            }
+                            for (int ks = 0; ks < 3; ++ks)
+                                ptx::mma_i8(d, ptx::smem_desc(ab + ks * 256, 128, A1_PITCH),
+                                            ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC, ks > 0 ? 1u : 0u);
+                            ptx::mma_i8(d, ptx::smem_desc(ab + 3 * 128, 128, A1_PITCH),
+                                        ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
+                            ptx::mma_i8(d, ptx::smem_desc(ab + 5 * 128, 128, A1_PITCH),
+                                        ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
+                        }
                         ptx::mma_commit(&S.mbar[mm]);
                     }
                 }
@@ -295,9 +333,10 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                 phase ^= 1;
                 ptx::tc_fence_after();
 
-                // ---- epilogue: 12 outputs (nodes 4·half .. 4·half+3): exact recombination + Eq. 9 ----
-                const double c1 = c_mat[m].c1, c2 = c_mat[m].c2;
-                const double sig = __dmul_rn(s, 0x1p-56);
+                // ---- epilogue: 12 outputs (nodes 4·half .. 4·half+3) ----
+                // D_p holds −C_j with C_j = K_D·b_j (K_D·1 = 0, so y = Σ_j 256^j C_j exactly).
+                // Two 64-bit limbs (< 2^44) through the 1.5·2^52 magic, one rounding in the fma.
+                const double alpha = -__dmul_rn(c_mat[m].c1, __dmul_rn(s, 0x1p-56));   // −RN(c1·s·2^-56)
                 const uint32_t tb = S.tmem + ((uint32_t)((warp & 3) * 32) << 16) + mt * 256 + half * 24;
 #pragma unroll
                 for (int cc = 0; cc < 3; ++cc) {           // 4 outputs per round (8 columns per array)
@@ -310,31 +349,32 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const int i = 12 * half + cc * 4 + q;
-                        const int32_t Cj[8] = {(int32_t)R0[2 * q], (int32_t)R0[2 * q + 1], (int32_t)R1[2 * q],
-                                               (int32_t)R1[2 * q + 1], (int32_t)R2[2 * q], (int32_t)R2[2 * q + 1],
-                                               (int32_t)R3[2 * q], (int32_t)R3[2 * q + 1]};
-                        const int32_t L0 = Cj[0] + 256 * Cj[1], L1 = Cj[2] + 256 * Cj[3];
-                        const int32_t L2 = Cj[4] + 256 * Cj[5], L3 = Cj[6] + 256 * Cj[7];
-                        // y = Σ_j 256^j C'_j + 2^63 = lo + 2^32 hi; both limbs < 2^44 -> exact via the
-                        // 1.5·2^52 magic (no 64-bit I2F), one rounding in the final fma = RN(y)
-                        const long long lo = (long long)L0 + (long long)L1 * 65536ll;
-                        const long long hi = (long long)L2 + (long long)L3 * 65536ll;
-                        const double dlo = __longlong_as_double(lo + 0x4338000000000000ll) - 0x1.8p52;
-                        const double dhi = __longlong_as_double(hi + 0x4338000000000000ll) - (0x1.8p52 - 0x1p31);
-                        const double Y = __fma_rn(dhi, 0x1p32, dlo);
-                        const double ui = uo[cc * 4 + q];
-                        const double f = __dmul_rn(c1, __dadd_rn(__dmul_rn(Y, sig), __dmul_rn(c2, ui)));
+                        const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
+                        const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
+                        const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
+                        const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
+                        const long long blo = 0x4338000000000000ll + (long long)c0 + (long long)c1_ * 256ll +
+                                              (long long)c2_ * 65536ll + (long long)c3 * 16777216ll;
+                        const long long bhi = 0x4338000000000000ll + (long long)c4 + (long long)c5 * 256ll +
+                                              (long long)c6 * 65536ll + (long long)c7 * 16777216ll;
+                        const double dlo = __longlong_as_double(blo) - 0x1.8p52;
+                        const double dhi = __longlong_as_double(bhi) - 0x1.8p52;
+                        const double Y = __fma_rn(dhi, 0x1p32, dlo);    // RN(−y)
+                        const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
                         if (MODE == MODE_DEBUG && dbg) {
+                            const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};
+                            __int128 y = 0;
+#pragma unroll
+                            for (int j = 7; j >= 0; --j) y = y * 256 - (__int128)Cj[j];
                             if (p.dbg_C)
 #pragma unroll
-                                for (int j = 0; j < 8; ++j) p.dbg_C[dj * 192 + j * 24 + i] = Cj[j];
-                            const __int128 y = ((__int128)hi + ((__int128)1 << 31)) * ((__int128)1 << 32) + (__int128)lo;
+                                for (int j = 0; j < 8; ++j) p.dbg_C[dj * 192 + j * 24 + i] = -Cj[j];
                             if (p.dbg_yhi) p.dbg_yhi[dj * 24 + i] = (long long)(y >> 64);
                             if (p.dbg_ylo) p.dbg_ylo[dj * 24 + i] = (long long)(unsigned long long)y;
-                            if (p.dbg_fe) p.dbg_fe[dj * 24 + i] = deg ? 0.0 : f;
+                            if (p.dbg_fe) p.dbg_fe[dj * 24 + i] = f;
                         }
                         // fe aliases M-tile 0's A: written only after this M-tile's MMAs completed
-                        S.u.fe[i][el] = deg ? 0.0 : f;
+                        S.u.fe[i][el] = f;
                     }
                 }
                 ptx::tc_fence_before();

@@ -89,7 +89,7 @@ def test_int8_element_records_bit_exact(ovxmod):
         nodes = oracle.element_nodes(m.nx, m.ny, e)
         ue = np.concatenate([u[3 * n:3 * n + 3] for n in nodes])
         mm = m.mat[e]
-        r = oracle.element_int8(ue, m.kappa[mm], m.G[mm], m.ds, 8, oracle.DIGITS_BYTES)
+        r = oracle.element_int8(ue, m.kappa[mm], m.G[mm], m.ds, 8, oracle.DIGITS_BYTES_FOLD)
         assert rec["s"][e] == r["s"]
         assert np.array_equal(rec["v"][e], r["v"])
         assert np.array_equal(rec["d"][e].astype(np.int32), r["d"])

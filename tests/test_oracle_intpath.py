@@ -159,9 +159,38 @@ def test_zero_and_subnormal_elements_give_zero_force():
 def test_rn_of_y_is_correctly_rounded():
     """fe = c1·(RN(y)·s·2^-56 + c2 u): recompute with Python's correctly rounded int→float."""
     for (u, kappa, G, ds) in _elem_inputs(5, 30):
-        r = oracle.element_int8(u, kappa, G, ds)
+        r = oracle.element_int8(u, kappa, G, ds, 8, oracle.DIGITS_BYTES)
         c1 = kappa * ds / 256.0
         c2 = (256.0 * G) / (3.0 * kappa)
         sig = r["s"] * 2.0 ** -56
         for i in range(24):
             assert r["fe"][i] == c1 * (float(r["y"][i]) * sig + c2 * u[i])
+
+
+# ---- variant D (Eq. 9 diagonal term folded into the integer product) -----------------
+
+def test_fold_variant_integer_identity_and_bound():
+    """y_D = K_D v with K_D = [K^κ | K̄^G + 128 I] (big integers), and f within the truncation
+    bound of the exact Eq. 9 value (one extra 128·s·2^-56 term from truncating ū_G)."""
+    KD = [row[:24] + [row[24 + c] + (128 if c == r else 0) for c in range(24)] for r, row in enumerate(K8)]
+    for (u, kappa, G, ds) in _elem_inputs(6, 40):
+        r = oracle.element_int8(u, kappa, G, ds, 8, oracle.DIGITS_BYTES_FOLD)
+        v = [int(x) for x in r["v"]]
+        for i in range(24):
+            assert r["y"][i] == sum(KD[i][k] * v[k] for k in range(48))
+        ex = _exact_eq9(u, kappa, G, ds)
+        c1, s = kappa * ds / 256, r["s"]
+        for i in range(24):
+            err = abs(Fr(r["fe"][i]) - ex[i])
+            bound = Fr(c1 * s) * Fr(2) ** -56 * (1130 + 128) * 34 + 8 * Fr(math.ulp(abs(float(ex[i])) + c1 * s))
+            assert err <= bound
+
+
+def test_fold_variant_matches_literal_to_fp64_precision_and_is_odd():
+    for (u, kappa, G, ds) in _elem_inputs(8, 40):
+        a = oracle.element_int8(u, kappa, G, ds, 8, oracle.DIGITS_BYTES_FOLD)
+        b = oracle.element_int8(u, kappa, G, ds, 8, oracle.DIGITS_BYTES)
+        sc = kappa * ds / 256 * a["s"] * 1300
+        assert np.abs(a["fe"] - b["fe"]).max() <= 2.0 ** -48 * sc
+        n = oracle.element_int8(-u, kappa, G, ds, 8, oracle.DIGITS_BYTES_FOLD)
+        assert np.array_equal(a["fe"], -n["fe"])
