@@ -44,10 +44,11 @@ constexpr int B1_PITCH = 6 * 128;                // main B: 48 rows × 96 K-byte
 constexpr int BI_PITCH = 2 * 128;                // identity blocks: 48 rows × 32 K-bytes
 
 struct SmemV1I8 {
-    union {
+    struct {
         uint8_t A[2][4][A1_BYTES];   // [M-tile][half-word array], K-major canonical layout
-        double fe[24][256];          // aliases M-tile 0's arrays (dead after its MMAs complete)
     } u;
+    double fe[24][256];              // separate from A: one M-tile's epilogue may run while the
+                                     // other M-tile's MMAs still read their A arrays
     alignas(128) uint8_t B[6 * B1_PITCH];
     alignas(128) uint8_t BI[2][6 * BI_PITCH];
     double up[3][V1<OVX_INT8>::PLANE];
@@ -56,12 +57,11 @@ struct SmemV1I8 {
     uint64_t mbar[2];
     uint32_t tmem;
 };
-static_assert(sizeof(double) * 24 * 256 <= 4 * A1_BYTES, "fe must alias inside M-tile 0's A arrays");
 
 template <int PATH>
 using SmemV1 = typename std::conditional<PATH == OVX_INT8, SmemV1I8, SmemV1F64>::type;
 
-__device__ __forceinline__ double (*fe_of(SmemV1I8 &S))[256] { return S.u.fe; }
+__device__ __forceinline__ double (*fe_of(SmemV1I8 &S))[256] { return S.fe; }
 __device__ __forceinline__ double (*fe_of(SmemV1F64 &S))[256] { return S.fe; }
 
 template <int PATH>
@@ -303,15 +303,17 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                 }
                 if (MODE == MODE_DEBUG && dbg && half == 0 && p.dbg_s) p.dbg_s[dj] = s;
 
-                // ---- Eq. 17 (+ folded diagonal): 2 M-tiles × 4 arrays × (3 + 2) K-steps, M128 N48 K32 ----
+                // ---- Eq. 17 (+ folded diagonal): this M-tile, 4 arrays × (3 + 2) K-steps, M128 N48 K32 ----
+                // Each M-tile (8 warps) hands off to the tensor core on its own named barrier, so one
+                // M-tile's MMAs overlap the other M-tile's digit or epilogue work.
                 ptx::fence_proxy_async_smem();
-                __syncthreads();
-                if (t == 0) {
+                asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");
+                if (t == 256 * mt) {
                     ptx::tc_fence_after();
                     const uint32_t b0 = ptx::smem_u32(&S.B[0]);
                     const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
-#pragma unroll
-                    for (int mm = 0; mm < 2; ++mm) {
+                    {
+                        const int mm = mt;
                         const uint32_t a0 = ptx::smem_u32(&S.u.A[mm][0][0]);
 #pragma unroll
                         for (int pa = 0; pa < 4; ++pa) {
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                         ptx::mma_commit(&S.mbar[mm]);
                     }
                 }
-                ptx::mbar_wait(&S.mbar[mt], phase);
+                ptx::mbar_wait_sleep(&S.mbar[mt], phase);
                 phase ^= 1;
                 ptx::tc_fence_after();
 
@@ -353,10 +355,11 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                         const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
                         const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
                         const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
-                        const long long blo = 0x4338000000000000ll + (long long)c0 + (long long)c1_ * 256ll +
-                                              (long long)c2_ * 65536ll + (long long)c3 * 16777216ll;
-                        const long long bhi = 0x4338000000000000ll + (long long)c4 + (long long)c5 * 256ll +
-                                              (long long)c6 * 65536ll + (long long)c7 * 16777216ll;
+                        const long long MAGIC = 0x4338000000000000ll;
+                        const long long blo = ptx::mad_wide(c3, 16777216, ptx::mad_wide(c2_, 65536,
+                                              ptx::mad_wide(c1_, 256, ptx::mad_wide(c0, 1, MAGIC))));
+                        const long long bhi = ptx::mad_wide(c7, 16777216, ptx::mad_wide(c6, 65536,
+                                              ptx::mad_wide(c5, 256, ptx::mad_wide(c4, 1, MAGIC))));
                         const double dlo = __longlong_as_double(blo) - 0x1.8p52;
                         const double dhi = __longlong_as_double(bhi) - 0x1.8p52;
                         const double Y = __fma_rn(dhi, 0x1p32, dlo);    // RN(−y)
@@ -373,8 +376,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                             if (p.dbg_ylo) p.dbg_ylo[dj * 24 + i] = (long long)(unsigned long long)y;
                             if (p.dbg_fe) p.dbg_fe[dj * 24 + i] = f;
                         }
-                        // fe aliases M-tile 0's A: written only after this M-tile's MMAs completed
-                        S.u.fe[i][el] = f;
+                        S.fe[i][el] = f;
                     }
                 }
                 ptx::tc_fence_before();
