@@ -62,6 +62,7 @@ def lib() -> ctypes.CDLL:
     L.oracle_run.restype = _int
     L.oracle_element_nodes.argtypes = [_i64, _i64, _i64, _i64p]
     L.oracle_digits.argtypes = [_i64, _int, _int, _i32p]
+    L.oracle_update_dofs.argtypes = [_i64, _dp, _dp, _dp, _dp, _dp]
     return L
 
 
@@ -95,6 +96,13 @@ def digits(v: int, M: int = 8, scheme: int = DIGITS_BYTES) -> list[int]:
     out = np.zeros(8, dtype=np.int32)
     lib().oracle_digits(int(v), M, scheme, _p(out, _i32p))
     return [int(x) for x in out[:nd]]
+
+
+def update_dofs(w, F, f, u, up) -> None:
+    """up <- fma(w, F - f, 2u - up) elementwise (Eq. 3), in place."""
+    args = [np.ascontiguousarray(a, dtype=np.float64) for a in (w, F, f, u)]
+    assert up.flags["C_CONTIGUOUS"] and up.dtype == np.float64
+    lib().oracle_update_dofs(len(up), *[_p(a, _dp) for a in args], _p(up, _dp))
 
 
 def node_w(nx, ny, nz, ds, mat, rho, dt) -> np.ndarray:

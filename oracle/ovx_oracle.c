@@ -253,3 +253,13 @@ int oracle_run(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat
     free(F);
     return status;
 }
+
+/* Central-difference update of n DOFs (Eq. 3): up[i] <- fma(w[i], F[i] - f[i], 2u[i] - up[i]).
+ * Used by the z-slab protocol emulation in the tests. */
+void oracle_update_dofs(int64_t n, const double *w, const double *F, const double *f, const double *u,
+                        double *up) {
+    for (int64_t i = 0; i < n; ++i) {
+        double b = 2.0 * u[i] - up[i];
+        up[i] = fma(w[i], F[i] - f[i], b);
+    }
+}

@@ -39,6 +39,12 @@ struct ovx_ctx {
     int64_t it = 0;
     std::vector<EventPair> ev_used, ev_free;
     int64_t launches = 0;
+    // z-slab (multi-GPU) state
+    int slab_flags = 0;
+    uint8_t *d_mat_below = nullptr;
+    double *d_bot_b = nullptr;
+    double *a_send = nullptr, *a_recv = nullptr, *u_send = nullptr, *u_recv = nullptr;
+    int64_t nn2() const { return (nx + 1) * (ny + 1); }
     int64_t nn() const { return (nx + 1) * (ny + 1) * (nz + 1); }
     int64_t ne() const { return nx * ny * nz; }
 };
@@ -77,7 +83,8 @@ ovx_status refresh_w(ovx_ctx *ctx) {
     if (!ctx->setup || !(ctx->dt > 0)) return OVX_OK;
     ovx_status s = ensure_constants(ctx);
     if (s) return s;
-    CK(launch_node_w(ctx->nx, ctx->ny, ctx->nz, ctx->d_mat, ctx->dt, ctx->d_w, ctx->stream));
+    CK(launch_node_w(ctx->nx, ctx->ny, ctx->nz, ctx->d_mat, (ctx->slab_flags & 1) ? ctx->d_mat_below : nullptr,
+                     ctx->dt, ctx->d_w, ctx->stream));
     return OVX_OK;
 }
 
@@ -147,6 +154,8 @@ ovx_status ovx_destroy(ovx_ctx *ctx) {
     dfree(ctx->d_u);
     dfree(ctx->d_up);
     dfree(ctx->d_w);
+    dfree(ctx->d_mat_below);
+    dfree(ctx->d_bot_b);
     for (auto &p : ctx->ev_used) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto &p : ctx->ev_free) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -187,6 +196,12 @@ ovx_status ovx_set_grid(ovx_ctx *ctx, int64_t nx, int64_t ny, int64_t nz, double
     ctx->d_mat = nullptr;
     ctx->d_mask = nullptr;
     ctx->d_u = ctx->d_up = ctx->d_w = nullptr;
+    dfree(ctx->d_mat_below);
+    dfree(ctx->d_bot_b);
+    ctx->d_mat_below = nullptr;
+    ctx->d_bot_b = nullptr;
+    ctx->slab_flags = 0;
+    ctx->a_send = ctx->a_recv = ctx->u_send = ctx->u_recv = nullptr;
     ctx->nx = nx;
     ctx->ny = ny;
     ctx->nz = nz;
@@ -394,6 +409,7 @@ ovx_status ovx_step(ovx_ctx *ctx, int64_t n) {
     if (s) return s;
     if (!(ctx->dt > 0)) return fail(ctx, OVX_ESTATE, "set dt first");
     if (n < 0) return fail(ctx, OVX_EINVAL, "n must be >= 0");
+    if (ctx->slab_flags) return fail(ctx, OVX_ESTATE, "slab contexts step with ovx_step_begin/iface/end");
     if (n == 0) return OVX_OK;
     cudaSetDevice(ctx->device);
     s = ensure_constants(ctx);
@@ -423,6 +439,93 @@ ovx_status ovx_step(ovx_ctx *ctx, int64_t n) {
     }
     CK(cudaEventRecord(ev.b, ctx->stream));
     ctx->ev_used.push_back(ev);
+    return OVX_OK;
+}
+
+ovx_status ovx_set_slab(ovx_ctx *ctx, int flags, const uint8_t *mat_below) {
+    if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
+    if (!ctx->have_grid || ctx->nmat == 0) return fail(ctx, OVX_ESTATE, "set grid and materials first");
+    if (flags < 0 || flags > 3) return fail(ctx, OVX_EINVAL, "slab flags must be in 0..3");
+    if ((flags & 1) && !mat_below) return fail(ctx, OVX_EINVAL, "a lower neighbour needs the halo materials");
+    cudaSetDevice(ctx->device);
+    const int64_t ne2 = ctx->nx * ctx->ny;
+    if (flags & 1) {
+        for (int64_t e = 0; e < ne2; ++e)
+            if (mat_below[e] >= ctx->nmat) return fail(ctx, OVX_EINVAL, "unknown material id in the halo layer");
+        if (!ctx->d_mat_below && cudaMalloc(&ctx->d_mat_below, ne2) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, OVX_ENOMEM, "halo allocation failed");
+        }
+        if (!ctx->d_bot_b && cudaMalloc(&ctx->d_bot_b, 8 * 12 * ctx->nn2()) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, OVX_ENOMEM, "interface allocation failed");
+        }
+        CK(cudaMemcpyAsync(ctx->d_mat_below, mat_below, ne2, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    ctx->slab_flags = flags;
+    return refresh_w(ctx);
+}
+
+ovx_status ovx_set_iface_buffers(ovx_ctx *ctx, double *a_send, double *a_recv, double *u_send, double *u_recv) {
+    if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
+    if (((ctx->slab_flags & 2) && !a_send) || ((ctx->slab_flags & 1) && (!a_recv || !u_send)) ||
+        ((ctx->slab_flags & 2) && !u_recv))
+        return fail(ctx, OVX_EINVAL, "missing interface buffer for the slab flags");
+    ctx->a_send = a_send;
+    ctx->a_recv = a_recv;
+    ctx->u_send = u_send;
+    ctx->u_recv = u_recv;
+    return OVX_OK;
+}
+
+static StepParams step_params(ovx_ctx *ctx) {
+    StepParams p = base_params(ctx);
+    p.u = ctx->d_u;
+    p.uo = ctx->d_up;
+    p.nsrc = ctx->nsrc;
+    for (int q = 0; q < ctx->nsrc; ++q) {
+        p.src_dof[q] = 3 * ctx->src_node[q] + ctx->src_axis[q];
+        p.src_val[q] = (ctx->it < ctx->n_t) ? ctx->amp[(size_t)q * ctx->n_t + ctx->it] : 0.0;
+    }
+    p.slab_flags = ctx->slab_flags;
+    p.iface_top_A = ctx->a_send;
+    p.iface_bot_b = ctx->d_bot_b;
+    return p;
+}
+
+ovx_status ovx_step_begin(ovx_ctx *ctx) {
+    ovx_status s = need_ready(ctx);
+    if (s) return s;
+    if (!(ctx->dt > 0)) return fail(ctx, OVX_ESTATE, "set dt first");
+    if (((ctx->slab_flags & 2) && !ctx->a_send) || ((ctx->slab_flags & 1) && !ctx->d_bot_b))
+        return fail(ctx, OVX_ESTATE, "interface buffers not set");
+    cudaSetDevice(ctx->device);
+    s = ensure_constants(ctx);
+    if (s) return s;
+    CK(launch_step(ctx->path, MODE_STEP, step_params(ctx), ctx->stream));
+    ctx->launches += 1;
+    return OVX_OK;
+}
+
+ovx_status ovx_step_iface(ovx_ctx *ctx) {
+    ovx_status s = need_ready(ctx);
+    if (s) return s;
+    if (!(ctx->slab_flags & 1)) return OVX_OK;
+    cudaSetDevice(ctx->device);
+    CK(launch_iface_update(step_params(ctx), ctx->a_recv, ctx->u_send, ctx->stream));
+    return OVX_OK;
+}
+
+ovx_status ovx_step_end(ovx_ctx *ctx) {
+    ovx_status s = need_ready(ctx);
+    if (s) return s;
+    cudaSetDevice(ctx->device);
+    if (ctx->slab_flags & 2)   // the owner above sent the updated top plane
+        CK(cudaMemcpyAsync(ctx->d_up + 3 * ctx->nn2() * ctx->nz, ctx->u_recv, 24 * ctx->nn2(),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    std::swap(ctx->d_u, ctx->d_up);
+    ctx->it += 1;
     return OVX_OK;
 }
 

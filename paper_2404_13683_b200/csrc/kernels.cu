@@ -211,8 +211,8 @@ cudaError_t launch_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_
     return launch_t<PATH, MODE_DEBUG>(p, ctas, st);
 }
 
-__global__ void node_w_kernel(int64_t nx, int64_t ny, int64_t nz, const uint8_t *__restrict__ mat, double dt,
-                              double *__restrict__ w) {
+__global__ void node_w_kernel(int64_t nx, int64_t ny, int64_t nz, const uint8_t *__restrict__ mat,
+                              const uint8_t *__restrict__ mat_below, double dt, double *__restrict__ w) {
     const int64_t NX1 = nx + 1, NY1 = ny + 1, nn = NX1 * NY1 * (nz + 1);
     for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn; n += (int64_t)gridDim.x * blockDim.x) {
         const int64_t ix = n % NX1, iy = (n / NX1) % NY1, iz = n / (NX1 * NY1);
@@ -222,7 +222,11 @@ __global__ void node_w_kernel(int64_t nx, int64_t ny, int64_t nz, const uint8_t 
             for (int dy = -1; dy <= 0; ++dy)
                 for (int dx = -1; dx <= 0; ++dx) {
                     const int64_t ex = ix + dx, ey = iy + dy, ez = iz + dz;
-                    if (ex < 0 || ex >= nx || ey < 0 || ey >= ny || ez < 0 || ez >= nz) continue;
+                    if (ex < 0 || ex >= nx || ey < 0 || ey >= ny || ez >= nz) continue;
+                    if (ez < 0) {   // element layer below the slab (z-slab halo), if any
+                        if (mat_below) m = __dadd_rn(m, c_mat[mat_below[ex + nx * ey]].rho_vol8);
+                        continue;
+                    }
                     m = __dadd_rn(m, c_mat[mat[ex + nx * (ey + ny * ez)]].rho_vol8);
                 }
         w[n] = __ddiv_rn(__dmul_rn(dt, dt), m);
@@ -282,9 +286,37 @@ cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
     return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);
 }
 
-cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, double dt, double *w,
-                          cudaStream_t st) {
-    node_w_kernel<<<1184, 256, 0, st>>>(nx, ny, nz, mat, dt, w);
+cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, const uint8_t *mat_below,
+                          double dt, double *w, cudaStream_t st) {
+    node_w_kernel<<<1184, 256, 0, st>>>(nx, ny, nz, mat, mat_below, dt, w);
+    return cudaGetLastError();
+}
+
+// Interface plane (local plane 0) of a z-slab: continue the received partial A of the layer
+// below with this rank's 4 layer-0 contributions in global element order, then update.
+__global__ void iface_update_kernel(const StepParams p, const double *__restrict__ a_recv, double *__restrict__ u_send) {
+    const int64_t nn2 = (p.nx + 1) * (p.ny + 1);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nn2; j += (int64_t)gridDim.x * blockDim.x) {
+        const double wn = p.w[j];
+        const uint8_t dm = p.dmask ? p.dmask[j] : (uint8_t)0;
+        for (int c = 0; c < 3; ++c) {
+            double f = a_recv[3 * j + c];
+            for (int k = 0; k < 4; ++k) f = __dadd_rn(f, p.iface_bot_b[12 * j + 3 * k + c]);
+            const int64_t dof = 3 * j + c;
+            double F = 0.0;
+            for (int k = 0; k < p.nsrc; ++k)
+                if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
+            const double b = __dsub_rn(__dmul_rn(2.0, p.u[dof]), p.uo[dof]);
+            double un = __fma_rn(wn, __dsub_rn(F, f), b);
+            if ((dm >> c) & 1) un = 0.0;
+            p.uo[dof] = un;
+            u_send[dof] = un;
+        }
+    }
+}
+
+cudaError_t launch_iface_update(const StepParams &p, const double *a_recv, double *u_send, cudaStream_t st) {
+    iface_update_kernel<<<296, 256, 0, st>>>(p, a_recv, u_send);
     return cudaGetLastError();
 }
 

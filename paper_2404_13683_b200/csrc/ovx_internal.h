@@ -32,6 +32,12 @@ struct StepParams {
     int nsrc;
     int64_t src_dof[kMaxSrc];
     double src_val[kMaxSrc];
+    // z-slab decomposition (multi-GPU): bit 0 = local plane 0 is an interface
+    // owned by this rank (its lower-layer partial arrives from below), bit 1 = the top local
+    // plane is an interface owned by the rank above (send its partial, do not update it)
+    int slab_flags;
+    double *iface_top_A;   // [NX1*NY1][3]   partial force of the top plane (bit 1)
+    double *iface_bot_b;   // [NX1*NY1][4][3] the 4 layer-0 contributions to plane 0 (bit 0)
     // tiling
     int tiles_x, tiles_y, zchunk;
     // MODE_DEBUG outputs for elements [dbg_e0, dbg_e0 + dbg_ne)
@@ -55,8 +61,9 @@ cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, c
                              const double *kg, cudaStream_t st);
 LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz);
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st);
-cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, double dt, double *w,
-                          cudaStream_t st);
+cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, const uint8_t *mat_below,
+                          double dt, double *w, cudaStream_t st);
+cudaError_t launch_iface_update(const StepParams &p, const double *a_recv, double *u_send, cudaStream_t st);
 cudaError_t launch_finite_check(const double *u, int64_t n, int *flag, cudaStream_t st);
 
 // element_setup.cpp

@@ -182,9 +182,13 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
     __syncthreads();
     if constexpr (PATH == OVX_INT8) ptx::tc_fence_after();
 
+    // material of this thread's element in the current layer (prefetched one layer ahead;
+    // elements outside the domain use the reserved zero material)
+    int mcur = (ein && Lfirst < p.nz) ? (int)__ldg(matcol + mstride * Lfirst) : kZeroMat;
     for (int64_t L = Z0 - 1; L < Z1; ++L) {
         const bool layer_ok = (L >= 0 && L < p.nz);
         const bool plane_done = (L >= Z0 && L <= p.nz);
+        const int mnext = (ein && L + 1 > Lfirst && L + 1 < p.nz) ? (int)__ldg(matcol + mstride * (L + 1)) : kZeroMat;
         // ---- (1) prefetch: plane L+2 (needed by layer L+1) and the update operands of plane L ----
         const int64_t pz = L + 2;
         const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < p.nz);
@@ -207,8 +211,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
         // ---- (2) element forces of layer L ----
         if (layer_ok) {
             const double *plo = S.up[L % 3], *phi = S.up[(L + 1) % 3];
-            // material of this element; elements outside the domain use the reserved zero material
-            const int m = ein ? (int)__ldg(matcol + mstride * L) : kZeroMat;
+            const int m = mcur;
             const int64_t eid = ex + p.nx * (ey + p.ny * L);
             const int64_t dj = eid - p.dbg_e0;
             const bool dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
@@ -355,13 +358,8 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                         const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
                         const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
                         const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
-                        const long long MAGIC = 0x4338000000000000ll;
-                        const long long blo = ptx::mad_wide(c3, 16777216, ptx::mad_wide(c2_, 65536,
-                                              ptx::mad_wide(c1_, 256, ptx::mad_wide(c0, 1, MAGIC))));
-                        const long long bhi = ptx::mad_wide(c7, 16777216, ptx::mad_wide(c6, 65536,
-                                              ptx::mad_wide(c5, 256, ptx::mad_wide(c4, 1, MAGIC))));
-                        const double dlo = __longlong_as_double(blo) - 0x1.8p52;
-                        const double dhi = __longlong_as_double(bhi) - 0x1.8p52;
+                        const double dlo = ptx::limb_magic(c0, c1_, c2_, c3) - (0x1.8p52 + 0x1p31);
+                        const double dhi = ptx::limb_magic(c4, c5, c6, c7) - (0x1.8p52 + 0x1p31);
                         const double Y = __fma_rn(dhi, 0x1p32, dlo);    // RN(−y)
                         const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
                         if (MODE == MODE_DEBUG && dbg) {
@@ -390,7 +388,19 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             const int e00 = nxl + EX * nyl, e10 = e00 + 1, e01 = e00 + EX, e11 = e01 + 1;
             double *fl = &S.facc[L & 1][t * 3];
             double *fh = &S.facc[(L + 1) & 1][t * 3];
-            if (layer_ok && L >= Z0) {     // bottom corners of layer L -> plane L
+            const bool bot_iface = (p.slab_flags & 1) && L == 0;             // plane 0 owned, partial from below
+            const bool top_iface = (p.slab_flags & 2) && L == p.nz;          // plane owned by the rank above
+            if (layer_ok && L >= Z0 && bot_iface) {   // keep the 4 contributions for the interface update
+                if (own)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        double *b = p.iface_bot_b + 12 * ucol + c;
+                        b[0] = fe[3 * 2 + c][e00];
+                        b[3] = fe[3 * 3 + c][e10];
+                        b[6] = fe[3 * 1 + c][e01];
+                        b[9] = fe[3 * 0 + c][e11];
+                    }
+            } else if (layer_ok && L >= Z0) {     // bottom corners of layer L -> plane L
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     double f = fl[c];
@@ -412,7 +422,10 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                     fh[c] = f;
                 }
             }
-            if (upd) {
+            if (upd && top_iface) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = fl[c];
+            } else if (upd && !bot_iface) {
                 const double *up = &S.up[L % 3][((nyl + 1) * PX + (nxl + 1)) * 3];
                 if (MODE == MODE_STEP) {
 #pragma unroll
@@ -434,6 +447,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             }
             if (plane_done) fl[0] = fl[1] = fl[2] = 0.0;
         }
+        if (L >= Lfirst) mcur = mnext;
         // ---- (4) park the prefetched plane L+2 (slot of plane L-1, no longer read) ----
         if (pf) {
             double *dst = S.up[pz % 3];

@@ -56,6 +56,11 @@ _SIGS = {
     "ovx_get_node_w": [_vp, _vp],
     "ovx_get_timers": [_vp, _vp, _vp, _int],
     "ovx_get_launch_config": [_vp, _vp, _vp, _vp],
+    "ovx_set_slab": [_vp, _int, _vp],
+    "ovx_set_iface_buffers": [_vp, _vp, _vp, _vp, _vp],
+    "ovx_step_begin": [_vp],
+    "ovx_step_iface": [_vp],
+    "ovx_step_end": [_vp],
 }
 EXPORTS = tuple(_SIGS) + ("ovx_last_error", "ovx_version")
 
@@ -258,6 +263,26 @@ class Ovx:
         s = np.zeros(1, dtype=np.int32)
         self._call("ovx_get_launch_config", _np_ptr(c), _np_ptr(t), _np_ptr(s))
         return int(c[0]), int(t[0]), int(s[0])
+
+    def set_slab(self, flags: int, mat_below=None) -> None:
+        mb = None if mat_below is None else _host(mat_below, np.uint8)
+        if mb is not None and mb.size != self.nx * self.ny:
+            raise OvxError(OVX_EINVAL, "halo material layer size mismatch")
+        self._call("ovx_set_slab", flags, None if mb is None else _np_ptr(mb))
+
+    def set_iface_buffers(self, a_send=None, a_recv=None, u_send=None, u_recv=None) -> None:
+        ptr = lambda t: None if t is None else _vp(_dev_ptr(t))
+        self._iface = (a_send, a_recv, u_send, u_recv)   # keep the tensors alive
+        self._call("ovx_set_iface_buffers", ptr(a_send), ptr(a_recv), ptr(u_send), ptr(u_recv))
+
+    def step_begin(self) -> None:
+        self._call("ovx_step_begin")
+
+    def step_iface(self) -> None:
+        self._call("ovx_step_iface")
+
+    def step_end(self) -> None:
+        self._call("ovx_step_end")
 
     # -- convenience ---------------------------------------------------------------
     def load_model(self, m, path: int = OVX_INT8) -> None:
