@@ -190,6 +190,7 @@ __device__ __forceinline__ void element_force_wht(const double (&ue)[24], const 
 }
 
 #include "step_v1.cuh"
+#include "step_f64.cuh"
 
 template <int PATH, int MODE>
 cudaError_t launch_t(const StepParams &p, int64_t ctas, cudaStream_t st) {
@@ -204,8 +205,25 @@ cudaError_t launch_t(const StepParams &p, int64_t ctas, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+template <int MODE>
+cudaError_t launch_f64(const StepParams &p, int64_t ctas, cudaStream_t st) {
+    static bool attr = false;
+    const int smem = (int)sizeof(SmemF2);
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(step_f64<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    step_f64<MODE><<<(unsigned)ctas, F2::NT, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
 template <int PATH>
 cudaError_t launch_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
+    if constexpr (PATH == OVX_FP64) {   // dedicated shuffle/register kernel; debug records via step_v1
+        if (mode == MODE_STEP && p.slab_flags == 0) return launch_f64<MODE_STEP>(p, ctas, st);
+        if (mode == MODE_APPLY) return launch_f64<MODE_APPLY>(p, ctas, st);
+    }
     if (mode == MODE_STEP) return launch_t<PATH, MODE_STEP>(p, ctas, st);
     if (mode == MODE_APPLY) return launch_t<PATH, MODE_APPLY>(p, ctas, st);
     return launch_t<PATH, MODE_DEBUG>(p, ctas, st);
@@ -245,10 +263,10 @@ LaunchInfo info_t(int64_t nx, int64_t ny, int64_t nz) {
     using C = V1<PATH>;
     LaunchInfo li;
     const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + C::TY - 1) / C::TY;
-    const int64_t tz = (nz + 1 + kZChunk - 1) / kZChunk;
+    const int64_t tz = (nz + 1 + kZChunk - 1) / kZChunk;   // balanced chunks (see launch_step)
     li.ctas = tx * ty * tz;
     li.threads = C::NT;
-    li.smem = (int)sizeof(SmemV1<PATH>);
+    li.smem = PATH == OVX_FP64 ? (int)sizeof(SmemF2) : (int)sizeof(SmemV1<PATH>);
     return li;
 }
 
@@ -278,7 +296,8 @@ cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
     const int ty = V1<OVX_INT8>::TY;   // same tile height for every path
     p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
     p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
-    p.zchunk = kZChunk;
+    const int64_t nchunk = (p.nz + 1 + kZChunk - 1) / kZChunk;        // chunks of <= 64 planes,
+    p.zchunk = (int)((p.nz + 1 + nchunk - 1) / nchunk);                 // balanced in size
     const int64_t tz = (p.nz + 1 + p.zchunk - 1) / p.zchunk;
     const int64_t ctas = (int64_t)p.tiles_x * p.tiles_y * tz;
     if (path == OVX_INT8) return launch_mode<OVX_INT8>(mode, p, ctas, st);

@@ -1,0 +1,186 @@
+// step_f64.cuh — fused time step for the factored FP64 path (OVX_FP64); included by kernels.cu.
+//
+// Same tiling and z-march as step_v1 (32×8 elements per layer, owned nodes 31×7, one halo ring),
+// but no per-element force staging in shared memory:
+//   * thread (lane = lx, warp = ly) computes element (lx, ly) with the Walsh-Hadamard factored
+//     K_e^o u_e (element_force_wht, ≈180 FP64 ops);
+//   * contributions are summed along x with one warp shuffle (the +x corners of lane lx-1 meet
+//     the -x corners of lane lx), along y through a 6-double-per-thread smem row exchange;
+//   * thread (lx, ly) owns node (lx, ly) of the tile (lx, ly >= 1) and keeps its plane-L and
+//     plane-(L+1) force accumulators in registers across the z-march; the completed plane is
+//     updated in place (Eq. 3 / L263-L266 with the sign of Eq. 3).
+// The summation order differs from the oracle's element order (parity: tolerance).
+
+struct F2 {
+    static constexpr int EY = 8;
+    static constexpr int NT = EX * EY;                 // 256 threads = elements per layer
+    static constexpr int TY = EY - 1;
+    static constexpr int PY = EY + 1;
+    static constexpr int PLANE = PX * PY * 3;          // 891 doubles
+    static constexpr int PF = (PLANE + NT - 1) / NT;   // 4
+};
+
+struct SmemF2 {
+    double up[3][F2::PLANE];
+    double ysum[F2::EY][EX][6];    // +y-corner x-sums of each element row, for the row above
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
+    constexpr int NT = F2::NT, TY = F2::TY, PLANE = F2::PLANE, PF = F2::PF;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    SmemF2 &S = *reinterpret_cast<SmemF2 *>(smem_raw);
+    const int t = threadIdx.x;
+    const int lx = t & 31, ly = t >> 5;
+
+    int bid = blockIdx.x;
+    const int tx = bid % p.tiles_x;
+    bid /= p.tiles_x;
+    const int ty = bid % p.tiles_y;
+    const int tz = bid / p.tiles_y;
+    const int64_t X0 = (int64_t)tx * TX, Y0 = (int64_t)ty * TY;
+    const int64_t Z0 = (int64_t)tz * p.zchunk;
+    const int64_t Z1 = min(Z0 + (int64_t)p.zchunk, p.nz + 1);
+    const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1, PSTRIDE = NX1 * NY1;
+
+    const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
+    const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
+    const uint8_t *matcol = p.mat + (ein ? ex + p.nx * ey : 0);
+    const int64_t mstride = p.nx * p.ny;
+
+    int64_t pfoff[PF];
+    bool pfok[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+        const int idx = t + j * NT;
+        const int py = idx / (PX * 3);
+        const int rem = idx - py * (PX * 3);
+        const int px = rem / 3, c = rem - px * 3;
+        const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
+        pfok[j] = idx < PLANE && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1;
+        pfoff[j] = pfok[j] ? 3 * (ix + NX1 * iy) + c : 0;
+    }
+    // owned node of this thread: tile node (lx, ly) = global (X0-1+lx, Y0-1+ly), lx, ly >= 1
+    const int64_t uix = X0 - 1 + lx, uiy = Y0 - 1 + ly;
+    const bool own = lx >= 1 && ly >= 1 && uix < NX1 && uiy < NY1;
+    const int64_t ucol = own ? uix + NX1 * uiy : 0;
+
+    bool has_src = false;
+    if (MODE == MODE_STEP)
+        for (int k = 0; k < p.nsrc; ++k) {
+            const int64_t n = p.src_dof[k] / 3;
+            const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+            has_src |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
+        }
+
+    const int64_t Lfirst = max(Z0 - 1, (int64_t)0);
+    // synchronous first two planes
+    for (int j = 0; j < 2; ++j) {
+        const int64_t iz = Lfirst + j;
+        double *dst = S.up[iz % 3];
+        for (int idx = t; idx < PLANE; idx += NT) {
+            const int py = idx / (PX * 3);
+            const int rem = idx - py * (PX * 3);
+            const int px = rem / 3, c = rem - px * 3;
+            const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
+            dst[idx] = (iz <= p.nz && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1)
+                           ? __ldg(p.u + 3 * (ix + NX1 * (iy + NY1 * iz)) + c) : 0.0;
+        }
+    }
+    __syncthreads();
+
+    double facc[3] = {0.0, 0.0, 0.0};   // plane L (receives layer L-1 top + layer L bottom)
+    int mcur = (ein && Lfirst < p.nz) ? (int)__ldg(matcol + mstride * Lfirst) : kZeroMat;
+    for (int64_t L = Z0 - 1; L < Z1; ++L) {
+        const bool layer_ok = (L >= 0 && L < p.nz);
+        const bool plane_done = (L >= Z0 && L <= p.nz);
+        const int mnext = (ein && L + 1 > Lfirst && L + 1 < p.nz) ? (int)__ldg(matcol + mstride * (L + 1)) : kZeroMat;
+        // ---- prefetch plane L+2 and the update operands of plane L ----
+        const int64_t pz = L + 2;
+        const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < p.nz);
+        double pfv[PF];
+        const double *uplane = p.u + 3 * PSTRIDE * pz;
+#pragma unroll
+        for (int j = 0; j < PF; ++j) pfv[j] = (pf && pfok[j]) ? __ldg(uplane + pfoff[j]) : 0.0;
+        const bool upd = plane_done && own;
+        const int64_t un_id = ucol + PSTRIDE * L;
+        double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;
+        uint8_t dm = 0;
+        if (MODE == MODE_STEP && upd) {
+            upv[0] = p.uo[3 * un_id];
+            upv[1] = p.uo[3 * un_id + 1];
+            upv[2] = p.uo[3 * un_id + 2];
+            wn = __ldg(p.w + un_id);
+            dm = p.dmask ? __ldg(p.dmask + un_id) : (uint8_t)0;
+        }
+
+        double nbot[3] = {0.0, 0.0, 0.0}, ntop[3] = {0.0, 0.0, 0.0};
+        if (layer_ok) {
+            double ue[24], fe[24];
+            gather<F2::PY>(ue, S.up[L % 3], S.up[(L + 1) % 3], lx, ly);
+            element_force_wht(ue, c_mat[mcur], fe);     // zero material outside the domain
+            // x-sums at this element's -x node column: own -x corners + lane lx-1's +x corners
+            // local nodes: (-x,-y)=0,4  (+x,-y)=1,5  (+x,+y)=2,6  (-x,+y)=3,7   (bottom, top)
+            double xs[12];   // [dy][dz][c]
+#pragma unroll
+            for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double pm = __shfl_up_sync(0xffffffffu, fe[3 * (1 + 4 * dz) + c], 1);  // (+x,-y) of lx-1
+                    const double pp = __shfl_up_sync(0xffffffffu, fe[3 * (2 + 4 * dz) + c], 1);  // (+x,+y) of lx-1
+                    xs[0 * 6 + dz * 3 + c] = fe[3 * (0 + 4 * dz) + c] + (lx > 0 ? pm : 0.0);
+                    xs[1 * 6 + dz * 3 + c] = fe[3 * (3 + 4 * dz) + c] + (lx > 0 ? pp : 0.0);
+                }
+#pragma unroll
+            for (int q = 0; q < 6; ++q) S.ysum[ly][lx][q] = xs[6 + q];
+            __syncthreads();
+            if (ly > 0) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    nbot[c] = xs[c] + S.ysum[ly - 1][lx][c];
+                    ntop[c] = xs[3 + c] + S.ysum[ly - 1][lx][3 + c];
+                }
+            }
+        } else {
+            __syncthreads();
+        }
+        if (L >= Z0) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) facc[c] += nbot[c];
+        }
+        // ---- plane L complete: update ----
+        if (upd) {
+            const double *up = &S.up[L % 3][(ly * PX + lx) * 3];
+            if (MODE == MODE_STEP) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int64_t dof = 3 * un_id + c;
+                    double F = 0.0;
+                    if (has_src)
+                        for (int k = 0; k < p.nsrc; ++k)
+                            if (p.src_dof[k] == dof) F += p.src_val[k];
+                    double un = fma(wn, F - facc[c], 2.0 * up[c] - upv[c]);
+                    if ((dm >> c) & 1) un = 0.0;
+                    p.uo[dof] = un;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) p.fout[3 * un_id + c] = facc[c];
+            }
+        }
+        if (L + 1 < Z1) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) facc[c] = ntop[c];
+        }
+        if (L >= Lfirst) mcur = mnext;
+        if (pf) {
+            double *dst = S.up[pz % 3];
+#pragma unroll
+            for (int j = 0; j < PF; ++j) {
+                const int idx = t + j * NT;
+                if (idx < PLANE) dst[idx] = pfv[j];
+            }
+        }
+        __syncthreads();
+    }
+}

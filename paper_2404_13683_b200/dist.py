@@ -118,8 +118,9 @@ class OvxCompute:
         import torch
         from .ovx import Ovx
         self.ovx = Ovx(device)
-        if stream is not None:
-            self.ovx.set_stream(stream)
+        # the interface exchange (torch copies / NCCL P2P) is ordered against torch's current
+        # stream, so the slab's kernels must run on that same stream
+        self.ovx.set_stream(stream if stream is not None else torch.cuda.current_stream(device))
         o = self.ovx
         o.set_grid(lm.nx, lm.ny, lm.nz, lm.ds)
         o.set_materials(lm.rho, lm.kappa, lm.G)
