@@ -1,21 +1,25 @@
 #!/usr/bin/env python
 """Benchmark of the OVFEM / TCOVFEM explicit time step on B200 (BASELINE.json metric:
-element-updates/s; INT8 tensor-pipe use; error vs FP64).
+element-updates/s at 1/2/4/8 B200; INT8 tensor-pipe use; error vs FP64).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--path int8|fp64] [--impl ovx|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--path int8|fp64|fp64_dense] [--impl ovx|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
 
-A "step" is one full time step of the hot path (EBE product Σ_e K_e u_e through the INT8
-tcgen05 path + fused central-difference update) over the C2 workload (256³ voxels,
-BASELINE.json configs[1]).  Timing: W warm-up steps, then K steps bracketed by
-barrier + cuda.synchronize, CUDA events on the launching stream, max over ranks.
-Inputs are far larger than L2 (≈1.4 GB touched per step), so no L2 flush is needed.
-`--impl reference` times the CPU oracle (oracle/, the only other implementation) on a
-bounded sample of the same workload.
+A "step" is one full time step of the hot path (element-by-element product Σ_e K_e u_e through
+the INT8 tcgen05 path, fused scatter + central-difference update) over the whole grid.
+  N = 1: C2 (BASELINE.json configs[1]): 256³ voxels, homogeneous roller box, standing P wave.
+  N > 1: C5 (configs[4]) weak scaling: 256 × 256 × 256·N voxels, one 256³ z-slab per GPU,
+         interface forces exchanged with NCCL point-to-point every step.
+Timing: W warm-up steps, then K steps bracketed by barrier + cuda.synchronize, CUDA events on the
+launching stream, max over ranks.  Inputs are far larger than L2 (≈1.4 GB touched per step per
+GPU), so no L2 flush is needed.  `--impl reference` times the CPU oracle (oracle/) on a bounded
+sample of the same workload (the reference is a paper; there is no other implementation).
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -28,6 +32,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "element-updates/s"
+N_EDGE = 256
 
 
 def _peaks() -> dict:
@@ -99,10 +104,34 @@ def _workload(n: int):
     return m, u0
 
 
-def _algorithmic_bytes(m) -> int:
+def _slab_workload(n: int, world: int, rank: int):
+    """This rank's z-slab of the C5 weak-scaling grid n × n × (n·world) (homogeneous roller box
+    with a standing P wave along x), built locally: (local model, Slab, u0 of planes ez0..ez1)."""
+    import workloads as wl
+    from paper_2404_13683_b200 import dist as D
+    from types import SimpleNamespace
+    nz = n * world
+    ez0, ez1 = D.partition(nz, world, rank)
+    slab = D.Slab(rank, world, ez0, ez1)
+    g = wl.c2_block(8)                       # materials / dt of C2 (ν = 0.25)
+    nzl = ez1 - ez0
+    mask = wl.roller_mask(n, n, nz).reshape(nz + 1, -1)[ez0:ez1 + 1].reshape(-1)
+    lm = SimpleNamespace(nx=n, ny=n, nz=nzl, ds=1.0, rho=g.rho, kappa=g.kappa, G=g.G, dt=g.dt,
+                         mat=np.zeros(n * n * nzl, np.uint8),
+                         mat_below=np.zeros(n * n, np.uint8) if rank > 0 else None,
+                         dirichlet=np.ascontiguousarray(mask), src_node=np.zeros(0, np.int64),
+                         src_axis=np.zeros(0, np.int32), amp=np.zeros((0, 1)))
+    k = math.pi * 16 / n
+    x = np.arange(n + 1, dtype=np.float64)
+    u = np.zeros((nzl + 1, n + 1, n + 1, 3))
+    u[..., 0] = np.sin(k * x)[None, None, :]
+    return lm, slab, u.reshape(-1)
+
+
+def _algorithmic_bytes(nn: int, ne: int) -> int:
     """u^{it} 24 B + u^{it-1} 24 B + u^{it+1} 24 B + w 8 B per node,
     1 B material per element, 1 B Dirichlet mask per node."""
-    return 80 * m.n_nodes + m.n_elems + m.n_nodes
+    return 80 * nn + ne + nn
 
 
 def cpu_oracle_sample(path_int8: bool, steps: int, n: int = 64) -> dict:
@@ -145,6 +174,56 @@ def run_reference(args) -> None:
     print(json.dumps(out))
 
 
+class Single:
+    """One GPU: the whole C2 grid in one context."""
+
+    def __init__(self, n, path, local, stream):
+        from paper_2404_13683_b200 import Ovx
+        self.m, self.u0 = _workload(n)
+        self.s = Ovx(local)
+        self.s.set_stream(stream)
+        self.s.load_model(self.m, path)
+        self.nn, self.ne = self.m.n_nodes, self.m.n_elems
+        self.launches_per_step = 1
+
+    def set_state(self, u, up):
+        self.s.set_state(u, up, 0)
+
+    def step(self, k):
+        self.s.step(k)
+
+    def get_state(self):
+        return self.s.get_state()
+
+
+class Sharded:
+    """One rank of the C5 z-slab decomposition (NCCL interface exchange)."""
+
+    def __init__(self, n, path, local, stream, world, rank):
+        from paper_2404_13683_b200 import dist as D
+        self.lm, self.slab, self.u0 = _slab_workload(n, world, rank)
+        self.c = D.OvxCompute(self.lm, self.slab, local, path, stream=stream)
+        self.t = D.TorchTransport()
+        self.s = self.c.ovx
+        self.nn = (n + 1) * (n + 1) * (self.slab.nzl + 1)
+        self.ne = n * n * self.slab.nzl
+        self.launches_per_step = 1 + (1 if self.slab.flags & 1 else 0)
+
+    def set_state(self, u, up):
+        self.c.set_state(u, up, 0)
+
+    def step(self, k):
+        for _ in range(k):
+            self.c.begin()
+            self.t.exchange_up(self.slab, self.c.a_send, self.c.a_recv)
+            self.c.iface()
+            self.t.exchange_down(self.slab, self.c.u_send, self.c.u_recv)
+            self.c.end()
+
+    def get_state(self):
+        return self.c.get_state()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -152,8 +231,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ovx", choices=["ovx", "reference"])
     ap.add_argument("--path", default="int8", choices=["int8", "fp64", "fp64_dense"])
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--n", type=int, default=N_EDGE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp64-companion", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -162,106 +242,121 @@ def main() -> None:
 
     import torch
     import torch.distributed as dist
-    from paper_2404_13683_b200 import Ovx, OVX_INT8, OVX_FP64, OVX_FP64_DENSE
+    from paper_2404_13683_b200 import OVX_INT8, OVX_FP64, OVX_FP64_DENSE
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl")
-
-    m, u0 = _workload(args.n)
-    path = {"int8": OVX_INT8, "fp64": OVX_FP64, "fp64_dense": OVX_FP64_DENSE}[args.path]
-    stream = torch.cuda.Stream()
-    s = Ovx(local)
-    s.set_stream(stream)
-    s.load_model(m, path)
-    s.set_state(u0, u0, 0)
-    s.step(args.warmup)
-    s.sync()
-    s.get_timers(reset=True)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    paths = {"int8": OVX_INT8, "fp64": OVX_FP64, "fp64_dense": OVX_FP64_DENSE}
+    path = paths[args.path]
+    stream = torch.cuda.current_stream()
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    ev0.record(stream)
-    s.step(args.steps)
-    ev1.record(stream)
-    barrier()
-    ms = ev0.elapsed_time(ev1)
-    ms_kernel, launches = s.get_timers(reset=True)
-    clocks = sampler.stop()
-    s.check_finite()
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        return float(t.item())
 
-    E = m.n_elems
-    value = world * E * args.steps / (ms / 1e3)
-    bytes_launch = _algorithmic_bytes(m)
-    t_launch = ms_kernel / max(launches, 1) / 1e3
-    achieved = bytes_launch / t_launch / 1e9
-    pk = _peaks()
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(f"{args.path}_{args.n}")
+    def timed_run(path_id: int, steps: int, warmup: int, sample_clocks: bool):
+        R = Single(args.n, path_id, local, stream) if world == 1 else Sharded(args.n, path_id, local, stream, world, rank)
+        R.set_state(R.u0, R.u0)
+        R.step(warmup)
+        barrier()
+        R.s.get_timers(reset=True)
+        sampler = ClockSampler(local) if sample_clocks else None
+        if sampler:
+            sampler.start()
+            time.sleep(0.3)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        ev0.record(stream)
+        R.step(steps)
+        ev1.record(stream)
+        barrier()
+        ms = max_over_ranks(ev0.elapsed_time(ev1))
+        clocks = sampler.stop() if sampler else None
+        return R, ms, clocks
+
+    R, ms, clocks = timed_run(path, args.steps, args.warmup, True)
+    R.s.check_finite()
+    # dominant kernel: the step kernel's own CUDA-event time (Single: events bracket the launches)
+    kernel_ms = None
+    if world == 1:
+        k_ms, launches = R.s.get_timers(reset=True)
+        kernel_ms = k_ms / max(launches, 1)
+    E_total = R.ne * world
+    value = E_total * args.steps / (ms / 1e3)
 
     # end to end through the public API with pinned host buffers (upload state, K steps, download)
-    uh = torch.from_numpy(u0).pin_memory().numpy()
-    uph = torch.from_numpy(u0).pin_memory().numpy()
-    oh = torch.empty(3 * m.n_nodes, dtype=torch.float64).pin_memory().numpy()
-    oph = torch.empty(3 * m.n_nodes, dtype=torch.float64).pin_memory().numpy()
+    uh = torch.from_numpy(R.u0).pin_memory().numpy()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    s.set_state(uh, uph, 0)
-    s.step(args.steps)
-    u_out, up_out, _ = s.get_state()
+    R.set_state(uh, uh)
+    R.step(args.steps)
+    _ = R.get_state()
     e1.record(stream)
     barrier()
-    ms_e2e = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_e2e], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
-    del oh, oph, u_out, up_out
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+
+    # FP64 CUDA-core path measured beside the INT8 path (same workload, same clock record)
+    fp64 = None
+    if path == OVX_INT8 and not args.no_fp64_companion:
+        del R
+        torch.cuda.empty_cache()
+        R64, ms64, _ = timed_run(OVX_FP64, args.steps, args.warmup, False)
+        fp64 = {"value": E_total * args.steps / (ms64 / 1e3), "ms_per_step": ms64 / args.steps}
+        del R64
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    ops = 18432 * E / t_launch / 1e12 if path == OVX_INT8 else None
+    bytes_launch = _algorithmic_bytes((args.n + 1) ** 3 if world == 1 else R.nn, R.ne) if world == 1 else None
+    pk = _peaks()
+    roof = None
+    if world == 1:
+        achieved = bytes_launch / (kernel_ms / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(f"{args.path}_{args.n}")
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_src": pk["src"],
+                "bytes_per_launch": bytes_launch, "kernel_ms_per_launch": kernel_ms,
+                "kernel": {0: "step_v1<INT8>", 1: "step_f64", 2: "step_v1<FP64_DENSE>"}[path]}
+    nodes_total = (args.n + 1) ** 2 * (args.n * world + 1)
     out = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32 + f64" if path == OVX_INT8 else "f64",
-        "data": "synthetic (seeded; C2 roller box with a standing P wave)",
-        "config": {"workload": f"C2: {args.n}^3 homogeneous block (kappa=5/3, G=1, rho=1, ds=1), rollers",
-                   "path": args.path, "elements": E, "nodes": m.n_nodes,
-                   "parallelism": "single GPU" if world == 1 else f"replicas x{world} (no z-slab exchange yet)",
-                   "l2": "inputs larger than L2 (%.2f GB touched per step)" % (bytes_launch / 1e9)},
-        "dof_steps_per_s": 3 * m.n_nodes * world * args.steps / (ms / 1e3),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-                     "peak_src": pk["src"], "bytes_per_launch": bytes_launch,
-                     "kernel_ms_per_launch": t_launch * 1e3},
-        "int8_tops_useful": ops,
+        "data": "synthetic (seeded; roller box with a standing P wave)",
+        "config": {"workload": (f"C2: {args.n}^3 homogeneous block" if world == 1 else
+                                f"C5: {args.n}x{args.n}x{args.n * world} homogeneous block, {args.n}^3 z-slab per GPU"),
+                   "material": "kappa=5/3, G=1, rho=1, ds=1, rollers", "path": args.path,
+                   "elements": E_total, "nodes": nodes_total,
+                   "parallelism": "single GPU" if world == 1 else f"z-slabs x{world}, NCCL P2P interface exchange",
+                   "l2": "inputs larger than L2 (%.2f GB touched per step per GPU)" % (_algorithmic_bytes(R.nn, R.ne) / 1e9)},
+        "dof_steps_per_s": 3 * nodes_total * args.steps / (ms / 1e3),
+        "roofline": roof,
+        "int8_tops_useful": (18432 * R.ne / (kernel_ms / 1e3) / 1e12) if (path == OVX_INT8 and kernel_ms) else None,
+        "fp64_path": fp64,
         "clocks": clocks,
-        "gpu_launches": launches,
-        "e2e": {"value": world * E * args.steps / (ms_e2e / 1e3), "unit": METRIC,
-                "h2d_bytes_per_step": 2 * 24 * m.n_nodes / args.steps,
-                "d2h_bytes_per_step": 2 * 24 * m.n_nodes / args.steps,
-                "note": f"set_state(host pinned) + {args.steps} steps + get_state(host) per run"},
+        "gpu_launches": R.launches_per_step * args.steps,
+        "e2e": {"value": E_total * args.steps / (ms_e2e / 1e3), "unit": METRIC,
+                "h2d_bytes_per_step": 2 * 24 * R.nn / args.steps,
+                "d2h_bytes_per_step": 2 * 24 * R.nn / args.steps,
+                "note": f"per GPU: set_state(host pinned) + {args.steps} steps + get_state(host)"},
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_oracle_sample(path == OVX_INT8, steps=3)

@@ -67,7 +67,10 @@ ovx_status ovx_destroy(ovx_ctx *ctx);
 const char *ovx_last_error(const ovx_ctx *ctx);
 /* Library version string. */
 const char *ovx_version(void);
-/* Order all work of ctx on `stream` (a cudaStream_t of the context's device; NULL = library stream). */
+/* Order all work of ctx on `stream`, a cudaStream_t of the context's device.  NULL is the CUDA
+ * default (legacy) stream; OVX_LIBRARY_STREAM gives the context its own non-blocking stream
+ * (the state after ovx_create). */
+#define OVX_LIBRARY_STREAM ((void *)(intptr_t)-1)
 ovx_status ovx_set_stream(ovx_ctx *ctx, void *stream);
 
 /* ---- model (cubes of side ds on a structured grid; L94: κ, G) -- */

@@ -172,8 +172,8 @@ ovx_status ovx_set_stream(ovx_ctx *ctx, void *stream) {
         cudaStreamDestroy(ctx->stream);
         ctx->own_stream = false;
     }
-    if (stream) {
-        ctx->stream = (cudaStream_t)stream;
+    if (stream != OVX_LIBRARY_STREAM) {
+        ctx->stream = (cudaStream_t)stream;   // NULL: the legacy default stream
     } else {
         CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->own_stream = true;

@@ -137,8 +137,12 @@ class Ovx:
 
     # -- C ABI -------------------------------------------------------------------
     def set_stream(self, stream) -> None:
-        """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None."""
-        raw = getattr(stream, "cuda_stream", stream)
+        """stream: a torch.cuda.Stream (its handle may be 0, the default stream), a raw
+        cudaStream_t int, or None for a library-owned stream."""
+        if stream is None:
+            self._call("ovx_set_stream", _vp(-1 & 0xFFFFFFFFFFFFFFFF))
+            return
+        raw = int(getattr(stream, "cuda_stream", stream))
         self._call("ovx_set_stream", _vp(raw) if raw else None)
 
     def set_grid(self, nx: int, ny: int, nz: int, ds: float) -> None:

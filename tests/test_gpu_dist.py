@@ -40,7 +40,10 @@ def test_slabs_on_one_gpu_equal_monolithic(world, path):
     s.set_state(u0, u0, 0)
     s.step(nsteps)
     mu, mup, _ = s.get_state()
-    assert np.array_equal(u, mu) and np.array_equal(up, mup)
+    if path == 0:   # INT8: same kernel and summation order -> bit-identical
+        assert np.array_equal(u, mu) and np.array_equal(up, mup)
+    else:           # factored FP64: monolithic runs use step_f64 (different summation order)
+        assert np.linalg.norm(u - mu) <= 1e-12 * np.linalg.norm(mu)
     if path == 0:
         ru, rup, _, _ = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=oracle.PATH_INT8)
         assert np.array_equal(u, ru)
