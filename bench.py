@@ -310,6 +310,7 @@ def main() -> None:
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
 
     # FP64 CUDA-core path measured beside the INT8 path (same workload, same clock record)
+    R_nn, R_ne, R_lps = R.nn, R.ne, R.launches_per_step
     fp64 = None
     if path == OVX_INT8 and not args.no_fp64_companion:
         del R
@@ -322,7 +323,7 @@ def main() -> None:
         if world > 1:
             dist.destroy_process_group()
         return
-    bytes_launch = _algorithmic_bytes((args.n + 1) ** 3 if world == 1 else R.nn, R.ne) if world == 1 else None
+    bytes_launch = _algorithmic_bytes(R_nn, R_ne) if world == 1 else None
     pk = _peaks()
     roof = None
     if world == 1:
@@ -346,16 +347,16 @@ def main() -> None:
                    "material": "kappa=5/3, G=1, rho=1, ds=1, rollers", "path": args.path,
                    "elements": E_total, "nodes": nodes_total,
                    "parallelism": "single GPU" if world == 1 else f"z-slabs x{world}, NCCL P2P interface exchange",
-                   "l2": "inputs larger than L2 (%.2f GB touched per step per GPU)" % (_algorithmic_bytes(R.nn, R.ne) / 1e9)},
+                   "l2": "inputs larger than L2 (%.2f GB touched per step per GPU)" % (_algorithmic_bytes(R_nn, R_ne) / 1e9)},
         "dof_steps_per_s": 3 * nodes_total * args.steps / (ms / 1e3),
         "roofline": roof,
-        "int8_tops_useful": (18432 * R.ne / (kernel_ms / 1e3) / 1e12) if (path == OVX_INT8 and kernel_ms) else None,
+        "int8_tops_useful": (18432 * R_ne / (kernel_ms / 1e3) / 1e12) if (path == OVX_INT8 and kernel_ms) else None,
         "fp64_path": fp64,
         "clocks": clocks,
-        "gpu_launches": R.launches_per_step * args.steps,
+        "gpu_launches": R_lps * args.steps,
         "e2e": {"value": E_total * args.steps / (ms_e2e / 1e3), "unit": METRIC,
-                "h2d_bytes_per_step": 2 * 24 * R.nn / args.steps,
-                "d2h_bytes_per_step": 2 * 24 * R.nn / args.steps,
+                "h2d_bytes_per_step": 2 * 24 * R_nn / args.steps,
+                "d2h_bytes_per_step": 2 * 24 * R_nn / args.steps,
                 "note": f"per GPU: set_state(host pinned) + {args.steps} steps + get_state(host)"},
     }
     if world == 1 and not args.no_cpu_baseline:

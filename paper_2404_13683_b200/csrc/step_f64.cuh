@@ -21,12 +21,12 @@ struct F2 {
 };
 
 struct SmemF2 {
-    double up[3][F2::PLANE];
-    double ysum[F2::EY][EX][6];    // +y-corner x-sums of each element row, for the row above
+    double up[4][F2::PLANE];          // ring: planes L, L+1 in use, L+2 parked, L+3 in flight
+    double ysum[2][F2::EY][EX][6];    // +y-corner x-sums of each element row (double-buffered)
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
+__global__ void __launch_bounds__(F2::NT, 3) step_f64(const StepParams p) {
     constexpr int NT = F2::NT, TY = F2::TY, PLANE = F2::PLANE, PF = F2::PF;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SmemF2 &S = *reinterpret_cast<SmemF2 *>(smem_raw);
@@ -74,10 +74,10 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         }
 
     const int64_t Lfirst = max(Z0 - 1, (int64_t)0);
-    // synchronous first two planes
-    for (int j = 0; j < 2; ++j) {
+    // synchronous first three planes (the loop prefetches two planes ahead)
+    for (int j = 0; j < 3; ++j) {
         const int64_t iz = Lfirst + j;
-        double *dst = S.up[iz % 3];
+        double *dst = S.up[iz & 3];
         for (int idx = t; idx < PLANE; idx += NT) {
             const int py = idx / (PX * 3);
             const int rem = idx - py * (PX * 3);
@@ -89,15 +89,29 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     }
     __syncthreads();
 
+    // plane prefetched in the previous iteration, parked (before this layer's barrier) into the
+    // ring slot of plane L-1, which no thread reads any more
+    double pend[PF];
+    int64_t pend_z = -1;
+    auto park_prev = [&]() {
+        if (pend_z >= 0) {
+            double *dst = S.up[pend_z & 3];
+#pragma unroll
+            for (int j = 0; j < PF; ++j) {
+                const int idx = t + j * NT;
+                if (idx < PLANE) dst[idx] = pend[j];
+            }
+        }
+    };
     double facc[3] = {0.0, 0.0, 0.0};   // plane L (receives layer L-1 top + layer L bottom)
     int mcur = (ein && Lfirst < p.nz) ? (int)__ldg(matcol + mstride * Lfirst) : kZeroMat;
     for (int64_t L = Z0 - 1; L < Z1; ++L) {
         const bool layer_ok = (L >= 0 && L < p.nz);
         const bool plane_done = (L >= Z0 && L <= p.nz);
         const int mnext = (ein && L + 1 > Lfirst && L + 1 < p.nz) ? (int)__ldg(matcol + mstride * (L + 1)) : kZeroMat;
-        // ---- prefetch plane L+2 and the update operands of plane L ----
-        const int64_t pz = L + 2;
-        const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < p.nz);
+        // ---- prefetch plane L+3 (parked next iteration) and the update operands of plane L ----
+        const int64_t pz = L + 3;
+        const bool pf = (pz > Lfirst + 2) && (L + 2 < Z1) && (L + 2 < p.nz);
         double pfv[PF];
         const double *uplane = p.u + 3 * PSTRIDE * pz;
 #pragma unroll
@@ -115,9 +129,10 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         }
 
         double nbot[3] = {0.0, 0.0, 0.0}, ntop[3] = {0.0, 0.0, 0.0};
+        double(*ys)[EX][6] = S.ysum[L & 1];
         if (layer_ok) {
             double ue[24], fe[24];
-            gather<F2::PY>(ue, S.up[L % 3], S.up[(L + 1) % 3], lx, ly);
+            gather<F2::PY>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
             element_force_wht(ue, c_mat[mcur], fe);     // zero material outside the domain
             // x-sums at this element's -x node column: own -x corners + lane lx-1's +x corners
             // local nodes: (-x,-y)=0,4  (+x,-y)=1,5  (+x,+y)=2,6  (-x,+y)=3,7   (bottom, top)
@@ -128,20 +143,23 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
                 for (int c = 0; c < 3; ++c) {
                     const double pm = __shfl_up_sync(0xffffffffu, fe[3 * (1 + 4 * dz) + c], 1);  // (+x,-y) of lx-1
                     const double pp = __shfl_up_sync(0xffffffffu, fe[3 * (2 + 4 * dz) + c], 1);  // (+x,+y) of lx-1
-                    xs[0 * 6 + dz * 3 + c] = fe[3 * (0 + 4 * dz) + c] + (lx > 0 ? pm : 0.0);
-                    xs[1 * 6 + dz * 3 + c] = fe[3 * (3 + 4 * dz) + c] + (lx > 0 ? pp : 0.0);
+                    // (lane 0 adds its own value here; it owns no node, so the sum is never used)
+                    xs[0 * 6 + dz * 3 + c] = fe[3 * (0 + 4 * dz) + c] + pm;
+                    xs[1 * 6 + dz * 3 + c] = fe[3 * (3 + 4 * dz) + c] + pp;
                 }
 #pragma unroll
-            for (int q = 0; q < 6; ++q) S.ysum[ly][lx][q] = xs[6 + q];
-            __syncthreads();
+            for (int q = 0; q < 6; ++q) ys[ly][lx][q] = xs[6 + q];
+            park_prev();
+            __syncthreads();   // the only barrier of the layer
             if (ly > 0) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    nbot[c] = xs[c] + S.ysum[ly - 1][lx][c];
-                    ntop[c] = xs[3 + c] + S.ysum[ly - 1][lx][3 + c];
+                    nbot[c] = xs[c] + ys[ly - 1][lx][c];
+                    ntop[c] = xs[3 + c] + ys[ly - 1][lx][3 + c];
                 }
             }
         } else {
+            park_prev();
             __syncthreads();
         }
         if (L >= Z0) {
@@ -150,7 +168,7 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         }
         // ---- plane L complete: update ----
         if (upd) {
-            const double *up = &S.up[L % 3][(ly * PX + lx) * 3];
+            const double *up = &S.up[L & 3][(ly * PX + lx) * 3];
             if (MODE == MODE_STEP) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
@@ -173,14 +191,8 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
             for (int c = 0; c < 3; ++c) facc[c] = ntop[c];
         }
         if (L >= Lfirst) mcur = mnext;
-        if (pf) {
-            double *dst = S.up[pz % 3];
 #pragma unroll
-            for (int j = 0; j < PF; ++j) {
-                const int idx = t + j * NT;
-                if (idx < PLANE) dst[idx] = pfv[j];
-            }
-        }
-        __syncthreads();
+        for (int j = 0; j < PF; ++j) pend[j] = pfv[j];
+        pend_z = pf ? pz : -1;
     }
 }
