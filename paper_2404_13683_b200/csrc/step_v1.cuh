@@ -264,28 +264,29 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
 #pragma unroll
                     for (int i = 0; i < 24; ++i) ue[i] = __dmul_rn(cG, ue[i]);
                 }
-                long long v[24];
-                if (!deg && s >= 0x1p-960) {
-                    const double R = __dmul_rn(1.0 / s, 0x1p56);   // RN(1/s_e)·2^56, exact scaling (Q7)
+                const bool straight = !deg && s >= 0x1p-960;
+                const double r = 1.0 / s;                          // RN(1/s_e), reading Q7
+                const double R = __dmul_rn(r, 0x1p56);             // exact power-of-two scaling
 #pragma unroll
-                    for (int i = 0; i < 24; ++i) v[i] = __double2ll_rz(__dmul_rn(ue[i], R));  // trunc (Q8)
-                } else {
-                    const double r = 1.0 / s;
+                for (int ch = 0; ch < 3; ++ch) {                   // 8 values at a time: convert, pack, store
+                    long long v[8];
+                    if (straight) {
 #pragma unroll
-                    for (int i = 0; i < 24; ++i)
-                        v[i] = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ue[i], r), 0x1p56));
-                }
+                        for (int q = 0; q < 8; ++q) v[q] = __double2ll_rz(__dmul_rn(ue[ch * 8 + q], R));  // trunc (Q8)
+                    } else {
 #pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
+                        for (int q = 0; q < 8; ++q)
+                            v[q] = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ue[ch * 8 + q], r), 0x1p56));
+                    }
                     uint32_t lo[8], hi[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const unsigned long long vp = (unsigned long long)v[ch * 8 + q] + (1ull << 56);
+                        const unsigned long long vp = (unsigned long long)v[q] + (1ull << 56);
                         lo[q] = (uint32_t)vp;
                         hi[q] = (uint32_t)(vp >> 32);
                         if (MODE == MODE_DEBUG && dbg) {
                             const int k = 24 * half + ch * 8 + q;
-                            if (p.dbg_v) p.dbg_v[dj * 48 + k] = v[ch * 8 + q];
+                            if (p.dbg_v) p.dbg_v[dj * 48 + k] = v[q];
                             if (p.dbg_d)
 #pragma unroll
                                 for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = (uint8_t)(vp >> (8 * j));
@@ -334,7 +335,10 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                         ptx::mma_commit(&S.mbar[mm]);
                     }
                 }
-                ptx::mbar_wait_sleep(&S.mbar[mt], phase);
+                // one warp of the M-tile polls the MMA-completion mbarrier; the other seven block in
+                // hardware on the named barrier (no issue slots spent spinning)
+                if (warp == 8 * mt) ptx::mbar_wait(&S.mbar[mt], phase);
+                asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");
                 phase ^= 1;
                 ptx::tc_fence_after();
 
