@@ -99,6 +99,13 @@ ovx_status ovx_critical_dt(ovx_ctx *ctx, double *dt_elem_bound);
 ovx_status ovx_set_sources(ovx_ctx *ctx, int n, const int64_t *node, const int32_t *axis,
                            int64_t n_t, const double *amp);
 
+/* Receivers (Table 1 observation points, L196-L212): at every step it < n_t, the new
+ * displacement u^{it+1} of node[k], component c, is recorded at trace index (3k + c)·n_t + it.
+ * n <= 32; replaces any previous receiver set and zeroes the traces. */
+ovx_status ovx_set_receivers(ovx_ctx *ctx, int n, const int64_t *node, int64_t n_t);
+/* Copy the traces (n × 3 × n_t doubles, receiver-major, then component, then step) to host memory. */
+ovx_status ovx_get_traces(ovx_ctx *ctx, double *out);
+
 /* ---- state (u^{it}, u^{it-1}, it) is the complete state: also checkpoint/resume -- */
 ovx_status ovx_set_state(ovx_ctx *ctx, const double *u, const double *u_prev, int64_t it);
 ovx_status ovx_get_state(ovx_ctx *ctx, double *u, double *u_prev, int64_t *it);

@@ -37,6 +37,10 @@ struct ovx_ctx {
     int64_t n_t = 0;
     std::vector<double> amp;
     int64_t it = 0;
+    int nrec = 0;
+    std::vector<int64_t> rec_node;
+    int64_t rec_nt = 0;
+    double *d_traces = nullptr;
     std::vector<EventPair> ev_used, ev_free;
     int64_t launches = 0;
     // z-slab (multi-GPU) state
@@ -92,6 +96,14 @@ bool finite_all(const double *a, int64_t n) {
     for (int64_t i = 0; i < n; ++i)
         if (!std::isfinite(a[i])) return false;
     return true;
+}
+
+void fill_receivers(ovx_ctx *ctx, StepParams &p) {
+    p.nrec = ctx->nrec;
+    for (int k = 0; k < ctx->nrec; ++k) p.rec_node[k] = ctx->rec_node[k];
+    p.traces = ctx->d_traces;
+    p.it = ctx->it;
+    p.rec_nt = ctx->d_traces ? ctx->rec_nt : 0;
 }
 
 StepParams base_params(ovx_ctx *ctx) {
@@ -156,6 +168,7 @@ ovx_status ovx_destroy(ovx_ctx *ctx) {
     dfree(ctx->d_w);
     dfree(ctx->d_mat_below);
     dfree(ctx->d_bot_b);
+    dfree(ctx->d_traces);
     for (auto &p : ctx->ev_used) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto &p : ctx->ev_free) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -432,6 +445,7 @@ ovx_status ovx_step(ovx_ctx *ctx, int64_t n) {
             p.src_dof[q] = 3 * ctx->src_node[q] + ctx->src_axis[q];
             p.src_val[q] = (ctx->it < ctx->n_t) ? ctx->amp[(size_t)q * ctx->n_t + ctx->it] : 0.0;
         }
+        fill_receivers(ctx, p);
         CK(launch_step(ctx->path, MODE_STEP, p, ctx->stream));
         std::swap(ctx->d_u, ctx->d_up);
         ctx->it += 1;
@@ -491,6 +505,7 @@ static StepParams step_params(ovx_ctx *ctx) {
     p.slab_flags = ctx->slab_flags;
     p.iface_top_A = ctx->a_send;
     p.iface_bot_b = ctx->d_bot_b;
+    fill_receivers(ctx, p);
     return p;
 }
 
@@ -526,6 +541,39 @@ ovx_status ovx_step_end(ovx_ctx *ctx) {
                            cudaMemcpyDeviceToDevice, ctx->stream));
     std::swap(ctx->d_u, ctx->d_up);
     ctx->it += 1;
+    return OVX_OK;
+}
+
+ovx_status ovx_set_receivers(ovx_ctx *ctx, int n, const int64_t *node, int64_t n_t) {
+    if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
+    if (!ctx->have_grid) return fail(ctx, OVX_ESTATE, "set grid first");
+    if (n < 0 || n > kMaxRec || n_t < 0 || (n > 0 && !node)) return fail(ctx, OVX_EINVAL, "0..32 receivers");
+    for (int k = 0; k < n; ++k)
+        if (node[k] < 0 || node[k] >= ctx->nn()) return fail(ctx, OVX_EINVAL, "receiver node out of range");
+    cudaSetDevice(ctx->device);
+    dfree(ctx->d_traces);
+    ctx->d_traces = nullptr;
+    ctx->nrec = n;
+    ctx->rec_node.assign(node, node + n);
+    ctx->rec_nt = n_t;
+    if (n > 0 && n_t > 0) {
+        if (cudaMalloc(&ctx->d_traces, 8 * 3 * (size_t)n * (size_t)n_t) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, OVX_ENOMEM, "trace allocation failed");
+        }
+        CK(cudaMemsetAsync(ctx->d_traces, 0, 8 * 3 * (size_t)n * (size_t)n_t, ctx->stream));
+    }
+    return OVX_OK;
+}
+
+ovx_status ovx_get_traces(ovx_ctx *ctx, double *out) {
+    if (!ctx || !out) return fail(ctx, OVX_EINVAL, "null argument");
+    cudaSetDevice(ctx->device);
+    if (ctx->d_traces) {
+        CK(cudaMemcpyAsync(out, ctx->d_traces, 8 * 3 * (size_t)ctx->nrec * (size_t)ctx->rec_nt,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
     return OVX_OK;
 }
 

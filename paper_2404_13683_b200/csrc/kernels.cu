@@ -293,7 +293,7 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
 }
 
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
-    const int ty = V1<OVX_INT8>::TY;   // same tile height for every path
+    const int ty = path == OVX_INT8 ? V1<OVX_INT8>::TY : V1<OVX_FP64>::TY;
     p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
     p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
     const int64_t nchunk = (p.nz + 1 + kZChunk - 1) / kZChunk;        // chunks of <= 64 planes,
@@ -330,6 +330,9 @@ __global__ void iface_update_kernel(const StepParams p, const double *__restrict
             if ((dm >> c) & 1) un = 0.0;
             p.uo[dof] = un;
             u_send[dof] = un;
+            if (p.it < p.rec_nt)
+                for (int k = 0; k < p.nrec; ++k)
+                    if (p.rec_node[k] == j) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
         }
     }
 }

@@ -8,6 +8,7 @@ namespace ovx {
 constexpr int kMaxMat = 256;   // constant-table size; id 255 is the reserved zero material
 constexpr int kZeroMat = kMaxMat - 1;
 constexpr int kMaxSrc = 16;
+constexpr int kMaxRec = 32;
 
 // Per-material constants, computed on the host in the operation order the
 // oracle's definition fixes (DESIGN.md §Integer path):
@@ -32,6 +33,12 @@ struct StepParams {
     int nsrc;
     int64_t src_dof[kMaxSrc];
     double src_val[kMaxSrc];
+    // receivers (Table 1 observation points): u^{it+1} of node rec_node[k] is stored at
+    // traces[(3k + c)·rec_nt + it] when it < rec_nt
+    int nrec;
+    int64_t rec_node[kMaxRec];
+    double *traces;
+    int64_t it, rec_nt;
     // z-slab decomposition (multi-GPU): bit 0 = local plane 0 is an interface
     // owned by this rank (its lower-layer partial arrives from below), bit 1 = the top local
     // plane is an interface owned by the rank above (send its partial, do not update it)

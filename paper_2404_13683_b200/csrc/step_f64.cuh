@@ -73,6 +73,15 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
             has_src |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
         }
 
+    // does any receiver fall on this tile's owned columns?
+    bool has_rec = false;
+    if (MODE == MODE_STEP && p.it < p.rec_nt)
+        for (int k = 0; k < p.nrec; ++k) {
+            const int64_t n = p.rec_node[k];
+            const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+            has_rec |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
+        }
+
     const int64_t Lfirst = max(Z0 - 1, (int64_t)0);
     // synchronous first three planes (the loop prefetches two planes ahead)
     for (int j = 0; j < 3; ++j) {
@@ -180,6 +189,9 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
                     double un = fma(wn, F - facc[c], 2.0 * up[c] - upv[c]);
                     if ((dm >> c) & 1) un = 0.0;
                     p.uo[dof] = un;
+                    if (has_rec)
+                        for (int k = 0; k < p.nrec; ++k)
+                            if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
                 }
             } else {
 #pragma unroll

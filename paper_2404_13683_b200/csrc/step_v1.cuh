@@ -15,9 +15,10 @@
 // 3 K-steps against B = −K_e^INT8 ⊗ I_2 plus 2 K-steps of the G bytes against −128·I ⊗ I_2, so
 // D = −(K_e^INT8 v + 128 v_G) byte-stage by byte-stage, and f_e = RN(c1 s_e 2^-56)·RN(y).
 
+constexpr int EY_I8V = 4;   // INT8 tile: 32×4 elements = one M=128 MMA tile; 2 CTAs per SM
 template <int PATH>
 struct V1 {
-    static constexpr int EY = 8;
+    static constexpr int EY = PATH == OVX_INT8 ? EY_I8V : 8;
     static constexpr int NE = EX * EY;                 // 256 elements per layer
     static constexpr int TPE = PATH == OVX_INT8 ? 2 : 1;
     static constexpr int NT = NE * TPE;                // threads
@@ -26,7 +27,9 @@ struct V1 {
     static constexpr int NOWN = TX * TY;               // 217 owned nodes per plane
     static constexpr int PLANE = PX * PY * 3;          // 891 doubles per plane
     static constexpr int PF = (PLANE + NT - 1) / NT;   // prefetched doubles per thread
-    static constexpr int MINB = PATH == OVX_INT8 ? 1 : 2;
+    static constexpr int MT = NE / 128;                // INT8: M=128 MMA tiles per layer
+    static constexpr int MINB = PATH == OVX_INT8 ? (MT == 1 ? 2 : 1) : 2;
+    static constexpr int TMEM_COLS = MT * 256;
 };
 
 struct SmemV1F64 {
@@ -45,24 +48,24 @@ constexpr int BI_PITCH = 2 * 128;                // identity blocks: 48 rows × 
 
 struct SmemV1I8 {
     struct {
-        uint8_t A[2][4][A1_BYTES];   // [M-tile][half-word array], K-major canonical layout
+        uint8_t A[V1<OVX_INT8>::MT][4][A1_BYTES];   // [M-tile][half-word array], K-major layout
     } u;
-    double fe[24][256];              // separate from A: one M-tile's epilogue may run while the
-                                     // other M-tile's MMAs still read their A arrays
+    double fe[24][V1<OVX_INT8>::NE];  // separate from A: one M-tile's epilogue may run while
+                                      // another M-tile's MMAs still read their A arrays
     alignas(128) uint8_t B[6 * B1_PITCH];
     alignas(128) uint8_t BI[2][6 * BI_PITCH];
     double up[3][V1<OVX_INT8>::PLANE];
     double facc[2][V1<OVX_INT8>::NOWN * 3];
-    double amax[2][256];
-    uint64_t mbar[2];
+    double amax[2][V1<OVX_INT8>::NE];
+    uint64_t mbar[V1<OVX_INT8>::MT];
     uint32_t tmem;
 };
 
 template <int PATH>
 using SmemV1 = typename std::conditional<PATH == OVX_INT8, SmemV1I8, SmemV1F64>::type;
 
-__device__ __forceinline__ double (*fe_of(SmemV1I8 &S))[256] { return S.fe; }
-__device__ __forceinline__ double (*fe_of(SmemV1F64 &S))[256] { return S.fe; }
+__device__ __forceinline__ auto fe_of(SmemV1I8 &S) { return S.fe; }
+__device__ __forceinline__ auto fe_of(SmemV1F64 &S) { return S.fe; }
 
 template <int PATH>
 __device__ __forceinline__ void v1_load_plane_sync(double *dst, const StepParams &p, int64_t X0, int64_t Y0,
@@ -145,6 +148,15 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             has_src |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
         }
 
+    // does any receiver fall on this tile's owned columns?
+    bool has_rec = false;
+    if (MODE == MODE_STEP && p.it < p.rec_nt)
+        for (int k = 0; k < p.nrec; ++k) {
+            const int64_t n = p.rec_node[k];
+            const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+            has_rec |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
+        }
+
     uint32_t phase = 0;
     if constexpr (PATH == OVX_INT8) {
         // resident B operands: B[n = 2i+b'][kb = 2k+b] = −K_e^INT8[i][k]·δ(b,b');
@@ -162,15 +174,14 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             S.BI[s2][off] = ((kb & 1) == (n & 1) && k == (n >> 1)) ? (uint8_t)0x80 : (uint8_t)0;
         }
         // zero the K-padding chunk of every A row (never written afterwards)
-        for (int idx = t; idx < 2 * 4 * 128; idx += NT) {
+        for (int idx = t; idx < C::MT * 4 * 128; idx += NT) {
             const int a = idx >> 7, r = idx & 127;
             *reinterpret_cast<uint4 *>(&S.u.A[a >> 2][a & 3][(r >> 3) * A1_PITCH + 6 * 128 + (r & 7) * 16]) =
                 make_uint4(0, 0, 0, 0);
         }
-        if (warp == 0) ptx::tmem_alloc<512>(&S.tmem);
+        if (warp == 0) ptx::tmem_alloc<C::TMEM_COLS>(&S.tmem);
         if (t == 0) {
-            ptx::mbar_init(&S.mbar[0], 1);
-            ptx::mbar_init(&S.mbar[1], 1);
+            for (int mm = 0; mm < C::MT; ++mm) ptx::mbar_init(&S.mbar[mm], 1);
         }
         ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
@@ -388,7 +399,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
 
         // ---- (3) scatter (global element order) + update of the completed plane L ----
         if (t < NOWN) {
-            double(*fe)[256] = fe_of(S);
+            auto fe = fe_of(S);
             const int e00 = nxl + EX * nyl, e10 = e00 + 1, e01 = e00 + EX, e11 = e01 + 1;
             double *fl = &S.facc[L & 1][t * 3];
             double *fh = &S.facc[(L + 1) & 1][t * 3];
@@ -443,6 +454,9 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                         double un = __fma_rn(wn, __dsub_rn(F, fl[c]), b);
                         if ((dm >> c) & 1) un = 0.0;
                         p.uo[dof] = un;
+                        if (has_rec)
+                            for (int k = 0; k < p.nrec; ++k)
+                                if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
                     }
                 } else {
 #pragma unroll
@@ -465,6 +479,6 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
     }
     if constexpr (PATH == OVX_INT8) {
         ptx::tc_fence_after();
-        if (warp == 0) ptx::tmem_dealloc<512>(S.tmem);
+        if (warp == 0) ptx::tmem_dealloc<C::TMEM_COLS>(S.tmem);
     }
 }

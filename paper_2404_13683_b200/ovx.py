@@ -61,6 +61,8 @@ _SIGS = {
     "ovx_step_begin": [_vp],
     "ovx_step_iface": [_vp],
     "ovx_step_end": [_vp],
+    "ovx_set_receivers": [_vp, _int, _vp, _i64],
+    "ovx_get_traces": [_vp, _vp],
 }
 EXPORTS = tuple(_SIGS) + ("ovx_last_error", "ovx_version")
 
@@ -267,6 +269,16 @@ class Ovx:
         s = np.zeros(1, dtype=np.int32)
         self._call("ovx_get_launch_config", _np_ptr(c), _np_ptr(t), _np_ptr(s))
         return int(c[0]), int(t[0]), int(s[0])
+
+    def set_receivers(self, node, n_t: int) -> None:
+        node = _host(node, np.int64)
+        self._nrec, self._rec_nt = len(node), int(n_t)
+        self._call("ovx_set_receivers", len(node), _np_ptr(node), int(n_t))
+
+    def get_traces(self) -> np.ndarray:
+        out = np.zeros((getattr(self, "_nrec", 0), 3, getattr(self, "_rec_nt", 0)))
+        self._call("ovx_get_traces", _np_ptr(out))
+        return out
 
     def set_slab(self, flags: int, mat_below=None) -> None:
         mb = None if mat_below is None else _host(mat_below, np.uint8)

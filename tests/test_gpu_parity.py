@@ -217,3 +217,32 @@ def test_c2_plane_wave_dispersion_on_gpu(ovxmod):
         u, _, _ = s.get_state()
         a = physics.mode_amplitude(lam, m.dt, 1000)
         assert np.abs(u - a * u0).max() <= 1e-10 * np.abs(u0).max()
+
+
+def test_receiver_traces_and_err_metric(ovxmod):
+    """Receivers at the paper's observation-point layout (Table 1: a line of points on the top
+    surface, z-force source): GPU traces equal the oracle's step-by-step trace bit for bit (INT8),
+    and the Err metric between the INT8 and FP64 paths is at FP64 round-off."""
+    from oracle import physics
+    m = wl.c1_cube(8, steps=120)
+    rec = np.array([m.node(ix, 4, 8) for ix in (1, 2, 3, 5, 6, 7)], dtype=np.int64)
+    z = np.zeros(3 * m.n_nodes)
+    traces = {}
+    for path in (0, 1):
+        s = _solver(ovxmod, m, path)
+        s.set_receivers(rec, 120)
+        s.set_state(z, z, 0)
+        s.step(120)
+        traces[path] = s.get_traces()
+    # oracle trace, one step at a time
+    u, up = z.copy(), z.copy()
+    ref = np.zeros((len(rec), 3, 120))
+    for it in range(120):
+        u, up, _, _ = oracle.run(m.as_dict(), u, up, it, 1, path=oracle.PATH_INT8)
+        for k, n in enumerate(rec):
+            ref[k, :, it] = u[3 * n:3 * n + 3]
+    assert np.array_equal(traces[0], ref)
+    a8, a64 = traces[0].reshape(-1, 120), traces[1].reshape(-1, 120)
+    live = np.abs(a64).sum(1) > 0
+    err = physics.err_metric(a8[live], a64[live])
+    assert err < 1e-24
