@@ -17,6 +17,8 @@
 //             tcgen05.mma.kind::i8 (M=128 elements, N=48, K=96, 4 half-word arrays),
 //             K_e^INT8 ⊗ I_2 as the resident s8 B operand, s32 accumulators in TMEM,
 //             exact two-limb recombination y = K_e^INT8 v and f_e = c1·(RN(y)·s_e 2^-56 + c2 u_e).
+#include <cstdlib>
+
 #include "ovx_internal.h"
 #include "ptx.cuh"
 
@@ -34,16 +36,6 @@ namespace {
 constexpr int EX = 32;                    // element columns per layer (x)
 constexpr int TX = EX - 1;                // owned node columns (x)
 constexpr int PX = TX + 2;                // node columns of a u plane held in smem (x)
-template <int EY> struct Tile {
-    static constexpr int TY = EY - 1;          // owned node rows (y)
-    static constexpr int NE = EX * EY;         // elements per layer = threads per CTA
-    static constexpr int PY = TY + 2;          // node rows of a u plane in smem
-    static constexpr int PLANE_D = PX * PY * 3;
-    static constexpr int NOWN = TX * TY;
-    static constexpr int FPL = NOWN * 3;
-};
-constexpr int EY_I8 = 4;                  // INT8 path: 128 elements = MMA M
-constexpr int EY_F64 = 8;                 // FP64 paths: 256 elements per layer
 constexpr int KB = 96;                    // K bytes per A row / B row (48 values × 2 bytes)
 constexpr int ROWGRP = 8 * KB;            // bytes per 8-row core-matrix group (6 chunks × 128)
 constexpr int A_BYTES = 128 * KB;         // one half-word array (M = 128 rows)
@@ -51,50 +43,6 @@ constexpr int B_ROWS = 48;                // N = 24 outputs × 2 byte positions
 constexpr int B_BYTES = B_ROWS * KB;
 constexpr int TMEM_COLS = 256;            // 4 accumulators of 48 columns at 64-column pitch
 constexpr uint32_t IDESC = ptx::idesc_i8(128, 48);
-
-template <int EY>
-struct SmemF64 {
-    using T = Tile<EY>;
-    double up[2][T::PLANE_D];
-    double fe[24][T::NE];
-    double facc[2][T::FPL];
-};
-
-struct SmemI8 {
-    using T = Tile<EY_I8>;
-    alignas(1024) uint8_t A[4][A_BYTES];
-    alignas(128) uint8_t B[B_BYTES];
-    double up[2][T::PLANE_D];
-    double fe[24][T::NE];
-    double facc[2][T::FPL];
-    double sig[T::NE];
-    int deg[T::NE];
-    uint64_t mbar;
-    uint32_t tmem;
-};
-
-template <int PATH>
-struct PathCfg {
-    static constexpr int EY = PATH == OVX_INT8 ? EY_I8 : EY_F64;
-    using T = Tile<EY>;
-    using Smem = typename std::conditional<PATH == OVX_INT8, SmemI8, SmemF64<EY>>::type;
-};
-
-// Load node plane iz of u (tile-local columns [X0-1, X0+TX] × [Y0-1, Y0+TY]) into smem.
-template <int EY>
-__device__ __forceinline__ void load_plane(double *dst, const double *__restrict__ u, const StepParams &p,
-                                           int64_t X0, int64_t Y0, int64_t iz) {
-    const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
-    for (int idx = threadIdx.x; idx < Tile<EY>::PLANE_D; idx += Tile<EY>::NE) {
-        int py = idx / (PX * 3);
-        int rem = idx - py * (PX * 3);
-        int px = rem / 3, c = rem - px * 3;
-        int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
-        double v = 0.0;
-        if (ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1) v = __ldg(u + 3 * (ix + NX1 * (iy + NY1 * iz)) + c);
-        dst[idx] = v;
-    }
-}
 
 // Gather u_e (local node order of reading Q1) of tile-local element (lx, ly) from the two planes.
 template <int PY>
@@ -191,6 +139,37 @@ __device__ __forceinline__ void element_force_wht(const double (&ue)[24], const 
 
 #include "step_v1.cuh"
 #include "step_f64.cuh"
+#include "step_i8.cuh"
+
+// INT8 tile height (elements per layer = 32 × EY): 8 (one CTA/SM, two MMA tiles per layer) or
+// 4 (two CTAs/SM, one MMA tile each).  OVX_I8_EY selects it; default 8.
+int i8_ey() {
+    static int ey = [] {
+        const char *e = getenv("OVX_I8_EY");
+        return (e && atoi(e) == 4) ? 4 : 8;
+    }();
+    return ey;
+}
+
+template <int MODE, int EY>
+cudaError_t launch_i8(const StepParams &p, int64_t ctas, cudaStream_t st) {
+    static bool attr = false;
+    const int smem = (int)sizeof(SmemI8<EY>);
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(step_i8<MODE, EY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    step_i8<MODE, EY><<<(unsigned)ctas, I8<EY>::NT, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int EY>
+cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
+    if (mode == MODE_STEP) return launch_i8<MODE_STEP, EY>(p, ctas, st);
+    if (mode == MODE_APPLY) return launch_i8<MODE_APPLY, EY>(p, ctas, st);
+    return launch_i8<MODE_DEBUG, EY>(p, ctas, st);
+}
 
 template <int PATH, int MODE>
 cudaError_t launch_t(const StepParams &p, int64_t ctas, cudaStream_t st) {
@@ -287,20 +266,31 @@ cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, c
 }
 
 LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
+    if (path == OVX_INT8) {
+        LaunchInfo li;
+        const int ey = i8_ey(), tyy = ey - 1;
+        const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + tyy - 1) / tyy;
+        const int64_t tz = (nz + 1 + kZChunk - 1) / kZChunk;
+        li.ctas = tx * ty * tz;
+        li.threads = 32 * ey;
+        li.smem = ey == 4 ? (int)sizeof(SmemI8<4>) : (int)sizeof(SmemI8<8>);
+        return li;
+    }
     if (path == OVX_INT8) return info_t<OVX_INT8>(nx, ny, nz);
     if (path == OVX_FP64) return info_t<OVX_FP64>(nx, ny, nz);
     return info_t<OVX_FP64_DENSE>(nx, ny, nz);
 }
 
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
-    const int ty = path == OVX_INT8 ? V1<OVX_INT8>::TY : V1<OVX_FP64>::TY;
+    const int ty = path == OVX_INT8 ? i8_ey() - 1 : V1<OVX_FP64>::TY;
     p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
     p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
     const int64_t nchunk = (p.nz + 1 + kZChunk - 1) / kZChunk;        // chunks of <= 64 planes,
     p.zchunk = (int)((p.nz + 1 + nchunk - 1) / nchunk);                 // balanced in size
     const int64_t tz = (p.nz + 1 + p.zchunk - 1) / p.zchunk;
     const int64_t ctas = (int64_t)p.tiles_x * p.tiles_y * tz;
-    if (path == OVX_INT8) return launch_mode<OVX_INT8>(mode, p, ctas, st);
+    if (path == OVX_INT8)
+        return i8_ey() == 4 ? launch_i8_mode<4>(mode, p, ctas, st) : launch_i8_mode<8>(mode, p, ctas, st);
     if (path == OVX_FP64) return launch_mode<OVX_FP64>(mode, p, ctas, st);
     return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);
 }

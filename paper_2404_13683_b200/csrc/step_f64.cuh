@@ -28,7 +28,7 @@ struct SmemF2 {
 template <int MODE>
 __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     constexpr int NT = F2::NT, TY = F2::TY, PLANE = F2::PLANE, PF = F2::PF;
-    extern __shared__ __align__(16) uint8_t smem_raw[];
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     SmemF2 &S = *reinterpret_cast<SmemF2 *>(smem_raw);
     const int t = threadIdx.x;
     const int lx = t & 31, ly = t >> 5;

@@ -1,0 +1,410 @@
+// step_i8.cuh — fused time step of the INT8 tensor-core path (OVX_INT8); included by kernels.cu.
+//
+// CTA = 32 × EY elements per layer (one thread per element; one halo ring recomputed by the
+// neighbour tiles), marching in z over a chunk of node planes.  Per layer L (one iteration):
+//   1. prefetch (registers): node plane L+2 of u^{it}, the update operands of plane L-1
+//      (u^{it-1}, w, mask), the material id of layer L+2;
+//   2. PAPER.md Eqs. 10-16 on CUDA cores: s_e = max|ū_e|, v = trunc(2^56 ū_e / s_e) (one
+//      reciprocal), byte slices of v + 2^56 packed as 4 half-word u8 arrays (variant B) into the
+//      K-major A operand;  one thread per M=128 tile issues the tcgen05.mma.kind::i8 chain
+//      (4 arrays × [3 K-steps against −K_e^INT8 ⊗ I_2 + 2 K-steps of the G bytes against
+//      −128·I ⊗ I_2]  = Eq. 17 with the Eq. 9 diagonal folded in, variant D);
+//   3. while the tensor core runs: scatter of layer L-1's element forces into the two smem force
+//      planes in global element order, and the central-difference update of plane L-1
+//      (Eq. 3 / L263-L266 with the sign of Eq. 3);
+//   4. epilogue of layer L: tcgen05.ld, exact two-limb recombination y = Σ_j 256^j C_j,
+//      f_e = RN(c1 s_e 2^-56)·RN(y) -> smem fe.
+// The scatter order, the integer path and every rounding are those of the oracle
+// (oracle/ovx_oracle.c, DIGITS_BYTES_FOLD), so results are bit-identical to it.
+
+template <int EY_>
+struct I8 {
+    static constexpr int EY = EY_;
+    static constexpr int NE = EX * EY;                 // elements per layer = threads
+    static constexpr int NT = NE;
+    static constexpr int MT = NE / 128;                // M=128 MMA tiles per layer
+    static constexpr int TY = EY - 1;
+    static constexpr int PY = EY + 1;
+    static constexpr int NOWN = TX * TY;
+    static constexpr int PLANE = PX * PY * 3;
+    static constexpr int PF = (PLANE + NT - 1) / NT;
+    static constexpr int MINB = MT == 1 ? 2 : 1;
+    static constexpr int TMEM_COLS = MT * 256;
+};
+
+template <int EY>
+struct SmemI8 {
+    using C = I8<EY>;
+    uint8_t A[C::MT][4][A1_BYTES];      // [M-tile][half-word array], K-major canonical layout
+    double fe[24][C::NE];
+    alignas(128) uint8_t B[6 * B1_PITCH];
+    alignas(128) uint8_t BI[2][6 * BI_PITCH];
+    double up[4][C::PLANE];             // ring: L-1 (update), L, L+1 (gather), L+2 (parked)
+    double facc[2][C::NOWN * 3];
+    uint64_t mbar[C::MT];
+    uint32_t tmem;
+};
+
+template <int MODE, int EY>
+__global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepParams p) {
+    using C = I8<EY>;
+    constexpr int NT = C::NT, TY = C::TY, NOWN = C::NOWN, PLANE = C::PLANE, PF = C::PF;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    SmemI8<EY> &S = *reinterpret_cast<SmemI8<EY> *>(smem_raw);
+    const int t = threadIdx.x;
+    const int warp = t >> 5;
+    const int mt = warp >> 2;                 // M-tile of this thread's element
+    const int row = t & 127;                  // MMA row = TMEM lane
+
+    int bid = blockIdx.x;
+    const int tx = bid % p.tiles_x;
+    bid /= p.tiles_x;
+    const int ty = bid % p.tiles_y;
+    const int tz = bid / p.tiles_y;
+    const int64_t X0 = (int64_t)tx * TX, Y0 = (int64_t)ty * TY;
+    const int64_t Z0 = (int64_t)tz * p.zchunk;
+    const int64_t Z1 = min(Z0 + (int64_t)p.zchunk, p.nz + 1);
+    const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
+    const int64_t PSTRIDE = NX1 * NY1;
+
+    const int lx = t % EX, ly = t / EX;
+    const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
+    const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
+    const uint8_t *matp = p.mat + (ein ? ex + p.nx * ey : 0);
+    const int64_t mstride = p.nx * p.ny;
+
+    // loop-invariant prefetch sources (element offsets within one plane of u)
+    int64_t pfoff[PF];
+    bool pfok[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+        const int idx = t + j * NT;
+        const int py = idx / (PX * 3);
+        const int rem = idx - py * (PX * 3);
+        const int px = rem / 3, c = rem - px * 3;
+        const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
+        pfok[j] = idx < PLANE && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1;
+        pfoff[j] = pfok[j] ? 3 * (ix + NX1 * iy) + c : 0;
+    }
+    // update role: owned node (nxl, nyl) of the tile
+    const int nxl = t % TX, nyl = t / TX;
+    const int64_t uix = X0 + nxl, uiy = Y0 + nyl;
+    const bool own = t < NOWN && uix < NX1 && uiy < NY1;
+    const int64_t ucol = own ? uix + NX1 * uiy : 0;
+
+    bool has_src = false, has_rec = false;
+    if (MODE == MODE_STEP) {
+        for (int k = 0; k < p.nsrc; ++k) {
+            const int64_t n = p.src_dof[k] / 3;
+            const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+            has_src |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
+        }
+        if (p.it < p.rec_nt)
+            for (int k = 0; k < p.nrec; ++k) {
+                const int64_t n = p.rec_node[k];
+                const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+                has_rec |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
+            }
+    }
+
+    // ---- one-time setup: B operands, zero K-padding chunks, TMEM, mbarriers ----
+    for (int idx = t; idx < 48 * 96; idx += NT) {
+        const int n = idx / 96, kb = idx - n * 96;
+        const int off = (n >> 3) * B1_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
+        S.B[off] = ((kb & 1) == (n & 1)) ? (uint8_t)(-(int)c_K8[(n >> 1) * 48 + (kb >> 1)]) : (uint8_t)0;
+    }
+    for (int idx = t; idx < 2 * 48 * 32; idx += NT) {
+        const int s2 = idx / (48 * 32), r2 = idx - s2 * 48 * 32;
+        const int n = r2 / 32, kb = r2 - n * 32;
+        const int off = (n >> 3) * BI_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
+        const int k = 16 * s2 + (kb >> 1);
+        S.BI[s2][off] = ((kb & 1) == (n & 1) && k == (n >> 1)) ? (uint8_t)0x80 : (uint8_t)0;
+    }
+    for (int idx = t; idx < C::MT * 4 * 128; idx += NT) {
+        const int a = idx >> 7, r = idx & 127;
+        *reinterpret_cast<uint4 *>(&S.A[a >> 2][a & 3][(r >> 3) * A1_PITCH + 6 * 128 + (r & 7) * 16]) =
+            make_uint4(0, 0, 0, 0);
+    }
+    if (warp == 0) ptx::tmem_alloc<C::TMEM_COLS>(&S.tmem);
+    if (t == 0)
+        for (int mm = 0; mm < C::MT; ++mm) ptx::mbar_init(&S.mbar[mm], 1);
+    for (int i = t; i < 2 * NOWN * 3; i += NT) (&S.facc[0][0])[i] = 0.0;
+    const int64_t Lfirst = max(Z0 - 1, (int64_t)0);
+    for (int j = 0; j < 2; ++j) {
+        const int64_t iz = Lfirst + j;
+        double *dst = S.up[iz & 3];
+        for (int idx = t; idx < PLANE; idx += NT) {
+            const int py = idx / (PX * 3);
+            const int rem = idx - py * (PX * 3);
+            const int px = rem / 3, c = rem - px * 3;
+            const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
+            dst[idx] = (iz <= p.nz && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1)
+                           ? __ldg(p.u + 3 * (ix + NX1 * (iy + NY1 * iz)) + c) : 0.0;
+        }
+    }
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+
+    uint32_t phase = 0;
+    // material ids: current layer and the next one (fetched two layers ahead)
+    int mcur = (ein && Lfirst < p.nz) ? (int)__ldg(matp + mstride * Lfirst) : kZeroMat;
+    int mnxt = (ein && Lfirst + 1 < p.nz) ? (int)__ldg(matp + mstride * (Lfirst + 1)) : kZeroMat;
+    // update operands of the plane updated in this iteration (prefetched one iteration earlier)
+    double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;
+    uint8_t dm = 0;
+    bool prev_layer = false;     // did the previous iteration compute a layer (fe valid)?
+    int64_t prevL = -1;
+
+    for (int64_t L = Z0 - 1; L <= Z1; ++L) {
+        const bool layer_ok = (L >= 0 && L < p.nz && L < Z1);
+        const int64_t Ld = L - 1;                               // layer scattered in this iteration
+        const bool plane_done = (Ld >= Z0 && Ld <= p.nz && Ld < Z1);   // plane Ld completes now
+        // ---- 1. prefetch: plane L+2, material of layer L+2, update operands of plane L (next iter.) ----
+        const int64_t pz = L + 2;
+        const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < p.nz);
+        double pfv[PF];
+        const double *uplane = p.u + 3 * PSTRIDE * pz;
+#pragma unroll
+        for (int j = 0; j < PF; ++j) pfv[j] = (pf && pfok[j]) ? __ldg(uplane + pfoff[j]) : 0.0;
+        const int mfar = (ein && L + 2 < p.nz && L + 2 > Lfirst + 1) ? (int)__ldg(matp + mstride * (L + 2)) : kZeroMat;
+        const bool upd_next = own && (L >= Z0 && L <= p.nz && L < Z1);
+        const int64_t un_next = ucol + PSTRIDE * L;
+        double upv_n[3] = {0.0, 0.0, 0.0}, wn_n = 0.0;
+        uint8_t dm_n = 0;
+        if (MODE == MODE_STEP && upd_next) {
+            upv_n[0] = p.uo[3 * un_next];
+            upv_n[1] = p.uo[3 * un_next + 1];
+            upv_n[2] = p.uo[3 * un_next + 2];
+            wn_n = __ldg(p.w + un_next);
+            dm_n = p.dmask ? __ldg(p.dmask + un_next) : (uint8_t)0;
+        }
+
+        // ---- 2. integer image of ū_e for layer L, tensor-core hand-off ----
+        double s = 0.0;
+        int64_t dj = -1;
+        bool dbg = false;
+        if (layer_ok) {
+            const int64_t eid = ex + p.nx * (ey + p.ny * L);
+            dj = eid - p.dbg_e0;
+            dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
+                  dj >= 0 && dj < p.dbg_ne;
+            double ue[24];
+            gather<C::PY>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
+            const double cG = c_mat[mcur].cG;
+            double amax = 0.0;
+#pragma unroll
+            for (int i = 0; i < 24; ++i) amax = fmax(amax, fabs(ue[i]));
+            s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
+            const bool deg = !ein || !(s >= 0x1p-1022) || isinf(s);
+            const bool straight = !deg && s >= 0x1p-960;
+            const double r = 1.0 / s;                          // RN(1/s_e), reading Q7
+            const double R = __dmul_rn(r, 0x1p56);             // exact power-of-two scaling
+            uint8_t *Ab = &S.A[mt][0][0];
+            const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
+#pragma unroll
+            for (int ch = 0; ch < 6; ++ch) {                    // chunks 0-2: u part, 3-5: G part
+                long long v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const double ub = ch < 3 ? ue[ch * 8 + q] : __dmul_rn(cG, ue[(ch - 3) * 8 + q]);
+                    v[q] = straight ? __double2ll_rz(__dmul_rn(ub, R))
+                                    : (deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), 0x1p56)));
+                }
+                uint32_t lo[8], hi[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const unsigned long long vp = (unsigned long long)v[q] + (1ull << 56);
+                    lo[q] = (uint32_t)vp;
+                    hi[q] = (uint32_t)(vp >> 32);
+                    if (MODE == MODE_DEBUG && dbg) {
+                        const int k = ch * 8 + q;
+                        if (p.dbg_v) p.dbg_v[dj * 48 + k] = v[q];
+                        if (p.dbg_d)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = (uint8_t)(vp >> (8 * j));
+                    }
+                }
+                const uint32_t off = rowoff + (uint32_t)ch * 128;
+#pragma unroll
+                for (int pa = 0; pa < 4; ++pa) {
+                    const uint32_t *src = pa < 2 ? lo : hi;
+                    const uint32_t sel = (pa & 1) ? 0x7632u : 0x5410u;
+                    uint4 wv;
+                    wv.x = __byte_perm(src[0], src[1], sel);
+                    wv.y = __byte_perm(src[2], src[3], sel);
+                    wv.z = __byte_perm(src[4], src[5], sel);
+                    wv.w = __byte_perm(src[6], src[7], sel);
+                    *reinterpret_cast<uint4 *>(Ab + pa * A1_BYTES + off) = wv;
+                }
+            }
+            if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
+            ptx::fence_proxy_async_smem();
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + mt) : "memory");   // the 4 warps of this M-tile
+            if (row == 0) {
+                ptx::tc_fence_after();
+                const uint32_t b0 = ptx::smem_u32(&S.B[0]);
+                const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
+                const uint32_t a0 = ptx::smem_u32(&S.A[mt][0][0]);
+#pragma unroll
+                for (int pa = 0; pa < 4; ++pa) {
+                    const uint32_t ab = a0 + pa * A1_BYTES;
+                    const uint32_t d = S.tmem + mt * 256 + pa * 64;
+#pragma unroll
+                    for (int ks = 0; ks < 3; ++ks)
+                        ptx::mma_i8(d, ptx::smem_desc(ab + ks * 256, 128, A1_PITCH),
+                                    ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC, ks > 0 ? 1u : 0u);
+                    ptx::mma_i8(d, ptx::smem_desc(ab + 3 * 128, 128, A1_PITCH), ptx::smem_desc(bi0, 128, BI_PITCH),
+                                IDESC, 1u);
+                    ptx::mma_i8(d, ptx::smem_desc(ab + 5 * 128, 128, A1_PITCH), ptx::smem_desc(bi1, 128, BI_PITCH),
+                                IDESC, 1u);
+                }
+                ptx::mma_commit(&S.mbar[mt]);
+            }
+        }
+
+        // ---- 3. (overlaps the MMAs) scatter of layer Ld = L-1 and update of plane Ld ----
+        if (t < NOWN) {
+            const int e00 = nxl + EX * nyl, e10 = e00 + 1, e01 = e00 + EX, e11 = e01 + 1;
+            double *fl = &S.facc[Ld & 1][t * 3];
+            double *fh = &S.facc[L & 1][t * 3];
+            const bool bot_iface = (p.slab_flags & 1) && Ld == 0;
+            const bool top_iface = (p.slab_flags & 2) && Ld == p.nz;
+            if (prev_layer && Ld >= Z0 && bot_iface) {
+                if (own)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        double *b = p.iface_bot_b + 12 * ucol + c;
+                        b[0] = S.fe[3 * 2 + c][e00];
+                        b[3] = S.fe[3 * 3 + c][e10];
+                        b[6] = S.fe[3 * 1 + c][e01];
+                        b[9] = S.fe[3 * 0 + c][e11];
+                    }
+            } else if (prev_layer && Ld >= Z0) {      // bottom corners of layer Ld -> plane Ld
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double f = fl[c];
+                    f = __dadd_rn(f, S.fe[3 * 2 + c][e00]);
+                    f = __dadd_rn(f, S.fe[3 * 3 + c][e10]);
+                    f = __dadd_rn(f, S.fe[3 * 1 + c][e01]);
+                    f = __dadd_rn(f, S.fe[3 * 0 + c][e11]);
+                    fl[c] = f;
+                }
+            }
+            if (prev_layer && Ld + 1 < Z1) {           // top corners of layer Ld -> plane Ld+1
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double f = fh[c];
+                    f = __dadd_rn(f, S.fe[3 * 6 + c][e00]);
+                    f = __dadd_rn(f, S.fe[3 * 7 + c][e10]);
+                    f = __dadd_rn(f, S.fe[3 * 5 + c][e01]);
+                    f = __dadd_rn(f, S.fe[3 * 4 + c][e11]);
+                    fh[c] = f;
+                }
+            }
+            if (plane_done && own) {
+                const int64_t un_id = ucol + PSTRIDE * Ld;
+                if (top_iface) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = fl[c];
+                } else if (!bot_iface) {
+                    const double *up = &S.up[Ld & 3][((nyl + 1) * PX + (nxl + 1)) * 3];
+                    if (MODE == MODE_STEP) {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const int64_t dof = 3 * un_id + c;
+                            double F = 0.0;
+                            if (has_src)
+                                for (int k = 0; k < p.nsrc; ++k)
+                                    if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
+                            const double b = __dsub_rn(__dmul_rn(2.0, up[c]), upv[c]);
+                            double un = __fma_rn(wn, __dsub_rn(F, fl[c]), b);
+                            if ((dm >> c) & 1) un = 0.0;
+                            p.uo[dof] = un;
+                            if (has_rec)
+                                for (int k = 0; k < p.nrec; ++k)
+                                    if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) p.fout[3 * un_id + c] = fl[c];
+                    }
+                }
+            }
+            if (plane_done) fl[0] = fl[1] = fl[2] = 0.0;
+        }
+
+        // ---- 4. epilogue of layer L ----
+        if (layer_ok) {
+            if (warp == 4 * mt) ptx::mbar_wait(&S.mbar[mt], phase);
+            phase ^= 1;
+        }
+        __syncthreads();   // MMAs of layer L done; all reads of fe (layer L-1) done
+        if (layer_ok) {
+            ptx::tc_fence_after();
+            const double alpha = -__dmul_rn(c_mat[mcur].c1, __dmul_rn(s, 0x1p-56));   // −RN(c1·s·2^-56)
+            const uint32_t tb = S.tmem + ((uint32_t)((warp & 3) * 32) << 16) + mt * 256;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {           // 8 outputs per round (16 columns per array)
+                uint32_t R0[16], R1[16], R2[16], R3[16];
+                ptx::tmem_ld16(tb + 0 + cc * 16, R0);
+                ptx::tmem_ld16(tb + 64 + cc * 16, R1);
+                ptx::tmem_ld16(tb + 128 + cc * 16, R2);
+                ptx::tmem_ld16(tb + 192 + cc * 16, R3);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int i = cc * 8 + q;
+                    const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
+                    const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
+                    const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
+                    const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
+                    // D holds −C_j, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^44
+                    const double dlo = ptx::limb_magic(c0, c1_, c2_, c3) - (0x1.8p52 + 0x1p31);
+                    const double dhi = ptx::limb_magic(c4, c5, c6, c7) - (0x1.8p52 + 0x1p31);
+                    const double Y = __fma_rn(dhi, 0x1p32, dlo);    // RN(−y)
+                    const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
+                    if (MODE == MODE_DEBUG && dbg) {
+                        const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};
+                        __int128 y = 0;
+#pragma unroll
+                        for (int j = 7; j >= 0; --j) y = y * 256 - (__int128)Cj[j];
+                        if (p.dbg_C)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) p.dbg_C[dj * 192 + j * 24 + i] = -Cj[j];
+                        if (p.dbg_yhi) p.dbg_yhi[dj * 24 + i] = (long long)(y >> 64);
+                        if (p.dbg_ylo) p.dbg_ylo[dj * 24 + i] = (long long)(unsigned long long)y;
+                        if (p.dbg_fe) p.dbg_fe[dj * 24 + i] = f;
+                    }
+                    S.fe[i][t] = f;
+                }
+            }
+            ptx::tc_fence_before();
+        }
+        // ---- park plane L+2 (slot of plane L-2, no longer read), advance the carried operands ----
+        if (pf) {
+            double *dst = S.up[pz & 3];
+#pragma unroll
+            for (int j = 0; j < PF; ++j) {
+                const int idx = t + j * NT;
+                if (idx < PLANE) dst[idx] = pfv[j];
+            }
+        }
+        prev_layer = layer_ok;
+        prevL = L;
+        if (L >= Lfirst) {
+            mcur = mnxt;
+            mnxt = mfar;
+        }
+        upv[0] = upv_n[0];
+        upv[1] = upv_n[1];
+        upv[2] = upv_n[2];
+        wn = wn_n;
+        dm = dm_n;
+        __syncthreads();
+    }
+    (void)prevL;
+    ptx::tc_fence_after();
+    if (warp == 0) ptx::tmem_dealloc<C::TMEM_COLS>(S.tmem);
+}
