@@ -14,8 +14,9 @@
 //      (Eq. 3 / L263-L266 with the sign of Eq. 3);
 //   4. epilogue of layer L: tcgen05.ld, exact two-limb recombination y = Σ_j 256^j C_j,
 //      f_e = RN(c1 s_e 2^-56)·RN(y) -> smem fe.
-// The scatter order, the integer path and every rounding are those of the oracle
-// (oracle/ovx_oracle.c, DIGITS_BYTES_FOLD), so results are bit-identical to it.
+// The scatter order, the integer path and every rounding follow the definitions in DESIGN.md
+// (byte slices + folded diagonal), which the test oracle implements independently: results
+// are bit-identical to it.
 
 template <int EY_>
 struct I8 {
