@@ -88,7 +88,9 @@ ovx_status ovx_set_dt(ovx_ctx *ctx, double dt);
 /* Derive K_e^INT8 on the host in exact rational arithmetic,
  * check that all 1152 entries are integers in [-128,127] (L110; else OVX_EINVAL),
  * build per-material constants and the per-node w = dt²/m (Eq. 6, m_n = Σ ρ_e ds³/8).
- * path: OVX_INT8, OVX_FP64 or OVX_FP64_DENSE.  stages: M (only 8 is supported by the kernels). */
+ * path: OVX_INT8, OVX_FP64 or OVX_FP64_DENSE.  stages: M, the number of INT8 stages (a = 2^{7M},
+ * PAPER.md Eq. 16, Table 3): 8 (FP64-class), or 4 / 6 on the INT8 path (the paper's M = 4 is
+ * FP32-class); the FP64 paths require 8. */
 ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages);
 /* Copy the library's derived K_e^INT8 (24x48 row-major) to host memory. */
 ovx_status ovx_get_int8_matrix(ovx_ctx *ctx, int8_t *out);

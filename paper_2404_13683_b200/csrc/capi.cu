@@ -115,6 +115,7 @@ StepParams base_params(ovx_ctx *ctx) {
     p.w = ctx->d_w;
     p.mat = ctx->d_mat;
     p.dmask = ctx->d_mask;
+    p.stages = ctx->stages;
     return p;
 }
 
@@ -297,7 +298,8 @@ ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
     if (!ctx->have_grid || !ctx->have_emat) return fail(ctx, OVX_ESTATE, "set grid and element materials first");
     if (path != OVX_INT8 && path != OVX_FP64 && path != OVX_FP64_DENSE)
         return fail(ctx, OVX_EINVAL, "path must be OVX_INT8, OVX_FP64 or OVX_FP64_DENSE");
-    if (stages != 8) return fail(ctx, OVX_EINVAL, "only M = 8 stages is implemented");
+    if (stages != 8 && !(path == OVX_INT8 && (stages == 4 || stages == 6)))
+        return fail(ctx, OVX_EINVAL, "stages: M = 8 (all paths), or M = 4 / 6 on the INT8 path");
     if (derive_element_matrices(ctx->k8, ctx->Ak, ctx->Ag) != 0)
         return fail(ctx, OVX_EINVAL, "K_e^INT8 derivation produced a non-INT8 entry (PAPER.md L110 violated)");
     for (int r = 0; r < 24; ++r)

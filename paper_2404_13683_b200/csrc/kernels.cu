@@ -151,24 +151,24 @@ int i8_ey() {
     return ey;
 }
 
-template <int MODE, int EY>
+template <int MODE, int EY, int M>
 cudaError_t launch_i8(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
     const int smem = (int)sizeof(SmemI8<EY>);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_i8<MODE, EY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_i8<MODE, EY, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_i8<MODE, EY><<<(unsigned)ctas, I8<EY>::NT, smem, st>>>(p);
+    step_i8<MODE, EY, M><<<(unsigned)ctas, I8<EY>::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-template <int EY>
+template <int EY, int M>
 cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
-    if (mode == MODE_STEP) return launch_i8<MODE_STEP, EY>(p, ctas, st);
-    if (mode == MODE_APPLY) return launch_i8<MODE_APPLY, EY>(p, ctas, st);
-    return launch_i8<MODE_DEBUG, EY>(p, ctas, st);
+    if (mode == MODE_STEP) return launch_i8<MODE_STEP, EY, M>(p, ctas, st);
+    if (mode == MODE_APPLY) return launch_i8<MODE_APPLY, EY, M>(p, ctas, st);
+    return launch_i8<MODE_DEBUG, EY, M>(p, ctas, st);
 }
 
 template <int PATH, int MODE>
@@ -282,15 +282,18 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
 }
 
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
-    const int ty = path == OVX_INT8 ? i8_ey() - 1 : V1<OVX_FP64>::TY;
+    const int ty = path == OVX_INT8 ? (p.stages == 8 ? i8_ey() : 8) - 1 : V1<OVX_FP64>::TY;
     p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
     p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
     const int64_t nchunk = (p.nz + 1 + kZChunk - 1) / kZChunk;        // chunks of <= 64 planes,
     p.zchunk = (int)((p.nz + 1 + nchunk - 1) / nchunk);                 // balanced in size
     const int64_t tz = (p.nz + 1 + p.zchunk - 1) / p.zchunk;
     const int64_t ctas = (int64_t)p.tiles_x * p.tiles_y * tz;
-    if (path == OVX_INT8)
-        return i8_ey() == 4 ? launch_i8_mode<4>(mode, p, ctas, st) : launch_i8_mode<8>(mode, p, ctas, st);
+    if (path == OVX_INT8) {
+        if (p.stages == 4) return launch_i8_mode<8, 4>(mode, p, ctas, st);
+        if (p.stages == 6) return launch_i8_mode<8, 6>(mode, p, ctas, st);
+        return i8_ey() == 4 ? launch_i8_mode<4, 8>(mode, p, ctas, st) : launch_i8_mode<8, 8>(mode, p, ctas, st);
+    }
     if (path == OVX_FP64) return launch_mode<OVX_FP64>(mode, p, ctas, st);
     return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);
 }

@@ -42,6 +42,7 @@ struct StepParams {
     // z-slab decomposition (multi-GPU): bit 0 = local plane 0 is an interface
     // owned by this rank (its lower-layer partial arrives from below), bit 1 = the top local
     // plane is an interface owned by the rank above (send its partial, do not update it)
+    int stages;            // INT8 path: M (4, 6 or 8)
     int slab_flags;
     double *iface_top_A;   // [NX1*NY1][3]   partial force of the top plane (bit 1)
     double *iface_bot_b;   // [NX1*NY1][4][3] the 4 layer-0 contributions to plane 0 (bit 0)

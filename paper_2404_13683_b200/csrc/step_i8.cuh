@@ -46,9 +46,17 @@ struct SmemI8 {
     uint32_t tmem;
 };
 
-template <int MODE, int EY>
+// M: number of INT8 stages (Eq. 16; a = 2^{7M}).  Byte slices of v + 2^{7M} need
+// NB = ceil((7M+1)/8) bytes = NA half-word arrays: M = 8 -> 4 arrays, M = 6 -> 3, M = 4 -> 2
+// (Table 3's M = 4 / M = 8 comparison, NEXT-4).
+template <int MODE, int EY, int M = 8>
 __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepParams p) {
     using C = I8<EY>;
+    constexpr int NB = (7 * M + 1 + 7) / 8;
+    constexpr int NA = (NB + 1) / 2;
+    constexpr double SCALE = (double)(1ull << (7 * M));          // a = 2^{7M}
+    constexpr double ISCALE = 1.0 / SCALE;                        // exact power of two
+    constexpr unsigned long long AOFF = 1ull << (7 * M);
     constexpr int NT = C::NT, TY = C::TY, NOWN = C::NOWN, PLANE = C::PLANE, PF = C::PF;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     SmemI8<EY> &S = *reinterpret_cast<SmemI8<EY> *>(smem_raw);
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
             const bool deg = !ein || !(s >= 0x1p-1022) || isinf(s);
             const bool straight = !deg && s >= 0x1p-960;
             const double r = 1.0 / s;                          // RN(1/s_e), reading Q7
-            const double R = __dmul_rn(r, 0x1p56);             // exact power-of-two scaling
+            const double R = __dmul_rn(r, SCALE);              // exact power-of-two scaling
             uint8_t *Ab = &S.A[mt][0][0];
             const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
 #pragma unroll
@@ -211,12 +219,12 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
                 for (int q = 0; q < 8; ++q) {
                     const double ub = ch < 3 ? ue[ch * 8 + q] : __dmul_rn(cG, ue[(ch - 3) * 8 + q]);
                     v[q] = straight ? __double2ll_rz(__dmul_rn(ub, R))
-                                    : (deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), 0x1p56)));
+                                    : (deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), SCALE)));
                 }
                 uint32_t lo[8], hi[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const unsigned long long vp = (unsigned long long)v[q] + (1ull << 56);
+                    const unsigned long long vp = (unsigned long long)v[q] + AOFF;
                     lo[q] = (uint32_t)vp;
                     hi[q] = (uint32_t)(vp >> 32);
                     if (MODE == MODE_DEBUG && dbg) {
@@ -224,12 +232,12 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
                         if (p.dbg_v) p.dbg_v[dj * 48 + k] = v[q];
                         if (p.dbg_d)
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = (uint8_t)(vp >> (8 * j));
+                            for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = j < NB ? (uint8_t)(vp >> (8 * j)) : 0;
                     }
                 }
                 const uint32_t off = rowoff + (uint32_t)ch * 128;
 #pragma unroll
-                for (int pa = 0; pa < 4; ++pa) {
+                for (int pa = 0; pa < NA; ++pa) {
                     const uint32_t *src = pa < 2 ? lo : hi;
                     const uint32_t sel = (pa & 1) ? 0x7632u : 0x5410u;
                     uint4 wv;
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
                 const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
                 const uint32_t a0 = ptx::smem_u32(&S.A[mt][0][0]);
 #pragma unroll
-                for (int pa = 0; pa < 4; ++pa) {
+                for (int pa = 0; pa < NA; ++pa) {
                     const uint32_t ab = a0 + pa * A1_BYTES;
                     const uint32_t d = S.tmem + mt * 256 + pa * 64;
 #pragma unroll
@@ -344,15 +352,15 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
         __syncthreads();   // MMAs of layer L done; all reads of fe (layer L-1) done
         if (layer_ok) {
             ptx::tc_fence_after();
-            const double alpha = -__dmul_rn(c_mat[mcur].c1, __dmul_rn(s, 0x1p-56));   // −RN(c1·s·2^-56)
+            const double alpha = -__dmul_rn(c_mat[mcur].c1, __dmul_rn(s, ISCALE));   // −RN(c1·s·2^{-7M})
             const uint32_t tb = S.tmem + ((uint32_t)((warp & 3) * 32) << 16) + mt * 256;
 #pragma unroll
             for (int cc = 0; cc < 3; ++cc) {           // 8 outputs per round (16 columns per array)
-                uint32_t R0[16], R1[16], R2[16], R3[16];
+                uint32_t R0[16], R1[16], R2[16] = {}, R3[16] = {};
                 ptx::tmem_ld16(tb + 0 + cc * 16, R0);
                 ptx::tmem_ld16(tb + 64 + cc * 16, R1);
-                ptx::tmem_ld16(tb + 128 + cc * 16, R2);
-                ptx::tmem_ld16(tb + 192 + cc * 16, R3);
+                if (NA > 2) ptx::tmem_ld16(tb + 128 + cc * 16, R2);
+                if (NA > 3) ptx::tmem_ld16(tb + 192 + cc * 16, R3);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
@@ -363,8 +371,8 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
                     const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
                     // D holds −C_j, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^44
                     const double dlo = ptx::limb_magic(c0, c1_, c2_, c3) - (0x1.8p52 + 0x1p31);
-                    const double dhi = ptx::limb_magic(c4, c5, c6, c7) - (0x1.8p52 + 0x1p31);
-                    const double Y = __fma_rn(dhi, 0x1p32, dlo);    // RN(−y)
+                    const double dhi = NA > 2 ? ptx::limb_magic(c4, c5, c6, c7) - (0x1.8p52 + 0x1p31) : 0.0;
+                    const double Y = NA > 2 ? __fma_rn(dhi, 0x1p32, dlo) : dlo;    // RN(−y)
                     const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
                     if (MODE == MODE_DEBUG && dbg) {
                         const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};

@@ -301,13 +301,13 @@ class Ovx:
         self._call("ovx_step_end")
 
     # -- convenience ---------------------------------------------------------------
-    def load_model(self, m, path: int = OVX_INT8) -> None:
+    def load_model(self, m, path: int = OVX_INT8, stages: int = 8) -> None:
         """Upload a workloads.Model-like object (grid, materials, mask, dt, sources) and set up."""
         self.set_grid(m.nx, m.ny, m.nz, m.ds)
         self.set_materials(m.rho, m.kappa, m.G)
         self.set_element_materials(m.mat)
         self.set_dirichlet(m.dirichlet)
-        self.setup_elements(path, 8)
+        self.setup_elements(path, stages)
         self.set_dt(m.dt)
         if len(m.src_node):
             self.set_sources(m.src_node, m.src_axis, m.amp)

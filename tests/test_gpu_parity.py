@@ -246,3 +246,44 @@ def test_receiver_traces_and_err_metric(ovxmod):
     live = np.abs(a64).sum(1) > 0
     err = physics.err_metric(a8[live], a64[live])
     assert err < 1e-24
+
+
+@pytest.mark.parametrize("M", [4, 6])
+def test_int8_stage_variants_bit_exact(ovxmod, M):
+    """NEXT-4: M = 4 / 6 INT8 stages (a = 2^{7M}) on the tensor cores, bit-exact vs the oracle."""
+    m = wl.small_random(35, 9, 11, ds=0.01)
+    u = wl.random_field(m)
+    s = ovxmod.Ovx(0)
+    s.load_model(m, 0, stages=M)
+    f = s.apply_K(u)
+    ref = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=oracle.PATH_INT8, M=M,
+                         digits=oracle.DIGITS_BYTES_FOLD)
+    assert np.array_equal(f, ref)
+    rec = s.debug_element_ints(u, 0, 40)
+    for e in range(40):
+        nodes = oracle.element_nodes(m.nx, m.ny, e)
+        ue = np.concatenate([u[3 * n:3 * n + 3] for n in nodes])
+        r = oracle.element_int8(ue, m.kappa[m.mat[e]], m.G[m.mat[e]], m.ds, M, oracle.DIGITS_BYTES_FOLD)
+        nb = r["d"].shape[0]
+        assert np.array_equal(rec["v"][e], r["v"])
+        assert np.array_equal(rec["d"][e][:nb].astype(np.int32), r["d"])
+        assert np.array_equal(rec["C"][e][:nb].astype(np.int64), r["C"])
+        assert rec["y"][e] == r["y"]
+
+
+def test_table3_hierarchy_on_gpu(ovxmod):
+    """PAPER.md Table 3 / L245 on the tensor cores: error vs the exact product falls from M = 4
+    (FP32-class, ~2^-28) to M = 8 (FP64-class), measured on K·u for a random u (reading Q21)."""
+    from fractions import Fraction as Fr
+    from oracle import assemble
+    m = wl.small_random(3, 3, 3, ds=2e-3)
+    u = wl.random_field(m)
+    K = assemble.assemble_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G)
+    ref = K @ u
+    errs = {}
+    for M in (4, 6, 8):
+        s = ovxmod.Ovx(0)
+        s.load_model(m, 0, stages=M)
+        errs[M] = np.linalg.norm(s.apply_K(u) - ref) / np.linalg.norm(ref)
+    assert errs[8] < 1e-14 and errs[6] < 1e-11 and 1e-10 < errs[4] < 1e-6
+    assert errs[8] < errs[6] < errs[4]
