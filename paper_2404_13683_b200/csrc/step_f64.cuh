@@ -113,11 +113,13 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         }
     };
     double facc[3] = {0.0, 0.0, 0.0};   // plane L (receives layer L-1 top + layer L bottom)
+    // material ids of the current and next layer; the one after is fetched two layers ahead
     int mcur = (ein && Lfirst < p.nz) ? (int)__ldg(matcol + mstride * Lfirst) : kZeroMat;
+    int mnxt = (ein && Lfirst + 1 < p.nz) ? (int)__ldg(matcol + mstride * (Lfirst + 1)) : kZeroMat;
     for (int64_t L = Z0 - 1; L < Z1; ++L) {
         const bool layer_ok = (L >= 0 && L < p.nz);
         const bool plane_done = (L >= Z0 && L <= p.nz);
-        const int mnext = (ein && L + 1 > Lfirst && L + 1 < p.nz) ? (int)__ldg(matcol + mstride * (L + 1)) : kZeroMat;
+        const int mfar = (ein && L + 2 > Lfirst + 1 && L + 2 < p.nz) ? (int)__ldg(matcol + mstride * (L + 2)) : kZeroMat;
         // ---- prefetch plane L+3 (parked next iteration) and the update operands of plane L ----
         const int64_t pz = L + 3;
         const bool pf = (pz > Lfirst + 2) && (L + 2 < Z1) && (L + 2 < p.nz);
@@ -202,7 +204,10 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) facc[c] = ntop[c];
         }
-        if (L >= Lfirst) mcur = mnext;
+        if (L >= Lfirst) {
+            mcur = mnxt;
+            mnxt = mfar;
+        }
 #pragma unroll
         for (int j = 0; j < PF; ++j) pend[j] = pfv[j];
         pend_z = pf ? pz : -1;
