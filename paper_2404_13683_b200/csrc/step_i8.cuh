@@ -215,11 +215,18 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
 #pragma unroll
             for (int ch = 0; ch < 6; ++ch) {                    // chunks 0-2: u part, 3-5: G part
                 long long v[8];
+                if (straight) {   // all but degenerate / tiny-s elements: one DMUL + one F2I per value
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const double ub = ch < 3 ? ue[ch * 8 + q] : __dmul_rn(cG, ue[(ch - 3) * 8 + q]);
-                    v[q] = straight ? __double2ll_rz(__dmul_rn(ub, R))
-                                    : (deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), SCALE)));
+                    for (int q = 0; q < 8; ++q) {
+                        const double ub = ch < 3 ? ue[ch * 8 + q] : __dmul_rn(cG, ue[(ch - 3) * 8 + q]);
+                        v[q] = __double2ll_rz(__dmul_rn(ub, R));
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const double ub = ch < 3 ? ue[ch * 8 + q] : __dmul_rn(cG, ue[(ch - 3) * 8 + q]);
+                        v[q] = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), SCALE));
+                    }
                 }
                 uint32_t lo[8], hi[8];
 #pragma unroll
