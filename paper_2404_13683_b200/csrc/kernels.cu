@@ -137,6 +137,23 @@ __device__ __forceinline__ void element_force_wht(const double (&ue)[24], const 
     }
 }
 
+// Exact double of the limb c0 + 2^8 c1 + 2^16 c2 + 2^24 c3 of the stage products (|c_j| < 2^21,
+// so the pairs p0, p1 fit 32 bits and the limb |.| < 2^46): p0 + 2^16 p1 is formed in the low
+// bits of the double 1.5·2^52 (one IMAD.WIDE; the multiplier is read from constant memory so
+// ptxas keeps it a single wide multiply-add), then the magic is subtracted exactly.
+__constant__ int32_t c_two16 = 65536;
+__device__ __forceinline__ double limb_exact(int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
+    const int32_t p0 = c0 + 256 * c1, p1 = c2 + 256 * c3;
+    long long acc = 0x4338000000000000ll + (long long)p0;
+    asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(acc) : "r"(p1), "r"(c_two16));
+    return __longlong_as_double(acc) - 0x1.8p52;
+}
+// max_i |x_i| of finite / infinite doubles as the integer max of their magnitude bit patterns
+// (monotone for non-NaN values; a NaN sorts above +inf and makes the element degenerate)
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+    return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+}
+
 #include "step_v1.cuh"
 #include "step_f64.cuh"
 #include "step_i8.cuh"

@@ -59,6 +59,13 @@ __device__ __forceinline__ double limb_magic(int32_t c0, int32_t c1, int32_t c2,
     return __hiloint2double((int)hi, (int)lo);
 }
 
+// One lane of a converged warp (elect.sync): keeps the tcgen05 issue code warp-uniform.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+
 // ---- proxy / tcgen05 fences --------------------------------------------------
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

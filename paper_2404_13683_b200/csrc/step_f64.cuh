@@ -116,6 +116,8 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     // material ids of the current and next layer; the one after is fetched two layers ahead
     int mcur = (ein && Lfirst < p.nz) ? (int)__ldg(matcol + mstride * Lfirst) : kZeroMat;
     int mnxt = (ein && Lfirst + 1 < p.nz) ? (int)__ldg(matcol + mstride * (Lfirst + 1)) : kZeroMat;
+    double nupv[3] = {0.0, 0.0, 0.0}, nwn = 0.0;
+    uint8_t ndm = 0;
     for (int64_t L = Z0 - 1; L < Z1; ++L) {
         const bool layer_ok = (L >= 0 && L < p.nz);
         const bool plane_done = (L >= Z0 && L <= p.nz);
@@ -129,14 +131,20 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         for (int j = 0; j < PF; ++j) pfv[j] = (pf && pfok[j]) ? __ldg(uplane + pfoff[j]) : 0.0;
         const bool upd = plane_done && own;
         const int64_t un_id = ucol + PSTRIDE * L;
-        double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;
-        uint8_t dm = 0;
-        if (MODE == MODE_STEP && upd) {
-            upv[0] = p.uo[3 * un_id];
-            upv[1] = p.uo[3 * un_id + 1];
-            upv[2] = p.uo[3 * un_id + 2];
-            wn = __ldg(p.w + un_id);
-            dm = p.dmask ? __ldg(p.dmask + un_id) : (uint8_t)0;
+        // update operands of plane L were loaded one layer ahead; fetch those of plane L+1
+        double upv[3] = {nupv[0], nupv[1], nupv[2]};
+        const double wn = nwn;
+        const uint8_t dm = ndm;
+        if (MODE == MODE_STEP) {
+            const int64_t L1 = L + 1;
+            if (own && L1 >= Z0 && L1 < Z1 && L1 <= p.nz) {
+                const int64_t nid = un_id + PSTRIDE;
+                nupv[0] = p.uo[3 * nid];
+                nupv[1] = p.uo[3 * nid + 1];
+                nupv[2] = p.uo[3 * nid + 2];
+                nwn = __ldg(p.w + nid);
+                ndm = p.dmask ? __ldg(p.dmask + nid) : (uint8_t)0;
+            }
         }
 
         double nbot[3] = {0.0, 0.0, 0.0}, ntop[3] = {0.0, 0.0, 0.0};

@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
     const int t = threadIdx.x;
     const int warp = t >> 5;
     const int mt = warp >> 2;                 // M-tile of this thread's element
+    const int wu = __shfl_sync(0xffffffffu, warp, 0);   // the warp index as a uniform value
     const int row = t & 127;                  // MMA row = TMEM lane
 
     int bid = blockIdx.x;
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
         // ---- 2. integer image of ū_e for layer L, tensor-core hand-off ----
         double s = 0.0;
         int64_t dj = -1;
-        bool dbg = false;
+        bool dbg = false, deg = false;
         if (layer_ok) {
             const int64_t eid = ex + p.nx * (ey + p.ny * L);
             dj = eid - p.dbg_e0;
@@ -202,20 +203,28 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
             double ue[24];
             gather<C::PY>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
             const double cG = c_mat[mcur].cG;
-            double amax = 0.0;
+            unsigned long long abits = 0;
 #pragma unroll
-            for (int i = 0; i < 24; ++i) amax = fmax(amax, fabs(ue[i]));
+            for (int i = 0; i < 24; ++i) {
+                const unsigned long long b = abs_bits(ue[i]);
+                abits = b > abits ? b : abits;
+            }
+            const double amax = __longlong_as_double((long long)abits);
             s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
-            const bool deg = !ein || !(s >= 0x1p-1022) || isinf(s);
-            const bool straight = !deg && s >= 0x1p-960;
+            deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
+            // fast conversion (one DMUL + one F2I per value) unless the warp holds a non-finite or a
+            // tiny-normal s (where r·2^{7M} would overflow); degenerate finite lanes use R = 0 -> v = 0
+            const bool vzero = !ein || !(s >= 0x1p-1022);
+            const bool fast = (s <= 0x1.fffffffffffffp1023) && (vzero || s >= 0x1p-960);
             const double r = 1.0 / s;                          // RN(1/s_e), reading Q7
-            const double R = __dmul_rn(r, SCALE);              // exact power-of-two scaling
+            const double R = vzero ? 0.0 : __dmul_rn(r, SCALE);   // exact power-of-two scaling
+            const bool wfast = __all_sync(0xffffffffu, fast);
             uint8_t *Ab = &S.A[mt][0][0];
             const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
 #pragma unroll
             for (int ch = 0; ch < 6; ++ch) {                    // chunks 0-2: u part, 3-5: G part
                 long long v[8];
-                if (straight) {   // all but degenerate / tiny-s elements: one DMUL + one F2I per value
+                if (wfast) {
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const double ub = ch < 3 ? ue[ch * 8 + q] : __dmul_rn(cG, ue[(ch - 3) * 8 + q]);
@@ -231,9 +240,14 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
                 uint32_t lo[8], hi[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const unsigned long long vp = (unsigned long long)v[q] + AOFF;
-                    lo[q] = (uint32_t)vp;
-                    hi[q] = (uint32_t)(vp >> 32);
+                    if constexpr (7 * M >= 32) {   // v + 2^{7M}: the offset only touches the high word
+                        lo[q] = (uint32_t)(unsigned long long)v[q];
+                        hi[q] = (uint32_t)((unsigned long long)v[q] >> 32) + (uint32_t)(AOFF >> 32);
+                    } else {                        // v + 2^{7M} < 2^32
+                        lo[q] = (uint32_t)(unsigned long long)v[q] + (uint32_t)AOFF;
+                        hi[q] = 0;
+                    }
+                    const unsigned long long vp = ((unsigned long long)hi[q] << 32) | lo[q];
                     if (MODE == MODE_DEBUG && dbg) {
                         const int k = ch * 8 + q;
                         if (p.dbg_v) p.dbg_v[dj * 48 + k] = v[q];
@@ -258,15 +272,17 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
             if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
             ptx::fence_proxy_async_smem();
             asm volatile("bar.sync %0, 128;" ::"r"(1 + mt) : "memory");   // the 4 warps of this M-tile
-            if (row == 0) {
+            if ((wu & 3) == 0) {     // first warp of the M-tile; one elected lane issues
+              const int mtu = wu >> 2;
+              if (ptx::elect_one()) {
                 ptx::tc_fence_after();
                 const uint32_t b0 = ptx::smem_u32(&S.B[0]);
                 const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
-                const uint32_t a0 = ptx::smem_u32(&S.A[mt][0][0]);
+                const uint32_t a0 = ptx::smem_u32(&S.A[mtu][0][0]);
 #pragma unroll
                 for (int pa = 0; pa < NA; ++pa) {
                     const uint32_t ab = a0 + pa * A1_BYTES;
-                    const uint32_t d = S.tmem + mt * 256 + pa * 64;
+                    const uint32_t d = S.tmem + mtu * 256 + pa * 64;
 #pragma unroll
                     for (int ks = 0; ks < 3; ++ks)
                         ptx::mma_i8(d, ptx::smem_desc(ab + ks * 256, 128, A1_PITCH),
@@ -276,7 +292,9 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
                     ptx::mma_i8(d, ptx::smem_desc(ab + 5 * 128, 128, A1_PITCH), ptx::smem_desc(bi1, 128, BI_PITCH),
                                 IDESC, 1u);
                 }
-                ptx::mma_commit(&S.mbar[mt]);
+                ptx::mma_commit(&S.mbar[mtu]);
+              }
+              __syncwarp();
             }
         }
 
@@ -359,7 +377,8 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
         __syncthreads();   // MMAs of layer L done; all reads of fe (layer L-1) done
         if (layer_ok) {
             ptx::tc_fence_after();
-            const double alpha = -__dmul_rn(c_mat[mcur].c1, __dmul_rn(s, ISCALE));   // −RN(c1·s·2^{-7M})
+            // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
+            const double alpha = deg ? 0.0 : -__dmul_rn(c_mat[mcur].c1, __dmul_rn(s, ISCALE));
             const uint32_t tb = S.tmem + ((uint32_t)((warp & 3) * 32) << 16) + mt * 256;
 #pragma unroll
             for (int cc = 0; cc < 3; ++cc) {           // 8 outputs per round (16 columns per array)
@@ -377,8 +396,8 @@ __global__ void __launch_bounds__(I8<EY>::NT, I8<EY>::MINB) step_i8(const StepPa
                     const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
                     const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
                     // D holds −C_j, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^44
-                    const double dlo = ptx::limb_magic(c0, c1_, c2_, c3) - (0x1.8p52 + 0x1p31);
-                    const double dhi = NA > 2 ? ptx::limb_magic(c4, c5, c6, c7) - (0x1.8p52 + 0x1p31) : 0.0;
+                    const double dlo = limb_exact(c0, c1_, c2_, c3);
+                    const double dhi = NA > 2 ? limb_exact(c4, c5, c6, c7) : 0.0;
                     const double Y = NA > 2 ? __fma_rn(dhi, 0x1p32, dlo) : dlo;    // RN(−y)
                     const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
                     if (MODE == MODE_DEBUG && dbg) {
