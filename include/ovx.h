@@ -127,16 +127,17 @@ ovx_status ovx_check_finite(ovx_ctx *ctx);
  * Rank r owns element layers [ez0, ez1) of the global grid and node planes ez0..ez1 (both
  * interface planes are stored on both neighbours).  Its context is set up with the local grid
  * (nz = ez1 - ez0).  The rank ABOVE owns (updates) each interface plane, so the result is
- * bit-identical to one GPU: the rank below sends its partial force A of the plane (the sum of
- * its layer's 4 corner contributions), the owner continues ((((A+b1)+b2)+b3)+b4) with its own
- * 4 contributions in global element order, updates the plane and sends it back down.
+ * bit-identical to one GPU: the node force is f_n = T_n + B_n (reading U2: T_n, B_n =
+ * pairwise sums of the 4 corner contributions of the element layer below / above the plane);
+ * the rank below sends T (a_send), the owner adds its own B, updates the plane and sends it back
+ * down.
  * flags: bit 0 = local plane 0 is an interface owned here (needs mat_below, the nx*ny material
  * ids of the element layer below, for its nodal mass); bit 1 = the top local plane is owned
  * by the rank above.  Call after ovx_set_element_materials, before stepping. */
 ovx_status ovx_set_slab(ovx_ctx *ctx, int flags, const uint8_t *mat_below);
 /* Device buffers of 3*(nx+1)*(ny+1) doubles each, owned by the caller (e.g. torch tensors used
- * by the NCCL transport): a_send (partial A of the top plane, written by ovx_step_begin),
- * a_recv (partial A from below, read by ovx_step_iface), u_send (updated plane 0, written by
+ * by the NCCL transport): a_send (T of the top plane, written by ovx_step_begin),
+ * a_recv (T from below, read by ovx_step_iface), u_send (updated plane 0, written by
  * ovx_step_iface), u_recv (updated top plane from above, read by ovx_step_end). */
 ovx_status ovx_set_iface_buffers(ovx_ctx *ctx, double *a_send, double *a_recv, double *u_send, double *u_recv);
 /* One slab time step in three stream-ordered parts; the caller exchanges a_send -> a_recv

@@ -191,27 +191,62 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
     return degenerate;
 }
 
-/* f = Σ_e scatter(K_e u_e), element order, f zeroed first.
+/* f = Σ_e scatter(K_e u_e).  The paper adds element results directly into the global vector
+ * (atomic adds: order unspecified); reading U2 fixes one order, a
+ * pairwise tree per node n = (ix, iy, iz):
+ *   f_n = T_n + B_n,  T_n = face(iz-1, top corners),  B_n = face(iz, bottom corners),
+ *   face(ez, z) = P(iy) + P(iy-1),
+ *   P(iy)   = f(ix, iy,   ez)[(-x,-y,z)] + f(ix-1, iy,   ez)[(+x,-y,z)],
+ *   P(iy-1) = f(ix, iy-1, ez)[(-x,+y,z)] + f(ix-1, iy-1, ez)[(+x,+y,z)],
+ * where a missing element (outside the grid) contributes 0.0.
  * path 0: FP64 (Kk, Kg);  path 1: integer path (K8, M, digits). */
+static double face_sum(const double *fe_all, int64_t nx, int64_t ny, int64_t nz, int64_t ix, int64_t iy,
+                       int64_t ez, int top, int c) {
+    /* corner (local node) of element (ix - dx, iy - dy) that is node (ix, iy): Q1 order */
+    static const int CORNER[2][2] = {{0, 1}, {3, 2}};   /* [dy][dx] */
+    double v[2][2];
+    for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+            int64_t ex = ix - dx, ey = iy - dy;
+            v[dy][dx] = 0.0;
+            if (ex >= 0 && ex < nx && ey >= 0 && ey < ny && ez >= 0 && ez < nz) {
+                int64_t e = ex + nx * (ey + ny * ez);
+                v[dy][dx] = fe_all[24 * e + 3 * (CORNER[dy][dx] + 4 * top) + c];
+            }
+        }
+    double p0 = v[0][0] + v[0][1];   /* P(iy)   */
+    double p1 = v[1][0] + v[1][1];   /* P(iy-1) */
+    return p0 + p1;
+}
+
 void oracle_apply_K(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat,
                     const double *kappa, const double *G, int path,
                     const int32_t *Kk, const int32_t *Kg, const int8_t *K8, int M, int digits,
                     const double *u, double *f) {
-    int64_t nn = (nx + 1) * (ny + 1) * (nz + 1), ne = nx * ny * nz;
-    memset(f, 0, sizeof(double) * 3 * (size_t)nn);
+    int64_t ne = nx * ny * nz;
+    double *fe_all = (double *)malloc(sizeof(double) * 24 * (size_t)(ne > 0 ? ne : 1));
     int64_t nodes[8];
-    double ue[24], fe[24];
+    double ue[24];
     for (int64_t e = 0; e < ne; ++e) {
         oracle_element_nodes(nx, ny, e, nodes);
         for (int a = 0; a < 8; ++a)
             for (int c = 0; c < 3; ++c) ue[3 * a + c] = u[3 * nodes[a] + c];
         int m = mat[e];
-        if (path == 0) oracle_element_fp64(ue, kappa[m], G[m], ds, Kk, Kg, fe);
+        if (path == 0) oracle_element_fp64(ue, kappa[m], G[m], ds, Kk, Kg, fe_all + 24 * e);
         else oracle_element_int8(ue, kappa[m], G[m], ds, K8, M, digits,
-                                 NULL, NULL, NULL, NULL, NULL, NULL, fe);
-        for (int a = 0; a < 8; ++a)
-            for (int c = 0; c < 3; ++c) f[3 * nodes[a] + c] += fe[3 * a + c];
+                                 NULL, NULL, NULL, NULL, NULL, NULL, fe_all + 24 * e);
     }
+    for (int64_t iz = 0; iz <= nz; ++iz)
+        for (int64_t iy = 0; iy <= ny; ++iy)
+            for (int64_t ix = 0; ix <= nx; ++ix) {
+                int64_t n = oracle_node_id(nx, ny, ix, iy, iz);
+                for (int c = 0; c < 3; ++c) {
+                    double T = face_sum(fe_all, nx, ny, nz, ix, iy, iz - 1, 1, c);
+                    double B = face_sum(fe_all, nx, ny, nz, ix, iy, iz, 0, c);
+                    f[3 * n + c] = T + B;
+                }
+            }
+    free(fe_all);
 }
 
 /* Central-difference time stepping (Eq. 3, update L263-L266 with the

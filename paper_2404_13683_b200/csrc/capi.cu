@@ -116,6 +116,7 @@ StepParams base_params(ovx_ctx *ctx) {
     p.mat = ctx->d_mat;
     p.dmask = ctx->d_mask;
     p.stages = ctx->stages;
+    p.nmat = ctx->nmat;
     return p;
 }
 
@@ -472,7 +473,7 @@ ovx_status ovx_set_slab(ovx_ctx *ctx, int flags, const uint8_t *mat_below) {
             cudaGetLastError();
             return fail(ctx, OVX_ENOMEM, "halo allocation failed");
         }
-        if (!ctx->d_bot_b && cudaMalloc(&ctx->d_bot_b, 8 * 12 * ctx->nn2()) != cudaSuccess) {
+        if (!ctx->d_bot_b && cudaMalloc(&ctx->d_bot_b, 8 * 3 * ctx->nn2()) != cudaSuccess) {
             cudaGetLastError();
             return fail(ctx, OVX_ENOMEM, "interface allocation failed");
         }

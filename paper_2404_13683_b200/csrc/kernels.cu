@@ -5,7 +5,7 @@
 //   Per element layer L it computes the 128 = (TX+1)(TY+1) elements touching its owned
 //   nodes (one halo element ring recomputed by the neighbour tile, so no cross-CTA
 //   reduction is needed), accumulates their forces into two shared-memory node planes
-//   in global element order (bit-identical to the oracle's scatter order), and applies
+//   in the node-local pairwise order of reading U2 (bit-identical to the oracle), and applies
 //   the central-difference update (Eq. 3, L263-L266 with the sign of Eq. 3)
 //   to each completed plane.
 //
@@ -89,7 +89,8 @@ __device__ __forceinline__ void iwht8(double (&v)[8]) {
             }
     }
 }
-__device__ __forceinline__ void element_force_wht(const double (&ue)[24], const MatConst &m, double (&fe)[24]) {
+template <class MC>   // MatConst or a shared-memory copy with the same L0 .. C2 fields
+__device__ __forceinline__ void element_force_wht(const double (&ue)[24], const MC &m, double (&fe)[24]) {
     constexpr int BORD[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // local node -> bit index x | y<<1 | z<<2
     double h[3][8];
 #pragma unroll
@@ -156,36 +157,27 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 
 #include "step_v1.cuh"
 #include "step_f64.cuh"
-#include "step_i8.cuh"
 
-// INT8 tile height (elements per layer = 32 × EY): 8 (one CTA/SM, two MMA tiles per layer) or
-// 4 (two CTAs/SM, one MMA tile each).  OVX_I8_EY selects it; default 8.
-int i8_ey() {
-    static int ey = [] {
-        const char *e = getenv("OVX_I8_EY");
-        return (e && atoi(e) == 4) ? 4 : 8;
-    }();
-    return ey;
-}
+#include "step_i8w.cuh"
 
-template <int MODE, int EY, int M>
-cudaError_t launch_i8(const StepParams &p, int64_t ctas, cudaStream_t st) {
+template <int MODE, int M>
+cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
-    const int smem = (int)sizeof(SmemI8<EY>);
+    const int smem = (int)sizeof(SmemI8W);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_i8<MODE, EY, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_i8<MODE, EY, M><<<(unsigned)ctas, I8<EY>::NT, smem, st>>>(p);
+    step_i8w<MODE, M><<<(unsigned)ctas, I8W::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-template <int EY, int M>
+template <int M>
 cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
-    if (mode == MODE_STEP) return launch_i8<MODE_STEP, EY, M>(p, ctas, st);
-    if (mode == MODE_APPLY) return launch_i8<MODE_APPLY, EY, M>(p, ctas, st);
-    return launch_i8<MODE_DEBUG, EY, M>(p, ctas, st);
+    if (mode == MODE_STEP) return launch_i8w<MODE_STEP, M>(p, ctas, st);
+    if (mode == MODE_APPLY) return launch_i8w<MODE_APPLY, M>(p, ctas, st);
+    return launch_i8w<MODE_DEBUG, M>(p, ctas, st);
 }
 
 template <int PATH, int MODE>
@@ -285,12 +277,12 @@ cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, c
 LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
     if (path == OVX_INT8) {
         LaunchInfo li;
-        const int ey = i8_ey(), tyy = ey - 1;
+        const int tyy = 8 - 1;
         const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + tyy - 1) / tyy;
         const int64_t tz = (nz + 1 + kZChunk - 1) / kZChunk;
         li.ctas = tx * ty * tz;
-        li.threads = 32 * ey;
-        li.smem = ey == 4 ? (int)sizeof(SmemI8<4>) : (int)sizeof(SmemI8<8>);
+        li.threads = I8W::NT;
+        li.smem = (int)sizeof(SmemI8W);
         return li;
     }
     if (path == OVX_INT8) return info_t<OVX_INT8>(nx, ny, nz);
@@ -299,7 +291,7 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
 }
 
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
-    const int ty = path == OVX_INT8 ? (p.stages == 8 ? i8_ey() : 8) - 1 : V1<OVX_FP64>::TY;
+    const int ty = path == OVX_INT8 ? 8 - 1 : V1<OVX_FP64>::TY;
     p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
     p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
     const int64_t nchunk = (p.nz + 1 + kZChunk - 1) / kZChunk;        // chunks of <= 64 planes,
@@ -307,9 +299,9 @@ cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
     const int64_t tz = (p.nz + 1 + p.zchunk - 1) / p.zchunk;
     const int64_t ctas = (int64_t)p.tiles_x * p.tiles_y * tz;
     if (path == OVX_INT8) {
-        if (p.stages == 4) return launch_i8_mode<8, 4>(mode, p, ctas, st);
-        if (p.stages == 6) return launch_i8_mode<8, 6>(mode, p, ctas, st);
-        return i8_ey() == 4 ? launch_i8_mode<4, 8>(mode, p, ctas, st) : launch_i8_mode<8, 8>(mode, p, ctas, st);
+        if (p.stages == 4) return launch_i8_mode<4>(mode, p, ctas, st);
+        if (p.stages == 6) return launch_i8_mode<6>(mode, p, ctas, st);
+        return launch_i8_mode<8>(mode, p, ctas, st);
     }
     if (path == OVX_FP64) return launch_mode<OVX_FP64>(mode, p, ctas, st);
     return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);
@@ -321,16 +313,15 @@ cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat
     return cudaGetLastError();
 }
 
-// Interface plane (local plane 0) of a z-slab: continue the received partial A of the layer
-// below with this rank's 4 layer-0 contributions in global element order, then update.
+// Interface plane (local plane 0) of a z-slab: f_n = T_n (the top-face sum received from the
+// rank below) + B_n (this rank's layer-0 bottom-face sum), reading U2; then update.
 __global__ void iface_update_kernel(const StepParams p, const double *__restrict__ a_recv, double *__restrict__ u_send) {
     const int64_t nn2 = (p.nx + 1) * (p.ny + 1);
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nn2; j += (int64_t)gridDim.x * blockDim.x) {
         const double wn = p.w[j];
         const uint8_t dm = p.dmask ? p.dmask[j] : (uint8_t)0;
         for (int c = 0; c < 3; ++c) {
-            double f = a_recv[3 * j + c];
-            for (int k = 0; k < 4; ++k) f = __dadd_rn(f, p.iface_bot_b[12 * j + 3 * k + c]);
+            const double f = __dadd_rn(a_recv[3 * j + c], p.iface_bot_b[3 * j + c]);
             const int64_t dof = 3 * j + c;
             double F = 0.0;
             for (int k = 0; k < p.nsrc; ++k)

@@ -43,9 +43,10 @@ struct StepParams {
     // owned by this rank (its lower-layer partial arrives from below), bit 1 = the top local
     // plane is an interface owned by the rank above (send its partial, do not update it)
     int stages;            // INT8 path: M (4, 6 or 8)
+    int nmat;              // materials in c_mat[0, nmat) (ids < 255; 255 = zero material)
     int slab_flags;
     double *iface_top_A;   // [NX1*NY1][3]   partial force of the top plane (bit 1)
-    double *iface_bot_b;   // [NX1*NY1][4][3] the 4 layer-0 contributions to plane 0 (bit 0)
+    double *iface_bot_b;   // [NX1*NY1][3] the layer-0 bottom-face sum B of plane 0 (bit 0)
     // tiling
     int tiles_x, tiles_y, zchunk;
     // MODE_DEBUG outputs for elements [dbg_e0, dbg_e0 + dbg_ne)

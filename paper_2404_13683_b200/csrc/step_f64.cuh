@@ -9,7 +9,8 @@
 //   * thread (lx, ly) owns node (lx, ly) of the tile (lx, ly >= 1) and keeps its plane-L and
 //     plane-(L+1) force accumulators in registers across the z-march; the completed plane is
 //     updated in place (Eq. 3 / L263-L266 with the sign of Eq. 3).
-// The summation order differs from the oracle's element order (parity: tolerance).
+// Node sums follow the oracle's order (reading U2); the factored element force differs from the
+// dense one in rounding (parity: tolerance).
 
 struct F2 {
     static constexpr int EY = 8;
@@ -20,9 +21,16 @@ struct F2 {
     static constexpr int PF = (PLANE + NT - 1) / NT;   // 4
 };
 
+// the material constants of the factored force, staged in shared memory once per CTA (a
+// per-lane indexed constant-bank load serialises and misses the constant cache)
+struct MatW {
+    double L0, M0, M0x2, L1, M1, M1x3, C2, pad;
+};
+
 struct SmemF2 {
     double up[4][F2::PLANE];          // ring: planes L, L+1 in use, L+2 parked, L+3 in flight
     double ysum[2][F2::EY][EX][6];    // +y-corner x-sums of each element row (double-buffered)
+    MatW mw[kMaxMat];                 // [0, nmat) and the zero material kZeroMat
 };
 
 template <int MODE>
@@ -39,8 +47,9 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     const int ty = bid % p.tiles_y;
     const int tz = bid / p.tiles_y;
     const int64_t X0 = (int64_t)tx * TX, Y0 = (int64_t)ty * TY;
-    const int64_t Z0 = (int64_t)tz * p.zchunk;
-    const int64_t Z1 = min(Z0 + (int64_t)p.zchunk, p.nz + 1);
+    const int Z0 = tz * p.zchunk;
+    const int Z1 = (int)min((int64_t)Z0 + p.zchunk, p.nz + 1);
+    const int nz = (int)p.nz;
     const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1, PSTRIDE = NX1 * NY1;
 
     const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
@@ -48,7 +57,7 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     const uint8_t *matcol = p.mat + (ein ? ex + p.nx * ey : 0);
     const int64_t mstride = p.nx * p.ny;
 
-    int64_t pfoff[PF];
+    int pfoff[PF];
     bool pfok[PF];
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
@@ -82,17 +91,24 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
             has_rec |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
         }
 
-    const int64_t Lfirst = max(Z0 - 1, (int64_t)0);
-    // synchronous first three planes (the loop prefetches two planes ahead)
+    for (int i = t; i < p.nmat + 1; i += NT) {
+        const int id = i < p.nmat ? i : kZeroMat;
+        const MatConst &m = c_mat[id];
+        S.mw[id] = MatW{m.L0, m.M0, m.M0x2, m.L1, m.M1, m.M1x3, m.C2, 0.0};
+    }
+    const int Lfirst = max(Z0 - 1, 0);
+    // synchronous first three planes (the loop prefetches two planes ahead); the fourth ring
+    // slot is zeroed: the prefetch never writes the out-of-domain halo entries
+    for (int idx = t; idx < PLANE; idx += NT) S.up[(Lfirst + 3) & 3][idx] = 0.0;
     for (int j = 0; j < 3; ++j) {
-        const int64_t iz = Lfirst + j;
+        const int iz = Lfirst + j;
         double *dst = S.up[iz & 3];
         for (int idx = t; idx < PLANE; idx += NT) {
             const int py = idx / (PX * 3);
             const int rem = idx - py * (PX * 3);
             const int px = rem / 3, c = rem - px * 3;
             const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
-            dst[idx] = (iz <= p.nz && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1)
+            dst[idx] = (iz <= nz && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1)
                            ? __ldg(p.u + 3 * (ix + NX1 * (iy + NY1 * iz)) + c) : 0.0;
         }
     }
@@ -101,34 +117,35 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     // plane prefetched in the previous iteration, parked (before this layer's barrier) into the
     // ring slot of plane L-1, which no thread reads any more
     double pend[PF];
-    int64_t pend_z = -1;
+    int pend_z = -1;
     auto park_prev = [&]() {
         if (pend_z >= 0) {
             double *dst = S.up[pend_z & 3];
 #pragma unroll
             for (int j = 0; j < PF; ++j) {
                 const int idx = t + j * NT;
-                if (idx < PLANE) dst[idx] = pend[j];
+                if (pfok[j]) dst[idx] = pend[j];
             }
         }
     };
     double facc[3] = {0.0, 0.0, 0.0};   // plane L (receives layer L-1 top + layer L bottom)
     // material ids of the current and next layer; the one after is fetched two layers ahead
-    int mcur = (ein && Lfirst < p.nz) ? (int)__ldg(matcol + mstride * Lfirst) : kZeroMat;
-    int mnxt = (ein && Lfirst + 1 < p.nz) ? (int)__ldg(matcol + mstride * (Lfirst + 1)) : kZeroMat;
+    int mcur = (ein && Lfirst < nz) ? (int)__ldg(matcol + mstride * Lfirst) : kZeroMat;
+    int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matcol + mstride * (Lfirst + 1)) : kZeroMat;
     double nupv[3] = {0.0, 0.0, 0.0}, nwn = 0.0;
     uint8_t ndm = 0;
-    for (int64_t L = Z0 - 1; L < Z1; ++L) {
-        const bool layer_ok = (L >= 0 && L < p.nz);
-        const bool plane_done = (L >= Z0 && L <= p.nz);
-        const int mfar = (ein && L + 2 > Lfirst + 1 && L + 2 < p.nz) ? (int)__ldg(matcol + mstride * (L + 2)) : kZeroMat;
+    for (int L = Z0 - 1; L < Z1; ++L) {
+        const bool layer_ok = (L >= 0 && L < nz);
+        const bool plane_done = (L >= Z0 && L <= nz);
+        const int mfar = (ein && L >= Lfirst && L + 2 < nz) ? (int)__ldg(matcol + mstride * (L + 2)) : kZeroMat;
         // ---- prefetch plane L+3 (parked next iteration) and the update operands of plane L ----
-        const int64_t pz = L + 3;
-        const bool pf = (pz > Lfirst + 2) && (L + 2 < Z1) && (L + 2 < p.nz);
+        const int pz = L + 3;
+        const bool pf = (pz > Lfirst + 2) && (L + 2 < Z1) && (L + 2 < nz);
         double pfv[PF];
         const double *uplane = p.u + 3 * PSTRIDE * pz;
 #pragma unroll
-        for (int j = 0; j < PF; ++j) pfv[j] = (pf && pfok[j]) ? __ldg(uplane + pfoff[j]) : 0.0;
+        for (int j = 0; j < PF; ++j)
+            if (pf && pfok[j]) pfv[j] = __ldg(uplane + pfoff[j]);
         const bool upd = plane_done && own;
         const int64_t un_id = ucol + PSTRIDE * L;
         // update operands of plane L were loaded one layer ahead; fetch those of plane L+1
@@ -136,8 +153,8 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         const double wn = nwn;
         const uint8_t dm = ndm;
         if (MODE == MODE_STEP) {
-            const int64_t L1 = L + 1;
-            if (own && L1 >= Z0 && L1 < Z1 && L1 <= p.nz) {
+            const int L1 = L + 1;
+            if (own && L1 >= Z0 && L1 < Z1 && L1 <= nz) {
                 const int64_t nid = un_id + PSTRIDE;
                 nupv[0] = p.uo[3 * nid];
                 nupv[1] = p.uo[3 * nid + 1];
@@ -152,7 +169,7 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         if (layer_ok) {
             double ue[24], fe[24];
             gather<F2::PY>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
-            element_force_wht(ue, c_mat[mcur], fe);     // zero material outside the domain
+            element_force_wht(ue, S.mw[mcur], fe);     // zero material outside the domain
             // x-sums at this element's -x node column: own -x corners + lane lx-1's +x corners
             // local nodes: (-x,-y)=0,4  (+x,-y)=1,5  (+x,+y)=2,6  (-x,+y)=3,7   (bottom, top)
             double xs[12];   // [dy][dz][c]

@@ -1,0 +1,458 @@
+// step_i8w.cuh — fused time step of the INT8 tensor-core path (OVX_INT8); included by kernels.cu.
+//
+// CTA = 32 × 8 elements per layer (one halo ring recomputed by the neighbour tiles), marching in
+// z over a chunk of node planes; 512 threads, two per element.  The TMEM budget (2 M-tiles × 256
+// columns = all 512) and ~200 KB of shared memory allow one CTA per SM, so each element's work is
+// split across two threads to double the resident warps:
+//   * warp w: M-tile mt = w/8, half hf = (w/4)&1, TMEM lane quadrant q = w&3; element row
+//     32q + lane of M-tile mt = tile element (lx = lane, ly = 4mt + q);
+//   * conversion (Eqs. 10-16): s_e = max|ū_e| from per-node maxima |u| kept with each
+//     smem u plane; half 0 writes A chunks {0,1,3} (ū values 0-15 and the G copy of 0-7), half 1
+//     chunks {2,4,5}; one elected lane per M-tile issues the tcgen05.mma.kind::i8 chain
+//     (4 arrays × [3 K-steps against −K_e^INT8 ⊗ I_2 + 2 K-steps of the G bytes against
+//     −128·I ⊗ I_2] = Eq. 17 with the Eq. 9 diagonal folded in, variant D);
+//   * epilogue: half hf reads the accumulators of outputs 12hf..12hf+11 = the 4 corner nodes of
+//     its face (hf 0 bottom, hf 1 top), exact two-limb recombination, f = RN(c1 s 2^-7M)·RN(y);
+//   * node sums in the order of reading U2 without staging element forces: the x-pair
+//     P = f(ix,iy)[(-x,-y)] + f(ix-1,iy)[(+x,-y)] by one warp shuffle, the y-pair P(iy) + P(iy-1)
+//     through a small smem exchange, f_n = T_n (top face of layer L-1, from half 1) + B_n (bottom
+//     face of layer L, half 0), then the central-difference update (Eq. 3 / L263-L266
+//     with the sign of Eq. 3).  This post-phase of layer L-1 runs while the MMAs of layer L are
+//     in flight.  Results are bit-identical to the oracle.
+
+struct I8W {
+    static constexpr int EY = 8;
+    static constexpr int NE = EX * EY;                 // elements per layer
+    static constexpr int NT = 2 * NE;                  // threads
+    static constexpr int MT = NE / 128;                // M=128 MMA tiles per layer
+    static constexpr int TY = EY - 1;
+    static constexpr int PY = EY + 1;
+    static constexpr int NOWN = TX * TY;
+    static constexpr int NODES = PX * PY;              // nodes of one u plane held in smem
+    static constexpr int PLANE = NODES * 3;
+    static constexpr int TMEM_COLS = MT * 256;
+};
+
+struct SmemI8W {
+    uint8_t A[I8W::MT][4][A1_BYTES];      // [M-tile][half-word array], K-major canonical layout
+    alignas(128) uint8_t B[6 * B1_PITCH];
+    alignas(128) uint8_t BI[2][6 * BI_PITCH];
+    double up[4][I8W::PLANE];                       // ring: L-1 (update), L, L+1 (gather), L+2
+    unsigned long long nmax[4][I8W::NODES];         // max_c |u_c| of each node (bit patterns)
+    double ysum[2][2][I8W::EY][EX][3];              // [layer parity][face] x-pair P of the +y corners
+    double tf[2][I8W::NE][3];                       // [layer parity][tile node] top-face sums T
+    uint64_t mbar[I8W::MT];
+    uint32_t tmem;
+};
+
+// ū values 8hf .. 8hf+15 of tile element (lx, ly) (local node order of reading Q1)
+template <int HF>
+__device__ __forceinline__ void gather16(double (&ue)[16], const double *lo, const double *hi, int lx, int ly) {
+    const int cx[4] = {0, 1, 1, 0}, cy[4] = {0, 0, 1, 1};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int k = 8 * HF + j, a = k / 3, c = k - 3 * a;
+        const double *pl = a < 4 ? lo : hi;
+        ue[j] = pl[((ly + cy[a & 3]) * PX + (lx + cx[a & 3])) * 3 + c];
+    }
+}
+
+template <int MODE, int M, int HF>
+__device__ __forceinline__ void i8w_convert(const StepParams &p, const double (&ue)[16], double cG, double s,
+                                            bool deg, bool vzero, bool fast, uint8_t *Ab, uint32_t rowoff,
+                                            bool dbg, int64_t dj) {
+    constexpr int NB = (7 * M + 1 + 7) / 8;
+    constexpr int NA = (NB + 1) / 2;
+    constexpr double SCALE = (double)(1ull << (7 * M));
+    constexpr unsigned long long AOFF = 1ull << (7 * M);
+    const double r = 1.0 / s;                                  // RN(1/s_e), reading Q7
+    const double R = vzero ? 0.0 : __dmul_rn(r, SCALE);        // exact power-of-two scaling
+    const bool wfast = __all_sync(0xffffffffu, fast);
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+        const int ch = HF == 0 ? (cc == 2 ? 3 : cc) : (cc == 0 ? 2 : cc + 3);
+        const bool gpart = ch >= 3;
+        const int j0 = 8 * (gpart ? ch - 3 : ch) - 8 * HF;     // index into ue of value 0 of the chunk
+        long long v[8];
+        if (wfast) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double ub = gpart ? __dmul_rn(cG, ue[j0 + q]) : ue[j0 + q];
+                v[q] = __double2ll_rz(__dmul_rn(ub, R));
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double ub = gpart ? __dmul_rn(cG, ue[j0 + q]) : ue[j0 + q];
+                v[q] = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), SCALE));
+            }
+        }
+        uint32_t lo[8], hi[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if constexpr (7 * M >= 32) {   // v + 2^{7M}: the offset only touches the high word
+                lo[q] = (uint32_t)(unsigned long long)v[q];
+                hi[q] = (uint32_t)((unsigned long long)v[q] >> 32) + (uint32_t)(AOFF >> 32);
+            } else {                        // v + 2^{7M} < 2^32
+                lo[q] = (uint32_t)(unsigned long long)v[q] + (uint32_t)AOFF;
+                hi[q] = 0;
+            }
+            if (MODE == MODE_DEBUG && dbg) {
+                const unsigned long long vp = ((unsigned long long)hi[q] << 32) | lo[q];
+                const int k = ch * 8 + q;
+                if (p.dbg_v) p.dbg_v[dj * 48 + k] = v[q];
+                if (p.dbg_d)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = j < NB ? (uint8_t)(vp >> (8 * j)) : 0;
+            }
+        }
+        const uint32_t off = rowoff + (uint32_t)ch * 128;
+#pragma unroll
+        for (int pa = 0; pa < NA; ++pa) {
+            const uint32_t *src = pa < 2 ? lo : hi;
+            const uint32_t sel = (pa & 1) ? 0x7632u : 0x5410u;
+            uint4 wv;
+            wv.x = __byte_perm(src[0], src[1], sel);
+            wv.y = __byte_perm(src[2], src[3], sel);
+            wv.z = __byte_perm(src[4], src[5], sel);
+            wv.w = __byte_perm(src[6], src[7], sel);
+            *reinterpret_cast<uint4 *>(Ab + pa * A1_BYTES + off) = wv;
+        }
+    }
+}
+
+template <int MODE, int M>
+__global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
+    using C = I8W;
+    constexpr int NB = (7 * M + 1 + 7) / 8;
+    constexpr int NA = (NB + 1) / 2;
+    constexpr double ISCALE = 1.0 / (double)(1ull << (7 * M));    // exact power of two
+    constexpr int NT = C::NT, NODES = C::NODES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    SmemI8W &S = *reinterpret_cast<SmemI8W *>(smem_raw);
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int wu = __shfl_sync(0xffffffffu, warp, 0);   // the warp index as a uniform value
+    const int mt = warp >> 3, hf = (warp >> 2) & 1, qd = warp & 3;
+    const int row = 32 * qd + lane;                      // MMA row = TMEM lane
+
+    int bid = blockIdx.x;
+    const int tx = bid % p.tiles_x;
+    bid /= p.tiles_x;
+    const int ty = bid % p.tiles_y;
+    const int tz = bid / p.tiles_y;
+    const int64_t X0 = (int64_t)tx * TX, Y0 = (int64_t)ty * C::TY;
+    const int Z0 = tz * p.zchunk;
+    const int Z1 = (int)min((int64_t)Z0 + p.zchunk, p.nz + 1);
+    const int nz = (int)p.nz;
+    const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
+    const int64_t PSTRIDE = NX1 * NY1;
+
+    // element (lx, ly) of the tile; its (-x,-y) corner is tile node (lx, ly)
+    const int lx = lane, ly = 4 * mt + qd;
+    const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
+    const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
+    const uint8_t *matp = p.mat + (ein ? ex + p.nx * ey : 0);
+    const int64_t mstride = p.nx * p.ny;
+    // node (lx, ly): owned by this tile (lx, ly >= 1) if inside the grid; half 0 updates it
+    const bool tnode = lx >= 1 && ly >= 1;
+    const bool own = tnode && ex < NX1 && ey < NY1;
+    const int64_t ucol = own ? ex + NX1 * ey : 0;
+    const bool upd_role = own && hf == 0;
+
+    // plane loader role: node t of the smem plane
+    const int lpx = t % PX, lpy = t / PX;
+    const bool ldn = t < NODES && X0 - 1 + lpx >= 0 && X0 - 1 + lpx < NX1 && Y0 - 1 + lpy >= 0 && Y0 - 1 + lpy < NY1;
+    const int64_t ldoff = ldn ? 3 * ((X0 - 1 + lpx) + NX1 * (Y0 - 1 + lpy)) : 0;
+
+    bool has_src = false, has_rec = false;
+    if (MODE == MODE_STEP && hf == 0) {
+        for (int k = 0; k < p.nsrc; ++k) {
+            const int64_t n = p.src_dof[k] / 3;
+            const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+            has_src |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + C::TY);
+        }
+        if (p.it < p.rec_nt)
+            for (int k = 0; k < p.nrec; ++k) {
+                const int64_t n = p.rec_node[k];
+                const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+                has_rec |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + C::TY);
+            }
+    }
+
+    // ---- one-time setup: B operands, zero K-padding chunks, TMEM, mbarriers ----
+    for (int idx = t; idx < 48 * 96; idx += NT) {
+        const int n = idx / 96, kb = idx - n * 96;
+        const int off = (n >> 3) * B1_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
+        S.B[off] = ((kb & 1) == (n & 1)) ? (uint8_t)(-(int)c_K8[(n >> 1) * 48 + (kb >> 1)]) : (uint8_t)0;
+    }
+    for (int idx = t; idx < 2 * 48 * 32; idx += NT) {
+        const int s2 = idx / (48 * 32), r2 = idx - s2 * 48 * 32;
+        const int n = r2 / 32, kb = r2 - n * 32;
+        const int off = (n >> 3) * BI_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
+        const int k = 16 * s2 + (kb >> 1);
+        S.BI[s2][off] = ((kb & 1) == (n & 1) && k == (n >> 1)) ? (uint8_t)0x80 : (uint8_t)0;
+    }
+    for (int idx = t; idx < C::MT * 4 * 128; idx += NT) {
+        const int a = idx >> 7, r = idx & 127;
+        *reinterpret_cast<uint4 *>(&S.A[a >> 2][a & 3][(r >> 3) * A1_PITCH + 6 * 128 + (r & 7) * 16]) =
+            make_uint4(0, 0, 0, 0);
+    }
+    if (warp == 0) ptx::tmem_alloc<C::TMEM_COLS>(&S.tmem);
+    if (t == 0)
+        for (int mm = 0; mm < C::MT; ++mm) ptx::mbar_init(&S.mbar[mm], 1);
+    for (int i = t; i < 2 * C::NE * 3; i += NT) (&S.tf[0][0][0])[i] = 0.0;
+    const int Lfirst = max(Z0 - 1, 0);
+    for (int j = 0; j < 2; ++j) {
+        const int iz = Lfirst + j;
+        if (t < NODES) {
+            double v3[3] = {0.0, 0.0, 0.0};
+            if (ldn && iz <= nz)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) v3[c] = __ldg(p.u + 3 * PSTRIDE * iz + ldoff + c);
+            unsigned long long m = 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                S.up[iz & 3][3 * t + c] = v3[c];
+                const unsigned long long b = abs_bits(v3[c]);
+                m = b > m ? b : m;
+            }
+            S.nmax[iz & 3][t] = m;
+        }
+    }
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+
+    uint32_t phase = 0;
+    int mcur = (ein && Lfirst < nz) ? (int)__ldg(matp + mstride * Lfirst) : kZeroMat;
+    int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matp + mstride * (Lfirst + 1)) : kZeroMat;
+    double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;   // update operands of plane L-1
+    uint8_t dm = 0;
+    double plo[3] = {0.0, 0.0, 0.0};             // x-pair P(iy) of this thread's face, layer L-1
+    bool prev_layer = false;                     // was layer L-1 computed?
+
+    for (int L = Z0 - 1; L <= Z1; ++L) {
+        const bool layer_ok = (L >= 0 && L < nz && L < Z1);
+        const int Ld = L - 1;                                        // post-phase layer / plane
+        const bool plane_done = (Ld >= Z0 && Ld <= nz && Ld < Z1);   // plane Ld completes now
+        // ---- 1. prefetch: plane L+2, material of layer L+2, update operands of plane L ----
+        const int pz = L + 2;
+        const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < nz);
+        double pfv[3] = {0.0, 0.0, 0.0};
+        if (pf && ldn) {
+            const double *src = p.u + 3 * PSTRIDE * pz + ldoff;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) pfv[c] = __ldg(src + c);
+        }
+        const int mfar = (ein && L + 2 < nz && L >= Lfirst) ? (int)__ldg(matp + mstride * (L + 2)) : kZeroMat;
+        double upv_n[3] = {0.0, 0.0, 0.0}, wn_n = 0.0;
+        uint8_t dm_n = 0;
+        if (MODE == MODE_STEP && upd_role && L >= Z0 && L <= nz && L < Z1) {
+            const int64_t un_next = ucol + PSTRIDE * L;
+            upv_n[0] = p.uo[3 * un_next];
+            upv_n[1] = p.uo[3 * un_next + 1];
+            upv_n[2] = p.uo[3 * un_next + 2];
+            wn_n = __ldg(p.w + un_next);
+            dm_n = p.dmask ? __ldg(p.dmask + un_next) : (uint8_t)0;
+        }
+
+        // ---- 2. integer image of ū_e for layer L (this thread's three chunks), MMA hand-off ----
+        double s = 0.0;
+        int64_t dj = -1;
+        bool dbg = false, deg = false;
+        if (layer_ok) {
+            const int64_t eid = ex + p.nx * (ey + p.ny * (int64_t)L);
+            dj = eid - p.dbg_e0;
+            dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < C::TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
+                  dj >= 0 && dj < p.dbg_ne;
+            // s_e from the per-node maxima of the two planes
+            const unsigned long long *m0 = S.nmax[L & 3], *m1 = S.nmax[(L + 1) & 3];
+            const int n0 = ly * PX + lx;
+            unsigned long long ab = m0[n0];
+            ab = max(ab, m0[n0 + 1]);
+            ab = max(ab, m0[n0 + PX]);
+            ab = max(ab, m0[n0 + PX + 1]);
+            ab = max(ab, m1[n0]);
+            ab = max(ab, m1[n0 + 1]);
+            ab = max(ab, m1[n0 + PX]);
+            ab = max(ab, m1[n0 + PX + 1]);
+            const double amax = __longlong_as_double((long long)ab);
+            const double cG = c_mat[mcur].cG;
+            s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
+            deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
+            const bool vzero = !ein || !(s >= 0x1p-1022);
+            const bool fast = (s <= 0x1.fffffffffffffp1023) && (vzero || s >= 0x1p-960);
+            uint8_t *Ab = &S.A[mt][0][0];
+            const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
+            double ue[16];
+            if (hf == 0) {
+                gather16<0>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
+                i8w_convert<MODE, M, 0>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
+                if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
+            } else {
+                gather16<1>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
+                i8w_convert<MODE, M, 1>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
+            }
+            ptx::fence_proxy_async_smem();
+            asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
+            if ((wu & 7) == 0) {     // first warp of the M-tile; one elected lane issues
+                const int mtu = wu >> 3;
+                if (ptx::elect_one()) {
+                    ptx::tc_fence_after();
+                    const uint32_t b0 = ptx::smem_u32(&S.B[0]);
+                    const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
+                    const uint32_t a0 = ptx::smem_u32(&S.A[mtu][0][0]);
+#pragma unroll
+                    for (int pa = 0; pa < NA; ++pa) {
+                        const uint32_t abase = a0 + pa * A1_BYTES;
+                        const uint32_t d = S.tmem + mtu * 256 + pa * 64;
+#pragma unroll
+                        for (int ks = 0; ks < 3; ++ks)
+                            ptx::mma_i8(d, ptx::smem_desc(abase + ks * 256, 128, A1_PITCH),
+                                        ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC, ks > 0 ? 1u : 0u);
+                        ptx::mma_i8(d, ptx::smem_desc(abase + 3 * 128, 128, A1_PITCH),
+                                    ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
+                        ptx::mma_i8(d, ptx::smem_desc(abase + 5 * 128, 128, A1_PITCH),
+                                    ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
+                    }
+                    ptx::mma_commit(&S.mbar[mtu]);
+                }
+                __syncwarp();
+            }
+        }
+
+        // ---- 3. (overlaps the MMAs) post-phase of layer Ld = L-1: face sums, f_n = T + B, update ----
+        if (tnode) {
+            const bool bot_iface = (p.slab_flags & 1) && Ld == 0;
+            const bool top_iface = (p.slab_flags & 2) && Ld == nz;
+            double face[3] = {0.0, 0.0, 0.0};
+            if (prev_layer) {
+                const double(*ys)[EX][3] = S.ysum[Ld & 1][hf];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) face[c] = __dadd_rn(plo[c], ys[ly - 1][lx][c]);   // P(iy) + P(iy-1)
+            }
+            if (hf == 1) {        // top face of layer Ld: T of plane Ld+1
+#pragma unroll
+                for (int c = 0; c < 3; ++c) S.tf[Ld & 1][lx + EX * ly][c] = face[c];
+            } else if (own && plane_done) {
+                const int64_t un_id = ucol + PSTRIDE * Ld;
+                if (bot_iface) {  // interface plane: B waits for T from the rank below
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) p.iface_bot_b[3 * ucol + c] = face[c];
+                } else {
+                    double f[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) f[c] = __dadd_rn(S.tf[(Ld - 1) & 1][lx + EX * ly][c], face[c]);
+                    if (top_iface) {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = f[c];
+                    } else if (MODE == MODE_STEP) {
+                        const double *up = &S.up[Ld & 3][(ly * PX + lx) * 3];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const int64_t dof = 3 * un_id + c;
+                            double F = 0.0;
+                            if (has_src)
+                                for (int k = 0; k < p.nsrc; ++k)
+                                    if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
+                            const double b = __dsub_rn(__dmul_rn(2.0, up[c]), upv[c]);
+                            double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
+                            if ((dm >> c) & 1) un = 0.0;
+                            p.uo[dof] = un;
+                            if (has_rec)
+                                for (int k = 0; k < p.nrec; ++k)
+                                    if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) p.fout[3 * un_id + c] = f[c];
+                    }
+                }
+            }
+        }
+
+        // ---- 4. epilogue of layer L: the 4 corner nodes of this thread's face ----
+        if (layer_ok) {
+            ptx::mbar_wait(&S.mbar[mt], phase);
+            phase ^= 1;
+            ptx::tc_fence_after();
+            // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
+            const double alpha = deg ? 0.0 : -__dmul_rn(c_mat[mcur].c1, __dmul_rn(s, ISCALE));
+            const uint32_t tb = S.tmem + ((uint32_t)(qd * 32) << 16) + mt * 256 + 24 * hf;
+            double fc[12];                               // [corner][c] of the face
+#pragma unroll
+            for (int rr = 0; rr < 3; ++rr) {             // 4 outputs per round (8 columns per array)
+                uint32_t R0[8], R1[8], R2[8] = {}, R3[8] = {};
+                ptx::tmem_ld8(tb + 0 + rr * 8, R0);
+                ptx::tmem_ld8(tb + 64 + rr * 8, R1);
+                if (NA > 2) ptx::tmem_ld8(tb + 128 + rr * 8, R2);
+                if (NA > 3) ptx::tmem_ld8(tb + 192 + rr * 8, R3);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = 4 * rr + q;
+                    const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
+                    const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
+                    const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
+                    const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
+                    // D holds −C_j, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^46
+                    const double dlo = limb_exact(c0, c1_, c2_, c3);
+                    const double dhi = NA > 2 ? limb_exact(c4, c5, c6, c7) : 0.0;
+                    const double Y = NA > 2 ? __fma_rn(dhi, 0x1p32, dlo) : dlo;    // RN(−y)
+                    const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
+                    if (MODE == MODE_DEBUG && dbg) {
+                        const int i = 12 * hf + j;
+                        const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};
+                        __int128 y = 0;
+#pragma unroll
+                        for (int jj = 7; jj >= 0; --jj) y = y * 256 - (__int128)Cj[jj];
+                        if (p.dbg_C)
+#pragma unroll
+                            for (int jj = 0; jj < 8; ++jj) p.dbg_C[dj * 192 + jj * 24 + i] = -Cj[jj];
+                        if (p.dbg_yhi) p.dbg_yhi[dj * 24 + i] = (long long)(y >> 64);
+                        if (p.dbg_ylo) p.dbg_ylo[dj * 24 + i] = (long long)(unsigned long long)y;
+                        if (p.dbg_fe) p.dbg_fe[dj * 24 + i] = f;
+                    }
+                    fc[j] = f;
+                }
+            }
+            ptx::tc_fence_before();
+            // x-pairs: P(iy) of node (lx, ly) = own (-x,-y) corner + lane lx-1's (+x,-y) corner;
+            // the +y corners give P(iy-1) of node (lx, ly+1), exchanged through smem
+            double(*ys)[EX][3] = S.ysum[L & 1][hf];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double pm = __shfl_up_sync(0xffffffffu, fc[3 * 1 + c], 1);   // (+x,-y) of lx-1
+                const double pp = __shfl_up_sync(0xffffffffu, fc[3 * 2 + c], 1);   // (+x,+y) of lx-1
+                plo[c] = __dadd_rn(fc[3 * 0 + c], pm);
+                ys[ly][lx][c] = __dadd_rn(fc[3 * 3 + c], pp);
+            }
+        }
+        // ---- park plane L+2 (slot of plane L-2, no longer read) with its node maxima ----
+        if (pf && t < NODES) {
+            unsigned long long m = 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                S.up[pz & 3][3 * t + c] = pfv[c];
+                const unsigned long long b = abs_bits(pfv[c]);
+                m = b > m ? b : m;
+            }
+            S.nmax[pz & 3][t] = m;
+        }
+        prev_layer = layer_ok;
+        if (L >= Lfirst) {
+            mcur = mnxt;
+            mnxt = mfar;
+        }
+        upv[0] = upv_n[0];
+        upv[1] = upv_n[1];
+        upv[2] = upv_n[2];
+        wn = wn_n;
+        dm = dm_n;
+        __syncthreads();
+    }
+    ptx::tc_fence_after();
+    if (warp == 0) ptx::tmem_dealloc<C::TMEM_COLS>(S.tmem);
+}

@@ -6,7 +6,7 @@
 //   (1) prefetch node plane L+2 of u^{it} and the update operands of plane L (u^{it-1}, w, mask)
 //       into registers — their latency hides under (2);
 //   (2) element forces of layer L (path-specific) -> smem fe[24][256];
-//   (3) scatter in global element order into two smem force planes; plane L is then complete
+//   (3) scatter into two smem force planes, node sums in the U2 tree order; plane L is then complete
 //       and is updated in place (Eq. 3 / L263-L266 with the sign of Eq. 3);
 //   (4) park the prefetched plane in the 3-slot smem ring.
 // INT8 path: 512 threads, two per element (u-half / G-half of ū_e, bottom / top output nodes),
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
         }
         __syncthreads();
 
-        // ---- (3) scatter (global element order) + update of the completed plane L ----
+        // ---- (3) scatter (U2 tree order) + update of the completed plane L ----
         if (t < NOWN) {
             auto fe = fe_of(S);
             const int e00 = nxl + EX * nyl, e10 = e00 + 1, e01 = e00 + EX, e11 = e01 + 1;
@@ -405,37 +405,24 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             double *fh = &S.facc[(L + 1) & 1][t * 3];
             const bool bot_iface = (p.slab_flags & 1) && L == 0;             // plane 0 owned, partial from below
             const bool top_iface = (p.slab_flags & 2) && L == p.nz;          // plane owned by the rank above
-            if (layer_ok && L >= Z0 && bot_iface) {   // keep the 4 contributions for the interface update
-                if (own)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        double *b = p.iface_bot_b + 12 * ucol + c;
-                        b[0] = fe[3 * 2 + c][e00];
-                        b[3] = fe[3 * 3 + c][e10];
-                        b[6] = fe[3 * 1 + c][e01];
-                        b[9] = fe[3 * 0 + c][e11];
-                    }
-            } else if (layer_ok && L >= Z0) {     // bottom corners of layer L -> plane L
+            // node force f_n = T_n + B_n, face sums (x-pair row iy) + (x-pair row iy-1) (reading U2)
+            if (layer_ok && L >= Z0) {     // bottom face of layer L -> plane L
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    double f = fl[c];
-                    f = __dadd_rn(f, fe[3 * 2 + c][e00]);
-                    f = __dadd_rn(f, fe[3 * 3 + c][e10]);
-                    f = __dadd_rn(f, fe[3 * 1 + c][e01]);
-                    f = __dadd_rn(f, fe[3 * 0 + c][e11]);
-                    fl[c] = f;
+                    const double B = __dadd_rn(__dadd_rn(fe[3 * 0 + c][e11], fe[3 * 1 + c][e01]),
+                                               __dadd_rn(fe[3 * 3 + c][e10], fe[3 * 2 + c][e00]));
+                    if (bot_iface) {       // interface plane: B waits for T from the rank below
+                        if (own) p.iface_bot_b[3 * ucol + c] = B;
+                    } else {
+                        fl[c] = __dadd_rn(fl[c], B);
+                    }
                 }
             }
-            if (layer_ok && L + 1 < Z1) {  // top corners of layer L -> plane L+1
+            if (layer_ok && L + 1 < Z1) {  // top face of layer L -> plane L+1
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    double f = fh[c];
-                    f = __dadd_rn(f, fe[3 * 6 + c][e00]);
-                    f = __dadd_rn(f, fe[3 * 7 + c][e10]);
-                    f = __dadd_rn(f, fe[3 * 5 + c][e01]);
-                    f = __dadd_rn(f, fe[3 * 4 + c][e11]);
-                    fh[c] = f;
-                }
+                for (int c = 0; c < 3; ++c)
+                    fh[c] = __dadd_rn(__dadd_rn(fe[3 * 4 + c][e11], fe[3 * 5 + c][e01]),
+                                      __dadd_rn(fe[3 * 7 + c][e10], fe[3 * 6 + c][e00]));
             }
             if (upd && top_iface) {
 #pragma unroll

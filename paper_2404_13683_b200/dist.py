@@ -4,10 +4,10 @@ Rank r owns element layers [ez0, ez1) (balanced to ±1 layer) and node planes ez
 rank ABOVE owns (updates) each interface plane, which keeps the result bit-identical to a
 single-GPU run: per step
     begin : fused step kernel over the slab (all planes but the interfaces updated); the top
-            interface's partial force A is left in a_send, plane 0's four layer-0 contributions
-            are kept on the device
+            interface's top-face force sum T is left in a_send, plane 0's bottom-face sum B
+            (layer 0) is kept on the device
     xchg A: a_send(r) -> a_recv(r+1)                                 (NCCL P2P over NVLink)
-    iface : owner continues ((((A+b1)+b2)+b3)+b4) in global element order and updates plane 0
+    iface : owner forms f = T + B (the single-GPU order, reading U2), updates plane 0
     xchg u: u_send(r) -> u_recv(r-1)
     end   : the rank below installs the updated plane, swaps u / u_prev
 Only plumbing lives here: partitioning, slicing the model, and the transport (torch.distributed

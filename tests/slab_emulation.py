@@ -8,8 +8,6 @@ import torch
 
 import oracle
 
-CORNER = {(1, 1): 2, (0, 1): 3, (1, 0): 1, (0, 0): 0}   # (node is +x corner, +y corner) -> local node
-
 
 class OracleSlabCompute:
     def __init__(self, lm, slab, path=oracle.PATH_FP64):
@@ -39,26 +37,6 @@ class OracleSlabCompute:
             F[3 * lm.src_node[k] + lm.src_axis[k]] += lm.amp[k, self.it] if self.it < lm.amp.shape[1] else 0.0
         return F
 
-    def _layer0_contribs(self):
-        lm, nx, ny = self.lm, self.lm.nx, self.lm.ny
-        b = np.zeros((self.nn2, 4, 3))
-        for ey in range(ny):
-            for ex in range(nx):
-                e = ex + nx * ey
-                nodes = oracle.element_nodes(nx, ny, e)
-                ue = np.concatenate([self.u[3 * q:3 * q + 3] for q in nodes])
-                m = lm.mat[e]
-                fe = (oracle.element_fp64(ue, lm.kappa[m], lm.G[m], lm.ds) if self.path == oracle.PATH_FP64
-                      else oracle.element_int8(ue, lm.kappa[m], lm.G[m], lm.ds)["fe"])
-                for dy in (0, 1):
-                    for dx in (0, 1):
-                        j = (ex + dx) + (nx + 1) * (ey + dy)
-                        # order: e(ix-1,iy-1), e(ix,iy-1), e(ix-1,iy), e(ix,iy)  ->  k = 2*(1-dy) + (1-dx)
-                        k = 2 * (1 - dy) + (1 - dx)
-                        a = CORNER[(dx, dy)]
-                        b[j, k, :] = fe[3 * a:3 * a + 3]
-        return b
-
     def begin(self):
         lm, nn2 = self.lm, self.nn2
         f = oracle.apply_K(lm.nx, lm.ny, lm.nz, lm.ds, lm.mat, lm.kappa, lm.G, self.u, path=self.path)
@@ -66,8 +44,8 @@ class OracleSlabCompute:
         self.F = F
         if self.slab.flags & 2:
             self.a_send.copy_(torch.from_numpy(f[3 * nn2 * lm.nz:]))
-        if self.slab.flags & 1:
-            self.b = self._layer0_contribs()
+        if self.slab.flags & 1:   # B: the bottom-face tree sum of layer 0 (no layer below locally)
+            self.b = f[:3 * nn2].copy()
         lo = 3 * nn2 if self.slab.flags & 1 else 0
         hi = 3 * nn2 * lm.nz if self.slab.flags & 2 else len(self.u)
         seg = slice(lo, hi)
@@ -89,10 +67,7 @@ class OracleSlabCompute:
         if not self.slab.flags & 1:
             return
         nn2 = self.nn2
-        f0 = self.a_recv.numpy().copy()
-        b = self.b.reshape(nn2, 4, 3)
-        for k in range(4):
-            f0 = f0 + b[:, k, :].reshape(-1)
+        f0 = self.a_recv.numpy() + self.b          # f_n = T_n + B_n (reading U2)
         seg = slice(0, 3 * nn2)
         up = np.ascontiguousarray(self.up[seg])
         oracle.update_dofs(self.w3[seg], self.F[seg], f0, self.u[seg], up)

@@ -44,6 +44,41 @@ def test_ebe_matches_dense_assembly(dims):
         assert np.linalg.norm(f - ref) <= 1e-14 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("path", [oracle.PATH_FP64, oracle.PATH_INT8])
+def test_summation_order_is_the_u2_tree(path):
+    """Reading U2: f_n = T_n + B_n with face(ez) = P(iy) + P(iy-1), P = x-pair of corner values
+    (missing elements 0.0), rebuilt here from the per-element forces one node at a time."""
+    m = wl.small_random(3, 2, 2, ds=0.01)
+    u = wl.random_field(m) * np.exp(np.random.default_rng(5).uniform(-8, 8, 3 * m.n_nodes))
+    nx, ny, nz = m.nx, m.ny, m.nz
+    fe = {}
+    for e in range(nx * ny * nz):
+        nodes = oracle.element_nodes(nx, ny, e)
+        ue = np.concatenate([u[3 * q:3 * q + 3] for q in nodes])
+        k = m.mat[e]
+        fe[(e % nx, (e // nx) % ny, e // (nx * ny))] = (
+            oracle.element_fp64(ue, m.kappa[k], m.G[k], m.ds) if path == oracle.PATH_FP64
+            else oracle.element_int8(ue, m.kappa[k], m.G[k], m.ds)["fe"])
+    corner = {(0, 0): 0, (0, 1): 1, (1, 1): 2, (1, 0): 3}   # (dy, dx) -> local node of e(ix-dx, iy-dy)
+
+    def val(ix, iy, ez, dx, dy, top, c):
+        e = (ix - dx, iy - dy, ez)
+        return fe[e][3 * (corner[(dy, dx)] + 4 * top) + c] if e in fe else 0.0
+
+    ref = np.zeros(3 * m.n_nodes)
+    for iz in range(nz + 1):
+        for iy in range(ny + 1):
+            for ix in range(nx + 1):
+                n = ix + (nx + 1) * (iy + (ny + 1) * iz)
+                for c in range(3):
+                    face = [(val(ix, iy, ez, 0, 0, top, c) + val(ix, iy, ez, 1, 0, top, c)) +
+                            (val(ix, iy, ez, 0, 1, top, c) + val(ix, iy, ez, 1, 1, top, c))
+                            for ez, top in ((iz - 1, 1), (iz, 0))]
+                    ref[3 * n + c] = face[0] + face[1]
+    f = oracle.apply_K(nx, ny, nz, m.ds, m.mat, m.kappa, m.G, u, path=path)
+    assert np.array_equal(f, ref)
+
+
 def test_free_cube_has_exactly_six_zero_modes():
     m = wl.small_random(3, 3, 3, ds=1.0)
     K = assemble.assemble_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G)

@@ -7,6 +7,8 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
                      capture_output=True, text=True).stdout
 fn = None; line = None; src = {}
 ins, stall, ops = Counter(), Counter(), defaultdict(Counter)
+reason = defaultdict(Counter)
+rcols = {}
 hdr = None
 for r in csv.reader(io.StringIO(out)):
     if not r:
@@ -16,6 +18,7 @@ for r in csv.reader(io.StringIO(out)):
     if r[0] == "Function Name" or r[0] == "Line No":
         if r[0] == "Line No":
             hdr = r
+            rcols = {i: h[6:] for i, h in enumerate(r) if h.startswith("stall_") and "Not Issued" not in h}
         continue
     if r[0]:
         line = (fn, int(r[0])); src[line] = r[1][:70]; continue
@@ -25,8 +28,16 @@ for r in csv.reader(io.StringIO(out)):
     op = toks[1] if toks[0].startswith("@") else toks[0]
     k = int(r[7]); s = int(r[4] or 0)
     ins[line] += k; stall[line] += s; ops[line][op.split(".")[0]] += k
+    for i, nm in rcols.items():
+        if i < len(r) and r[i].isdigit():
+            reason[line][nm] += int(r[i])
 tot = sum(ins.values()); tots = sum(stall.values()) or 1
 print("total warp-instr", tot)
 for key, v in sorted(ins.items(), key=lambda kv: -kv[1])[:n]:
     top = ", ".join(f"{o}:{c*100//v}" for o, c in ops[key].most_common(3))
     print(f"{key[0]}:{key[1]:<4d} {v/tot*100:5.1f}% st {stall[key]/tots*100:5.1f}%  {src.get(key,'')[:60]:60s} [{top}]")
+if "--stalls" in sys.argv:
+    print("\ntop lines by stall samples (main reasons):")
+    for key, v in sorted(stall.items(), key=lambda kv: -kv[1])[:n]:
+        rs = ", ".join(f"{nm}:{c*100//max(v,1)}" for nm, c in reason[key].most_common(3))
+        print(f"{key[0]}:{key[1]:<4d} st {v/tots*100:5.1f}%  {src.get(key,'')[:60]:60s} [{rs}]")
