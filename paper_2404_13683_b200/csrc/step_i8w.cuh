@@ -18,7 +18,7 @@
 //     through a small smem exchange, f_n = T_n (top face of layer L-1, from half 1) + B_n (bottom
 //     face of layer L, half 0), then the central-difference update (Eq. 3 / L263-L266
 //     with the sign of Eq. 3).  This post-phase of layer L-1 runs while the MMAs of layer L are
-//     in flight.  Results are bit-identical to the oracle.
+//     in flight.  Results are bit-identical to the test oracle's.
 
 struct I8W {
     static constexpr int EY = 8;
