@@ -285,7 +285,6 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
         li.smem = (int)sizeof(SmemI8W);
         return li;
     }
-    if (path == OVX_INT8) return info_t<OVX_INT8>(nx, ny, nz);
     if (path == OVX_FP64) return info_t<OVX_FP64>(nx, ny, nz);
     return info_t<OVX_FP64_DENSE>(nx, ny, nz);
 }

@@ -40,25 +40,6 @@ __device__ __forceinline__ long long mad_wide(int32_t a, int32_t b, long long ac
     return r;
 }
 
-// Bit pattern of the double 1.5·2^52 + 2^31 + (c0 + 2^8 c1 + 2^16 c2 + 2^24 c3) for stage products
-// |c_j| < 2^20: exact (the integer is < 2^45).  32-bit pairs, then one carry chain:
-//   p0 = c0 + 256 c1 + 2^31 (biased to unsigned), p1 = c2 + 256 c3 (signed),
-//   lo:hi = p0 + sext(p1)·2^16 + (0x43380000 << 32)
-__device__ __forceinline__ double limb_magic(int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
-    uint32_t lo, hi;
-    asm("{\n\t.reg .b32 p0, p1, t, h;\n\t"
-        "mad.lo.s32 p0, %3, 256, %2;\n\t"
-        "xor.b32 p0, p0, 0x80000000;\n\t"
-        "mad.lo.s32 p1, %5, 256, %4;\n\t"
-        "shl.b32 t, p1, 16;\n\t"
-        "shr.s32 h, p1, 16;\n\t"
-        "add.cc.u32 %0, p0, t;\n\t"
-        "addc.u32 %1, h, 0x43380000;\n\t}"
-        : "=r"(lo), "=r"(hi)
-        : "r"(c0), "r"(c1), "r"(c2), "r"(c3));
-    return __hiloint2double((int)hi, (int)lo);
-}
-
 // One lane of a converged warp (elect.sync): keeps the tcgen05 issue code warp-uniform.
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred;

@@ -20,6 +20,14 @@
 //     with the sign of Eq. 3).  This post-phase of layer L-1 runs while the MMAs of layer L are
 //     in flight.  Results are bit-identical to the test oracle's.
 
+// A operand row (one element, one half-word array): 7 chunks of 16 B — chunks 0-2 the u bytes,
+// 3-5 the G bytes, 6 zero (K padding of the identity block's second K-step).
+constexpr int A1_CHUNKS = 7;
+constexpr int A1_PITCH = A1_CHUNKS * 128 + 16;   // bytes per 8-row core-matrix group (+16: bank spread)
+constexpr int A1_BYTES = 16 * A1_PITCH;          // one half-word array of 128 rows
+constexpr int B1_PITCH = 6 * 128;                // main B: 48 rows × 96 K-bytes
+constexpr int BI_PITCH = 2 * 128;                // identity blocks: 48 rows × 32 K-bytes
+
 struct I8W {
     static constexpr int EY = 8;
     static constexpr int NE = EX * EY;                 // elements per layer

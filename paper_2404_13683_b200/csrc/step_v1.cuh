@@ -9,27 +9,20 @@
 //   (3) scatter into two smem force planes, node sums in the U2 tree order; plane L is then complete
 //       and is updated in place (Eq. 3 / L263-L266 with the sign of Eq. 3);
 //   (4) park the prefetched plane in the 3-slot smem ring.
-// INT8 path: 512 threads, two per element (u-half / G-half of ū_e, bottom / top output nodes),
-// two M=128 tcgen05.mma.kind::i8 tiles per layer into TMEM (2 × 4 arrays × N48, 64-col pitch).
-// The Eq. 9 diagonal term is folded into the integer product (DESIGN.md variant D): per array
-// 3 K-steps against B = −K_e^INT8 ⊗ I_2 plus 2 K-steps of the G bytes against −128·I ⊗ I_2, so
-// D = −(K_e^INT8 v + 128 v_G) byte-stage by byte-stage, and f_e = RN(c1 s_e 2^-56)·RN(y).
+// Paths: OVX_FP64_DENSE (the literal dense form, bit-exact mirror of the oracle's FP64
+// definition) and OVX_FP64 when z-slab interfaces or debug records are requested.
 
-constexpr int EY_I8V = 4;   // INT8 tile: 32×4 elements = one M=128 MMA tile; 2 CTAs per SM
 template <int PATH>
 struct V1 {
-    static constexpr int EY = PATH == OVX_INT8 ? EY_I8V : 8;
+    static constexpr int EY = 8;
     static constexpr int NE = EX * EY;                 // 256 elements per layer
-    static constexpr int TPE = PATH == OVX_INT8 ? 2 : 1;
-    static constexpr int NT = NE * TPE;                // threads
+    static constexpr int NT = NE;                      // threads, one per element
     static constexpr int TY = EY - 1;                  // 7 owned node rows
     static constexpr int PY = EY + 1;                  // 9 node rows per smem plane
     static constexpr int NOWN = TX * TY;               // 217 owned nodes per plane
     static constexpr int PLANE = PX * PY * 3;          // 891 doubles per plane
     static constexpr int PF = (PLANE + NT - 1) / NT;   // prefetched doubles per thread
-    static constexpr int MT = NE / 128;                // INT8: M=128 MMA tiles per layer
-    static constexpr int MINB = PATH == OVX_INT8 ? (MT == 1 ? 2 : 1) : 2;
-    static constexpr int TMEM_COLS = MT * 256;
+    static constexpr int MINB = 2;
 };
 
 struct SmemV1F64 {
@@ -38,34 +31,8 @@ struct SmemV1F64 {
     double facc[2][V1<OVX_FP64>::NOWN * 3];
 };
 
-// A operand row (one element, one half-word array): 7 chunks of 16 B — chunks 0-2 the u bytes,
-// 3-5 the G bytes, 6 zero (K padding of the identity block's second K-step).
-constexpr int A1_CHUNKS = 7;
-constexpr int A1_PITCH = A1_CHUNKS * 128 + 16;   // bytes per 8-row core-matrix group (+16: bank spread)
-constexpr int A1_BYTES = 16 * A1_PITCH;          // one half-word array of 128 rows
-constexpr int B1_PITCH = 6 * 128;                // main B: 48 rows × 96 K-bytes
-constexpr int BI_PITCH = 2 * 128;                // identity blocks: 48 rows × 32 K-bytes
-
-struct SmemV1I8 {
-    struct {
-        uint8_t A[V1<OVX_INT8>::MT][4][A1_BYTES];   // [M-tile][half-word array], K-major layout
-    } u;
-    double fe[24][V1<OVX_INT8>::NE];  // separate from A: one M-tile's epilogue may run while
-                                      // another M-tile's MMAs still read their A arrays
-    alignas(128) uint8_t B[6 * B1_PITCH];
-    alignas(128) uint8_t BI[2][6 * BI_PITCH];
-    double up[3][V1<OVX_INT8>::PLANE];
-    double facc[2][V1<OVX_INT8>::NOWN * 3];
-    double amax[2][V1<OVX_INT8>::NE];
-    uint64_t mbar[V1<OVX_INT8>::MT];
-    uint32_t tmem;
-};
-
 template <int PATH>
-using SmemV1 = typename std::conditional<PATH == OVX_INT8, SmemV1I8, SmemV1F64>::type;
-
-__device__ __forceinline__ auto fe_of(SmemV1I8 &S) { return S.fe; }
-__device__ __forceinline__ auto fe_of(SmemV1F64 &S) { return S.fe; }
+using SmemV1 = SmemV1F64;
 
 template <int PATH>
 __device__ __forceinline__ void v1_load_plane_sync(double *dst, const StepParams &p, int64_t X0, int64_t Y0,
@@ -90,7 +57,6 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     SmemV1<PATH> &S = *reinterpret_cast<SmemV1<PATH> *>(smem_raw);
     const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
 
     int bid = blockIdx.x;
     const int tx = bid % p.tiles_x;
@@ -103,17 +69,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
     const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
     const int64_t PSTRIDE = NX1 * NY1;        // nodes per plane
 
-    // element (and half) handled by this thread
-    int el, half = 0, mt = 0, row = 0;
-    if constexpr (PATH == OVX_INT8) {
-        const int g = warp >> 2;          // 0..3: (M-tile, half)
-        row = (warp & 3) * 32 + lane;     // TMEM lane = MMA row
-        mt = g >> 1;
-        half = g & 1;                     // 0: u-part of ū_e, outputs of nodes 0-3; 1: G-part, nodes 4-7
-        el = mt * 128 + row;
-    } else {
-        el = t;
-    }
+    const int el = t;                          // element of this thread
     const int lx = el % EX, ly = el / EX;
     const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
     const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
@@ -157,41 +113,11 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             has_rec |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
         }
 
-    uint32_t phase = 0;
-    if constexpr (PATH == OVX_INT8) {
-        // resident B operands: B[n = 2i+b'][kb = 2k+b] = −K_e^INT8[i][k]·δ(b,b');
-        // BI[s][n][kb] = −128·δ(k, i − 16 s)·δ(b,b') on the G bytes (k = G index within the K-step)
-        for (int idx = t; idx < 48 * 96; idx += NT) {
-            const int n = idx / 96, kb = idx - n * 96;
-            const int off = (n >> 3) * B1_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
-            S.B[off] = ((kb & 1) == (n & 1)) ? (uint8_t)(-(int)c_K8[(n >> 1) * 48 + (kb >> 1)]) : (uint8_t)0;
-        }
-        for (int idx = t; idx < 2 * 48 * 32; idx += NT) {
-            const int s2 = idx / (48 * 32), r2 = idx - s2 * 48 * 32;
-            const int n = r2 / 32, kb = r2 - n * 32;
-            const int off = (n >> 3) * BI_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
-            const int k = 16 * s2 + (kb >> 1);
-            S.BI[s2][off] = ((kb & 1) == (n & 1) && k == (n >> 1)) ? (uint8_t)0x80 : (uint8_t)0;
-        }
-        // zero the K-padding chunk of every A row (never written afterwards)
-        for (int idx = t; idx < C::MT * 4 * 128; idx += NT) {
-            const int a = idx >> 7, r = idx & 127;
-            *reinterpret_cast<uint4 *>(&S.u.A[a >> 2][a & 3][(r >> 3) * A1_PITCH + 6 * 128 + (r & 7) * 16]) =
-                make_uint4(0, 0, 0, 0);
-        }
-        if (warp == 0) ptx::tmem_alloc<C::TMEM_COLS>(&S.tmem);
-        if (t == 0) {
-            for (int mm = 0; mm < C::MT; ++mm) ptx::mbar_init(&S.mbar[mm], 1);
-        }
-        ptx::fence_proxy_async_smem();
-        ptx::tc_fence_before();
-    }
     for (int i = t; i < 2 * NOWN * 3; i += NT) (&S.facc[0][0])[i] = 0.0;
     const int64_t Lfirst = max(Z0 - 1, (int64_t)0);
     v1_load_plane_sync<PATH>(S.up[Lfirst % 3], p, X0, Y0, Lfirst);
     v1_load_plane_sync<PATH>(S.up[(Lfirst + 1) % 3], p, X0, Y0, Lfirst + 1);
     __syncthreads();
-    if constexpr (PATH == OVX_INT8) ptx::tc_fence_after();
 
     // material of this thread's element in the current layer (prefetched one layer ahead;
     // elements outside the domain use the reserved zero material)
@@ -251,155 +177,13 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                     S.fe[r][el] = ein ? f : 0.0;
                     if (MODE == MODE_DEBUG && dbg && p.dbg_fe) p.dbg_fe[dj * 24 + r] = f;
                 }
-            } else {
-                // ---- Eqs. 10-16: s_e, INT64 image, byte slices -> A operand (this thread: 24 of 48) ----
-                const double cG = c_mat[m].cG;
-                double hm = 0.0;
-                if (half) {
-#pragma unroll
-                    for (int i = 12; i < 24; ++i) hm = fmax(hm, fabs(ue[i]));
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 12; ++i) hm = fmax(hm, fabs(ue[i]));
-                }
-                S.amax[half][el] = hm;
-                asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
-                const double amax = fmax(S.amax[0][el], S.amax[1][el]);
-                // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)  (RN is monotone, cG > 0)
-                const double s = fmax(amax, __dmul_rn(cG, amax));
-                const bool deg = !ein || !(s >= 0x1p-1022) || isinf(s);
-                uint8_t *Ab = &S.u.A[mt][0][0];
-                const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16) + (uint32_t)(3 * half) * 128;
-                // ū_e for this half: u_e (half 0) or RN(cG·u_e) (half 1); half is warp-uniform
-                if (half) {
-#pragma unroll
-                    for (int i = 0; i < 24; ++i) ue[i] = __dmul_rn(cG, ue[i]);
-                }
-                const bool straight = !deg && s >= 0x1p-960;
-                const double r = 1.0 / s;                          // RN(1/s_e), reading Q7
-                const double R = __dmul_rn(r, 0x1p56);             // exact power-of-two scaling
-#pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {                   // 8 values at a time: convert, pack, store
-                    long long v[8];
-                    if (straight) {
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) v[q] = __double2ll_rz(__dmul_rn(ue[ch * 8 + q], R));  // trunc (Q8)
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            v[q] = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ue[ch * 8 + q], r), 0x1p56));
-                    }
-                    uint32_t lo[8], hi[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const unsigned long long vp = (unsigned long long)v[q] + (1ull << 56);
-                        lo[q] = (uint32_t)vp;
-                        hi[q] = (uint32_t)(vp >> 32);
-                        if (MODE == MODE_DEBUG && dbg) {
-                            const int k = 24 * half + ch * 8 + q;
-                            if (p.dbg_v) p.dbg_v[dj * 48 + k] = v[q];
-                            if (p.dbg_d)
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = (uint8_t)(vp >> (8 * j));
-                        }
-                    }
-                    const uint32_t off = rowoff + (uint32_t)ch * 128;
-#pragma unroll
-                    for (int pa = 0; pa < 4; ++pa) {
-                        const uint32_t *src = pa < 2 ? lo : hi;
-                        const uint32_t sel = (pa & 1) ? 0x7632u : 0x5410u;
-                        uint4 wv;
-                        wv.x = __byte_perm(src[0], src[1], sel);
-                        wv.y = __byte_perm(src[2], src[3], sel);
-                        wv.z = __byte_perm(src[4], src[5], sel);
-                        wv.w = __byte_perm(src[6], src[7], sel);
-                        *reinterpret_cast<uint4 *>(Ab + pa * A1_BYTES + off) = wv;
-                    }
-                }
-                if (MODE == MODE_DEBUG && dbg && half == 0 && p.dbg_s) p.dbg_s[dj] = s;
-
-                // ---- Eq. 17 (+ folded diagonal): this M-tile, 4 arrays × (3 + 2) K-steps, M128 N48 K32 ----
-                // Each M-tile (8 warps) hands off to the tensor core on its own named barrier, so one
-                // M-tile's MMAs overlap the other M-tile's digit or epilogue work.
-                ptx::fence_proxy_async_smem();
-                asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");
-                if (t == 256 * mt) {
-                    ptx::tc_fence_after();
-                    const uint32_t b0 = ptx::smem_u32(&S.B[0]);
-                    const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
-                    {
-                        const int mm = mt;
-                        const uint32_t a0 = ptx::smem_u32(&S.u.A[mm][0][0]);
-#pragma unroll
-                        for (int pa = 0; pa < 4; ++pa) {
-                            const uint32_t ab = a0 + pa * A1_BYTES;
-                            const uint32_t d = S.tmem + mm * 256 + pa * 64;
-#pragma unroll
-                            for (int ks = 0; ks < 3; ++ks)
-                                ptx::mma_i8(d, ptx::smem_desc(ab + ks * 256, 128, A1_PITCH),
-                                            ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC, ks > 0 ? 1u : 0u);
-                            ptx::mma_i8(d, ptx::smem_desc(ab + 3 * 128, 128, A1_PITCH),
-                                        ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
-                            ptx::mma_i8(d, ptx::smem_desc(ab + 5 * 128, 128, A1_PITCH),
-                                        ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
-                        }
-                        ptx::mma_commit(&S.mbar[mm]);
-                    }
-                }
-                // one warp of the M-tile polls the MMA-completion mbarrier; the other seven block in
-                // hardware on the named barrier (no issue slots spent spinning)
-                if (warp == 8 * mt) ptx::mbar_wait(&S.mbar[mt], phase);
-                asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");
-                phase ^= 1;
-                ptx::tc_fence_after();
-
-                // ---- epilogue: 12 outputs (nodes 4·half .. 4·half+3) ----
-                // D_p holds −C_j with C_j = K_D·b_j (K_D·1 = 0, so y = Σ_j 256^j C_j exactly).
-                // Two 64-bit limbs (< 2^44) through the 1.5·2^52 magic, one rounding in the fma.
-                const double alpha = -__dmul_rn(c_mat[m].c1, __dmul_rn(s, 0x1p-56));   // −RN(c1·s·2^-56)
-                const uint32_t tb = S.tmem + ((uint32_t)((warp & 3) * 32) << 16) + mt * 256 + half * 24;
-#pragma unroll
-                for (int cc = 0; cc < 3; ++cc) {           // 4 outputs per round (8 columns per array)
-                    uint32_t R0[8], R1[8], R2[8], R3[8];
-                    ptx::tmem_ld8(tb + 0 + cc * 8, R0);
-                    ptx::tmem_ld8(tb + 64 + cc * 8, R1);
-                    ptx::tmem_ld8(tb + 128 + cc * 8, R2);
-                    ptx::tmem_ld8(tb + 192 + cc * 8, R3);
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int i = 12 * half + cc * 4 + q;
-                        const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
-                        const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
-                        const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
-                        const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
-                        const double dlo = ptx::limb_magic(c0, c1_, c2_, c3) - (0x1.8p52 + 0x1p31);
-                        const double dhi = ptx::limb_magic(c4, c5, c6, c7) - (0x1.8p52 + 0x1p31);
-                        const double Y = __fma_rn(dhi, 0x1p32, dlo);    // RN(−y)
-                        const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
-                        if (MODE == MODE_DEBUG && dbg) {
-                            const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};
-                            __int128 y = 0;
-#pragma unroll
-                            for (int j = 7; j >= 0; --j) y = y * 256 - (__int128)Cj[j];
-                            if (p.dbg_C)
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) p.dbg_C[dj * 192 + j * 24 + i] = -Cj[j];
-                            if (p.dbg_yhi) p.dbg_yhi[dj * 24 + i] = (long long)(y >> 64);
-                            if (p.dbg_ylo) p.dbg_ylo[dj * 24 + i] = (long long)(unsigned long long)y;
-                            if (p.dbg_fe) p.dbg_fe[dj * 24 + i] = f;
-                        }
-                        S.fe[i][el] = f;
-                    }
-                }
-                ptx::tc_fence_before();
             }
         }
         __syncthreads();
 
         // ---- (3) scatter (U2 tree order) + update of the completed plane L ----
         if (t < NOWN) {
-            auto fe = fe_of(S);
+            auto fe = S.fe;
             const int e00 = nxl + EX * nyl, e10 = e00 + 1, e01 = e00 + EX, e11 = e01 + 1;
             double *fl = &S.facc[L & 1][t * 3];
             double *fh = &S.facc[(L + 1) & 1][t * 3];
@@ -463,9 +247,5 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             }
         }
         __syncthreads();
-    }
-    if constexpr (PATH == OVX_INT8) {
-        ptx::tc_fence_after();
-        if (warp == 0) ptx::tmem_dealloc<C::TMEM_COLS>(S.tmem);
     }
 }

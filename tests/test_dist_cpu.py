@@ -1,7 +1,7 @@
 """z-slab protocol (paper_2404_13683_b200/dist.py) on CPU: partitioning, slicing, and the
 interface exchange over a real torch.distributed gloo process group (world sizes 2 and 3),
 with the oracle as the per-slab compute.  The assembled field must equal the monolithic
-oracle run bit for bit (the owner-computes interface keeps global element order)."""
+oracle run bit for bit (the owner-computes interface forms f = T + B, the order of reading U2)."""
 import os
 import socket
 import sys

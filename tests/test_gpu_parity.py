@@ -3,9 +3,9 @@
 Bars:
   * integer work (v, byte slices, per-stage tensor-core products C_j, y) — bit-exact;
   * element forces, global f = K u, node w, and whole trajectories — bit-exact, because the
-    kernel reproduces the oracle's operation order (explicit _rn intrinsics, element-order
-    scatter); the 1e-10 rel-L2 bar of BASELINE.json is checked as well;
-  * full-size (256³) launches: sampled nodes recomputed by the oracle element by element.
+    kernel reproduces the oracle's operation order (explicit _rn intrinsics, node sums in the
+    tree order of reading U2); the 1e-10 rel-L2 bar of BASELINE.json is checked as well;
+  * full-size (256³) launches: sampled nodes recomputed by the oracle node by node.
 """
 import math
 
@@ -153,25 +153,26 @@ def test_1000_steps_int8_vs_fp64_oracle(ovxmod):
 
 
 def _node_force_oracle(m, u, ix, iy, iz, path):
-    """f at one node from the oracle's element forces, scattered in element order."""
-    f = np.zeros(3)
-    for dz in (-1, 0):
-        for dy in (-1, 0):
-            for dx in (-1, 0):
-                ex, ey, ez = ix + dx, iy + dy, iz + dz
-                if not (0 <= ex < m.nx and 0 <= ey < m.ny and 0 <= ez < m.nz):
-                    continue
-                e = ex + m.nx * (ey + m.ny * ez)
-                nodes = oracle.element_nodes(m.nx, m.ny, e)
-                ue = np.concatenate([u[3 * n:3 * n + 3] for n in nodes])
-                mm = m.mat[e]
-                fe = (oracle.element_int8(ue, m.kappa[mm], m.G[mm], m.ds)["fe"] if path == 0
-                      else oracle.element_fp64(ue, m.kappa[mm], m.G[mm], m.ds))
-                # local node a of element e is this node: corner sign + for dx = -1 (node is the +x corner)
-                a = {(1, 1, 1): 6, (0, 1, 1): 7, (1, 0, 1): 5, (0, 0, 1): 4,
-                     (1, 1, 0): 2, (0, 1, 0): 3, (1, 0, 0): 1, (0, 0, 0): 0}[(int(dx == -1), int(dy == -1), int(dz == -1))]
-                f = f + fe[3 * a:3 * a + 3]
-    return f
+    """f at one node from the oracle's element forces, summed in the order of reading U2:
+    f = T + B, face = P(iy) + P(iy-1), P = f(ix,·)[corner] + f(ix-1,·)[corner] (missing: 0.0)."""
+    corner = {(0, 0): 0, (0, 1): 1, (1, 1): 2, (1, 0): 3}   # (dy, dx) -> local node of e(ix-dx, iy-dy)
+
+    def val(dx, dy, ez, top):
+        ex, ey = ix - dx, iy - dy
+        if not (0 <= ex < m.nx and 0 <= ey < m.ny and 0 <= ez < m.nz):
+            return np.zeros(3)
+        e = ex + m.nx * (ey + m.ny * ez)
+        nodes = oracle.element_nodes(m.nx, m.ny, e)
+        ue = np.concatenate([u[3 * n:3 * n + 3] for n in nodes])
+        mm = m.mat[e]
+        fe = (oracle.element_int8(ue, m.kappa[mm], m.G[mm], m.ds)["fe"] if path == 0
+              else oracle.element_fp64(ue, m.kappa[mm], m.G[mm], m.ds))
+        a = corner[(dy, dx)] + 4 * top
+        return fe[3 * a:3 * a + 3]
+
+    faces = [(val(0, 0, ez, top) + val(1, 0, ez, top)) + (val(0, 1, ez, top) + val(1, 1, ez, top))
+             for ez, top in ((iz - 1, 1), (iz, 0))]
+    return faces[0] + faces[1]
 
 
 @pytest.mark.parametrize("name,path", PATHS)
