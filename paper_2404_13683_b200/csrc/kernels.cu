@@ -17,6 +17,7 @@
 //             tcgen05.mma.kind::i8 (M=128 elements, N=48, K=96, 4 half-word arrays),
 //             K_e^INT8 ⊗ I_2 as the resident s8 B operand, s32 accumulators in TMEM,
 //             exact two-limb recombination y = K_e^INT8 v and f_e = c1·(RN(y)·s_e 2^-56 + c2 u_e).
+#include <algorithm>
 #include <cstdlib>
 
 #include "ovx_internal.h"
@@ -244,15 +245,41 @@ __global__ void finite_kernel(const double *__restrict__ u, int64_t n, int *flag
         if (!isfinite(u[i])) *flag = 1;
 }
 
-constexpr int kZChunk = 64;
+// z-chunk length (node planes per CTA).  Each CTA recomputes one halo layer below its chunk, and
+// the grid runs in waves of (SMs × resident CTAs per SM); pick the chunk count n minimising
+//   waves(n) × layers per CTA = ceil(tiles_xy·n / (SMs·cps)) × (ceil(planes/n) + 1)
+// (fewest chunks on ties), with chunks of at least 8 planes.
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    return n;
+}
+
+int choose_zchunk(int64_t planes, int64_t tiles_xy, int ctas_per_sm) {
+    const int64_t slots = (int64_t)num_sms() * ctas_per_sm;
+    const int64_t nmax = std::max<int64_t>(1, planes / 8);
+    int64_t best_n = 1, best_cost = -1;
+    for (int64_t n = 1; n <= nmax; ++n) {
+        const int64_t len = (planes + n - 1) / n;
+        const int64_t cost = ((tiles_xy * n + slots - 1) / slots) * (len + 1);
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best_n = n;
+        }
+    }
+    return (int)((planes + best_n - 1) / best_n);
+}
 
 template <int PATH>
 LaunchInfo info_t(int64_t nx, int64_t ny, int64_t nz) {
     using C = V1<PATH>;
     LaunchInfo li;
     const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + C::TY - 1) / C::TY;
-    const int64_t tz = (nz + 1 + kZChunk - 1) / kZChunk;   // balanced chunks (see launch_step)
-    li.ctas = tx * ty * tz;
+    const int zc = choose_zchunk(nz + 1, tx * ty, 2);
+    li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
     li.threads = C::NT;
     li.smem = PATH == OVX_FP64 ? (int)sizeof(SmemF2) : (int)sizeof(SmemV1<PATH>);
     return li;
@@ -279,8 +306,8 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
         LaunchInfo li;
         const int tyy = 8 - 1;
         const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + tyy - 1) / tyy;
-        const int64_t tz = (nz + 1 + kZChunk - 1) / kZChunk;
-        li.ctas = tx * ty * tz;
+        const int zc = choose_zchunk(nz + 1, tx * ty, 1);
+        li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
         li.threads = I8W::NT;
         li.smem = (int)sizeof(SmemI8W);
         return li;
@@ -293,8 +320,7 @@ cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
     const int ty = path == OVX_INT8 ? 8 - 1 : V1<OVX_FP64>::TY;
     p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
     p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
-    const int64_t nchunk = (p.nz + 1 + kZChunk - 1) / kZChunk;        // chunks of <= 64 planes,
-    p.zchunk = (int)((p.nz + 1 + nchunk - 1) / nchunk);                 // balanced in size
+    p.zchunk = choose_zchunk(p.nz + 1, (int64_t)p.tiles_x * p.tiles_y, path == OVX_INT8 ? 1 : 2);
     const int64_t tz = (p.nz + 1 + p.zchunk - 1) / p.zchunk;
     const int64_t ctas = (int64_t)p.tiles_x * p.tiles_y * tz;
     if (path == OVX_INT8) {

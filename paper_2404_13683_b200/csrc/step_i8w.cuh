@@ -168,9 +168,12 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     const int64_t ucol = own ? ex + NX1 * ey : 0;
     const bool upd_role = own && hf == 0;
 
-    // plane loader role: node t of the smem plane
-    const int lpx = t % PX, lpy = t / PX;
-    const bool ldn = t < NODES && X0 - 1 + lpx >= 0 && X0 - 1 + lpx < NX1 && Y0 - 1 + lpy >= 0 && Y0 - 1 + lpy < NY1;
+    // plane loader role: node li of the smem plane, taken by the last NODES threads (mostly
+    // half-1 warps, which have the lighter post-phase)
+    const int li = t - (NT - NODES);
+    const bool lrole = li >= 0;
+    const int lpx = lrole ? li % PX : 0, lpy = lrole ? li / PX : 0;
+    const bool ldn = lrole && X0 - 1 + lpx >= 0 && X0 - 1 + lpx < NX1 && Y0 - 1 + lpy >= 0 && Y0 - 1 + lpy < NY1;
     const int64_t ldoff = ldn ? 3 * ((X0 - 1 + lpx) + NX1 * (Y0 - 1 + lpy)) : 0;
 
     bool has_src = false, has_rec = false;
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     const int Lfirst = max(Z0 - 1, 0);
     for (int j = 0; j < 2; ++j) {
         const int iz = Lfirst + j;
-        if (t < NODES) {
+        if (lrole) {
             double v3[3] = {0.0, 0.0, 0.0};
             if (ldn && iz <= nz)
 #pragma unroll
@@ -221,11 +224,11 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             unsigned long long m = 0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                S.up[iz & 3][3 * t + c] = v3[c];
+                S.up[iz & 3][3 * li + c] = v3[c];
                 const unsigned long long b = abs_bits(v3[c]);
                 m = b > m ? b : m;
             }
-            S.nmax[iz & 3][t] = m;
+            S.nmax[iz & 3][li] = m;
         }
     }
     ptx::fence_proxy_async_smem();
@@ -439,15 +442,15 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             }
         }
         // ---- park plane L+2 (slot of plane L-2, no longer read) with its node maxima ----
-        if (pf && t < NODES) {
+        if (pf && lrole) {
             unsigned long long m = 0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                S.up[pz & 3][3 * t + c] = pfv[c];
+                S.up[pz & 3][3 * li + c] = pfv[c];
                 const unsigned long long b = abs_bits(pfv[c]);
                 m = b > m ? b : m;
             }
-            S.nmax[pz & 3][t] = m;
+            S.nmax[pz & 3][li] = m;
         }
         prev_layer = layer_ok;
         if (L >= Lfirst) {
