@@ -335,7 +335,7 @@ def main() -> None:
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_src": pk["src"],
                 "bytes_per_launch": bytes_launch, "kernel_ms_per_launch": kernel_ms,
-                "kernel": {0: "step_v1<INT8>", 1: "step_f64", 2: "step_v1<FP64_DENSE>"}[path]}
+                "kernel": {0: "step_i8w<M=8>", 1: "step_f64", 2: "step_v1<FP64_DENSE>"}[path]}
     nodes_total = (args.n + 1) ** 2 * (args.n * world + 1)
     out = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
