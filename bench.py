@@ -360,7 +360,7 @@ def main() -> None:
                 "note": f"per GPU: set_state(host pinned) + {args.steps} steps + get_state(host)"},
     }
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_oracle_sample(path == OVX_INT8, steps=3)
+        out["cpu_baseline"] = cpu_oracle_sample(path == OVX_INT8, steps=8)   # ~10 s of oracle work
     print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
