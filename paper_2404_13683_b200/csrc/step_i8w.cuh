@@ -45,9 +45,9 @@ struct SmemI8W {
     uint8_t A[I8W::MT][4][A1_BYTES];      // [M-tile][half-word array], K-major canonical layout
     alignas(128) uint8_t B[6 * B1_PITCH];
     alignas(128) uint8_t BI[2][6 * BI_PITCH];
-    double up[4][I8W::PLANE];                       // ring: L-1 (update), L, L+1 (gather), L+2
-    unsigned long long nmax[4][I8W::NODES];         // max_c |u_c| of each node (bit patterns)
-    double ysum[2][2][I8W::EY][EX][3];              // [layer parity][face] x-pair P of the +y corners
+    double up[5][I8W::PLANE];                       // ring: L-2, L-1 (updates), L, L+1 (gather), L+2
+    unsigned long long nmax[5][I8W::NODES];         // max_c |u_c| of each node (bit patterns)
+    double ysum[3][2][I8W::EY][EX][3];              // [layer mod 3][face] x-pair P of the +y corners
     double tf[2][I8W::NE][3];                       // [layer parity][tile node] top-face sums T
     uint64_t mbar[I8W::MT];
     uint32_t tmem;
@@ -129,6 +129,15 @@ __device__ __forceinline__ void i8w_convert(const StepParams &p, const double (&
     }
 }
 
+__device__ __forceinline__ int ring5(int x) { return (x + 10) % 5; }   // x >= -10
+__device__ __forceinline__ int ring3(int x) { return (x + 9) % 3; }    // x >= -9
+
+// Skewed M-tiles: in iteration L (one CTA barrier at its end)
+//   M-tile 0: convert(L) -> MMA(L) | post-phase(L-1) | epilogue(L)
+//   M-tile 1: post-phase(L-2) | epilogue(L-1) | convert(L) -> MMA(L)   (its MMAs run across the barrier)
+// so one M-tile's conversion (F2I / FP64 heavy) overlaps the other's epilogue (integer heavy) and the
+// tensor core work of the two M-tiles is spread over the iteration.  Node row 4 (M-tile 1) reads the
+// x-pairs of element row 3 (M-tile 0) one iteration after they were written.
 template <int MODE, int M>
 __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     using C = I8W;
@@ -155,6 +164,9 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     const int nz = (int)p.nz;
     const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
     const int64_t PSTRIDE = NX1 * NY1;
+    const int Lfirst = max(Z0 - 1, 0);
+    const int Lend = min(nz, Z1);                       // layers [Lfirst, Lend) are computed
+    auto layer_ok = [&](int x) { return x >= Lfirst && x < Lend; };
 
     // element (lx, ly) of the tile; its (-x,-y) corner is tile node (lx, ly)
     const int lx = lane, ly = 4 * mt + qd;
@@ -168,8 +180,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     const int64_t ucol = own ? ex + NX1 * ey : 0;
     const bool upd_role = own && hf == 0;
 
-    // plane loader role: node li of the smem plane, taken by the last NODES threads (mostly
-    // half-1 warps, which have the lighter post-phase)
+    // plane loader role: node li of the smem plane, taken by the last NODES threads
     const int li = t - (NT - NODES);
     const bool lrole = li >= 0;
     const int lpx = lrole ? li % PX : 0, lpy = lrole ? li / PX : 0;
@@ -213,7 +224,6 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     if (t == 0)
         for (int mm = 0; mm < C::MT; ++mm) ptx::mbar_init(&S.mbar[mm], 1);
     for (int i = t; i < 2 * C::NE * 3; i += NT) (&S.tf[0][0][0])[i] = 0.0;
-    const int Lfirst = max(Z0 - 1, 0);
     for (int j = 0; j < 2; ++j) {
         const int iz = Lfirst + j;
         if (lrole) {
@@ -224,11 +234,11 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             unsigned long long m = 0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                S.up[iz & 3][3 * li + c] = v3[c];
+                S.up[ring5(iz)][3 * li + c] = v3[c];
                 const unsigned long long b = abs_bits(v3[c]);
                 m = b > m ? b : m;
             }
-            S.nmax[iz & 3][li] = m;
+            S.nmax[ring5(iz)][li] = m;
         }
     }
     ptx::fence_proxy_async_smem();
@@ -239,16 +249,194 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     uint32_t phase = 0;
     int mcur = (ein && Lfirst < nz) ? (int)__ldg(matp + mstride * Lfirst) : kZeroMat;
     int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matp + mstride * (Lfirst + 1)) : kZeroMat;
-    double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;   // update operands of plane L-1
+    double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;   // update operands of this M-tile's post-phase plane
     uint8_t dm = 0;
-    double plo[3] = {0.0, 0.0, 0.0};             // x-pair P(iy) of this thread's face, layer L-1
-    bool prev_layer = false;                     // was layer L-1 computed?
+    double plo[3] = {0.0, 0.0, 0.0};             // x-pair P(iy) of this thread's face, last epilogue layer
+    // conversion -> epilogue hand-over (the same iteration for M-tile 0, the next one for M-tile 1)
+    double es = 0.0;
+    bool edeg = false, edbg = false;
+    int em = kZeroMat;
+    int64_t edj = -1;
 
-    for (int L = Z0 - 1; L <= Z1; ++L) {
-        const bool layer_ok = (L >= 0 && L < nz && L < Z1);
-        const int Ld = L - 1;                                        // post-phase layer / plane
-        const bool plane_done = (Ld >= Z0 && Ld <= nz && Ld < Z1);   // plane Ld completes now
-        // ---- 1. prefetch: plane L+2, material of layer L+2, update operands of plane L ----
+    // ---- post-phase of layer / plane Lp: face sums, f_n = T + B, update ----
+    auto post_phase = [&](int Lp) {
+        if (!tnode) return;
+        const bool plane_done = (Lp >= Z0 && Lp <= nz && Lp < Z1);
+        const bool bot_iface = (p.slab_flags & 1) && Lp == 0;
+        const bool top_iface = (p.slab_flags & 2) && Lp == nz;
+        double face[3] = {0.0, 0.0, 0.0};
+        if (layer_ok(Lp)) {
+            const double(*ys)[EX][3] = S.ysum[ring3(Lp)][hf];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) face[c] = __dadd_rn(plo[c], ys[ly - 1][lx][c]);   // P(iy) + P(iy-1)
+        }
+        if (hf == 1) {        // top face of layer Lp: T of plane Lp+1
+#pragma unroll
+            for (int c = 0; c < 3; ++c) S.tf[Lp & 1][lx + EX * ly][c] = face[c];
+        } else if (own && plane_done) {
+            const int64_t un_id = ucol + PSTRIDE * Lp;
+            if (bot_iface) {  // interface plane: B waits for T from the rank below
+#pragma unroll
+                for (int c = 0; c < 3; ++c) p.iface_bot_b[3 * ucol + c] = face[c];
+            } else {
+                double f[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) f[c] = __dadd_rn(S.tf[(Lp - 1) & 1][lx + EX * ly][c], face[c]);
+                if (top_iface) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = f[c];
+                } else if (MODE == MODE_STEP) {
+                    const double *up = &S.up[ring5(Lp)][(ly * PX + lx) * 3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const int64_t dof = 3 * un_id + c;
+                        double F = 0.0;
+                        if (has_src)
+                            for (int k = 0; k < p.nsrc; ++k)
+                                if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
+                        const double b = __dsub_rn(__dmul_rn(2.0, up[c]), upv[c]);
+                        double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
+                        if ((dm >> c) & 1) un = 0.0;
+                        p.uo[dof] = un;
+                        if (has_rec)
+                            for (int k = 0; k < p.nrec; ++k)
+                                if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) p.fout[3 * un_id + c] = f[c];
+                }
+            }
+        }
+    };
+
+    // ---- epilogue of layer Le: the 4 corner nodes of this thread's face ----
+    auto epilogue = [&](int Le) {
+        ptx::mbar_wait(&S.mbar[mt], phase);
+        phase ^= 1;
+        ptx::tc_fence_after();
+        // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
+        const double alpha = edeg ? 0.0 : -__dmul_rn(c_mat[em].c1, __dmul_rn(es, ISCALE));
+        const uint32_t tb = S.tmem + ((uint32_t)(qd * 32) << 16) + mt * 256 + 24 * hf;
+        double fc[12];                               // [corner][c] of the face
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {             // 4 outputs per round (8 columns per array)
+            uint32_t R0[8], R1[8], R2[8] = {}, R3[8] = {};
+            ptx::tmem_ld8(tb + 0 + rr * 8, R0);
+            ptx::tmem_ld8(tb + 64 + rr * 8, R1);
+            if (NA > 2) ptx::tmem_ld8(tb + 128 + rr * 8, R2);
+            if (NA > 3) ptx::tmem_ld8(tb + 192 + rr * 8, R3);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = 4 * rr + q;
+                const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
+                const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
+                const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
+                const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
+                // D holds −C_j, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^46
+                const double dlo = limb_exact(c0, c1_, c2_, c3);
+                const double dhi = NA > 2 ? limb_exact(c4, c5, c6, c7) : 0.0;
+                const double Y = NA > 2 ? __fma_rn(dhi, 0x1p32, dlo) : dlo;    // RN(−y)
+                const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
+                if (MODE == MODE_DEBUG && edbg) {
+                    const int i = 12 * hf + j;
+                    const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};
+                    __int128 y = 0;
+#pragma unroll
+                    for (int jj = 7; jj >= 0; --jj) y = y * 256 - (__int128)Cj[jj];
+                    if (p.dbg_C)
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) p.dbg_C[edj * 192 + jj * 24 + i] = -Cj[jj];
+                    if (p.dbg_yhi) p.dbg_yhi[edj * 24 + i] = (long long)(y >> 64);
+                    if (p.dbg_ylo) p.dbg_ylo[edj * 24 + i] = (long long)(unsigned long long)y;
+                    if (p.dbg_fe) p.dbg_fe[edj * 24 + i] = f;
+                }
+                fc[j] = f;
+            }
+        }
+        ptx::tc_fence_before();
+        // x-pairs: P(iy) of node (lx, ly) = own (-x,-y) corner + lane lx-1's (+x,-y) corner;
+        // the +y corners give P(iy-1) of node (lx, ly+1), exchanged through smem
+        double(*ys)[EX][3] = S.ysum[ring3(Le)][hf];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double pm = __shfl_up_sync(0xffffffffu, fc[3 * 1 + c], 1);   // (+x,-y) of lx-1
+            const double pp = __shfl_up_sync(0xffffffffu, fc[3 * 2 + c], 1);   // (+x,+y) of lx-1
+            plo[c] = __dadd_rn(fc[3 * 0 + c], pm);
+            ys[ly][lx][c] = __dadd_rn(fc[3 * 3 + c], pp);
+        }
+    };
+
+    // ---- conversion of layer L (this thread's three chunks) and the MMA hand-off ----
+    auto convert = [&](int L) {
+        const int64_t eid = ex + p.nx * (ey + p.ny * (int64_t)L);
+        const int64_t dj = eid - p.dbg_e0;
+        const bool dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < C::TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
+                         dj >= 0 && dj < p.dbg_ne;
+        // s_e from the per-node maxima of the two planes
+        const unsigned long long *m0 = S.nmax[ring5(L)], *m1 = S.nmax[ring5(L + 1)];
+        const int n0 = ly * PX + lx;
+        unsigned long long ab = m0[n0];
+        ab = max(ab, m0[n0 + 1]);
+        ab = max(ab, m0[n0 + PX]);
+        ab = max(ab, m0[n0 + PX + 1]);
+        ab = max(ab, m1[n0]);
+        ab = max(ab, m1[n0 + 1]);
+        ab = max(ab, m1[n0 + PX]);
+        ab = max(ab, m1[n0 + PX + 1]);
+        const double amax = __longlong_as_double((long long)ab);
+        const double cG = c_mat[mcur].cG;
+        const double s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
+        const bool deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
+        const bool vzero = !ein || !(s >= 0x1p-1022);
+        const bool fast = (s <= 0x1.fffffffffffffp1023) && (vzero || s >= 0x1p-960);
+        uint8_t *Ab = &S.A[mt][0][0];
+        const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
+        double ue[16];
+        if (hf == 0) {
+            gather16<0>(ue, S.up[ring5(L)], S.up[ring5(L + 1)], lx, ly);
+            i8w_convert<MODE, M, 0>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
+            if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
+        } else {
+            gather16<1>(ue, S.up[ring5(L)], S.up[ring5(L + 1)], lx, ly);
+            i8w_convert<MODE, M, 1>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
+        }
+        es = s;
+        edeg = deg;
+        em = mcur;
+        edbg = dbg;
+        edj = dj;
+        ptx::fence_proxy_async_smem();
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
+        if ((wu & 7) == 0) {     // first warp of the M-tile; one elected lane issues
+            const int mtu = wu >> 3;
+            if (ptx::elect_one()) {
+                ptx::tc_fence_after();
+                const uint32_t b0 = ptx::smem_u32(&S.B[0]);
+                const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
+                const uint32_t a0 = ptx::smem_u32(&S.A[mtu][0][0]);
+#pragma unroll
+                for (int pa = 0; pa < NA; ++pa) {
+                    const uint32_t abase = a0 + pa * A1_BYTES;
+                    const uint32_t d = S.tmem + mtu * 256 + pa * 64;
+#pragma unroll
+                    for (int ks = 0; ks < 3; ++ks)
+                        ptx::mma_i8(d, ptx::smem_desc(abase + ks * 256, 128, A1_PITCH),
+                                    ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC, ks > 0 ? 1u : 0u);
+                    ptx::mma_i8(d, ptx::smem_desc(abase + 3 * 128, 128, A1_PITCH),
+                                ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
+                    ptx::mma_i8(d, ptx::smem_desc(abase + 5 * 128, 128, A1_PITCH),
+                                ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
+                }
+                ptx::mma_commit(&S.mbar[mtu]);
+            }
+            __syncwarp();
+        }
+    };
+
+    for (int L = Z0 - 1; L <= Z1 + 1; ++L) {
+        // ---- prefetch: plane L+2, material of layer L+2, update operands of the next post plane ----
         const int pz = L + 2;
         const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < nz);
         double pfv[3] = {0.0, 0.0, 0.0};
@@ -258,10 +446,11 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             for (int c = 0; c < 3; ++c) pfv[c] = __ldg(src + c);
         }
         const int mfar = (ein && L + 2 < nz && L >= Lfirst) ? (int)__ldg(matp + mstride * (L + 2)) : kZeroMat;
+        const int Pn = L - mt;                    // plane this thread updates in the next iteration
         double upv_n[3] = {0.0, 0.0, 0.0}, wn_n = 0.0;
         uint8_t dm_n = 0;
-        if (MODE == MODE_STEP && upd_role && L >= Z0 && L <= nz && L < Z1) {
-            const int64_t un_next = ucol + PSTRIDE * L;
+        if (MODE == MODE_STEP && upd_role && Pn >= Z0 && Pn <= nz && Pn < Z1) {
+            const int64_t un_next = ucol + PSTRIDE * Pn;
             upv_n[0] = p.uo[3 * un_next];
             upv_n[1] = p.uo[3 * un_next + 1];
             upv_n[2] = p.uo[3 * un_next + 2];
@@ -269,190 +458,27 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             dm_n = p.dmask ? __ldg(p.dmask + un_next) : (uint8_t)0;
         }
 
-        // ---- 2. integer image of ū_e for layer L (this thread's three chunks), MMA hand-off ----
-        double s = 0.0;
-        int64_t dj = -1;
-        bool dbg = false, deg = false;
-        if (layer_ok) {
-            const int64_t eid = ex + p.nx * (ey + p.ny * (int64_t)L);
-            dj = eid - p.dbg_e0;
-            dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < C::TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
-                  dj >= 0 && dj < p.dbg_ne;
-            // s_e from the per-node maxima of the two planes
-            const unsigned long long *m0 = S.nmax[L & 3], *m1 = S.nmax[(L + 1) & 3];
-            const int n0 = ly * PX + lx;
-            unsigned long long ab = m0[n0];
-            ab = max(ab, m0[n0 + 1]);
-            ab = max(ab, m0[n0 + PX]);
-            ab = max(ab, m0[n0 + PX + 1]);
-            ab = max(ab, m1[n0]);
-            ab = max(ab, m1[n0 + 1]);
-            ab = max(ab, m1[n0 + PX]);
-            ab = max(ab, m1[n0 + PX + 1]);
-            const double amax = __longlong_as_double((long long)ab);
-            const double cG = c_mat[mcur].cG;
-            s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
-            deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
-            const bool vzero = !ein || !(s >= 0x1p-1022);
-            const bool fast = (s <= 0x1.fffffffffffffp1023) && (vzero || s >= 0x1p-960);
-            uint8_t *Ab = &S.A[mt][0][0];
-            const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
-            double ue[16];
-            if (hf == 0) {
-                gather16<0>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
-                i8w_convert<MODE, M, 0>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
-                if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
-            } else {
-                gather16<1>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
-                i8w_convert<MODE, M, 1>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
-            }
-            ptx::fence_proxy_async_smem();
-            asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
-            if ((wu & 7) == 0) {     // first warp of the M-tile; one elected lane issues
-                const int mtu = wu >> 3;
-                if (ptx::elect_one()) {
-                    ptx::tc_fence_after();
-                    const uint32_t b0 = ptx::smem_u32(&S.B[0]);
-                    const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
-                    const uint32_t a0 = ptx::smem_u32(&S.A[mtu][0][0]);
-#pragma unroll
-                    for (int pa = 0; pa < NA; ++pa) {
-                        const uint32_t abase = a0 + pa * A1_BYTES;
-                        const uint32_t d = S.tmem + mtu * 256 + pa * 64;
-#pragma unroll
-                        for (int ks = 0; ks < 3; ++ks)
-                            ptx::mma_i8(d, ptx::smem_desc(abase + ks * 256, 128, A1_PITCH),
-                                        ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC, ks > 0 ? 1u : 0u);
-                        ptx::mma_i8(d, ptx::smem_desc(abase + 3 * 128, 128, A1_PITCH),
-                                    ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
-                        ptx::mma_i8(d, ptx::smem_desc(abase + 5 * 128, 128, A1_PITCH),
-                                    ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
-                    }
-                    ptx::mma_commit(&S.mbar[mtu]);
-                }
-                __syncwarp();
-            }
+        if (mt == 0) {
+            if (layer_ok(L)) convert(L);
+            post_phase(L - 1);
+            if (layer_ok(L)) epilogue(L);
+        } else {
+            post_phase(L - 2);
+            if (layer_ok(L - 1)) epilogue(L - 1);
+            if (layer_ok(L)) convert(L);
         }
 
-        // ---- 3. (overlaps the MMAs) post-phase of layer Ld = L-1: face sums, f_n = T + B, update ----
-        if (tnode) {
-            const bool bot_iface = (p.slab_flags & 1) && Ld == 0;
-            const bool top_iface = (p.slab_flags & 2) && Ld == nz;
-            double face[3] = {0.0, 0.0, 0.0};
-            if (prev_layer) {
-                const double(*ys)[EX][3] = S.ysum[Ld & 1][hf];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) face[c] = __dadd_rn(plo[c], ys[ly - 1][lx][c]);   // P(iy) + P(iy-1)
-            }
-            if (hf == 1) {        // top face of layer Ld: T of plane Ld+1
-#pragma unroll
-                for (int c = 0; c < 3; ++c) S.tf[Ld & 1][lx + EX * ly][c] = face[c];
-            } else if (own && plane_done) {
-                const int64_t un_id = ucol + PSTRIDE * Ld;
-                if (bot_iface) {  // interface plane: B waits for T from the rank below
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) p.iface_bot_b[3 * ucol + c] = face[c];
-                } else {
-                    double f[3];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) f[c] = __dadd_rn(S.tf[(Ld - 1) & 1][lx + EX * ly][c], face[c]);
-                    if (top_iface) {
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = f[c];
-                    } else if (MODE == MODE_STEP) {
-                        const double *up = &S.up[Ld & 3][(ly * PX + lx) * 3];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            const int64_t dof = 3 * un_id + c;
-                            double F = 0.0;
-                            if (has_src)
-                                for (int k = 0; k < p.nsrc; ++k)
-                                    if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
-                            const double b = __dsub_rn(__dmul_rn(2.0, up[c]), upv[c]);
-                            double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
-                            if ((dm >> c) & 1) un = 0.0;
-                            p.uo[dof] = un;
-                            if (has_rec)
-                                for (int k = 0; k < p.nrec; ++k)
-                                    if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
-                        }
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) p.fout[3 * un_id + c] = f[c];
-                    }
-                }
-            }
-        }
-
-        // ---- 4. epilogue of layer L: the 4 corner nodes of this thread's face ----
-        if (layer_ok) {
-            ptx::mbar_wait(&S.mbar[mt], phase);
-            phase ^= 1;
-            ptx::tc_fence_after();
-            // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
-            const double alpha = deg ? 0.0 : -__dmul_rn(c_mat[mcur].c1, __dmul_rn(s, ISCALE));
-            const uint32_t tb = S.tmem + ((uint32_t)(qd * 32) << 16) + mt * 256 + 24 * hf;
-            double fc[12];                               // [corner][c] of the face
-#pragma unroll
-            for (int rr = 0; rr < 3; ++rr) {             // 4 outputs per round (8 columns per array)
-                uint32_t R0[8], R1[8], R2[8] = {}, R3[8] = {};
-                ptx::tmem_ld8(tb + 0 + rr * 8, R0);
-                ptx::tmem_ld8(tb + 64 + rr * 8, R1);
-                if (NA > 2) ptx::tmem_ld8(tb + 128 + rr * 8, R2);
-                if (NA > 3) ptx::tmem_ld8(tb + 192 + rr * 8, R3);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int j = 4 * rr + q;
-                    const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
-                    const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
-                    const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
-                    const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
-                    // D holds −C_j, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^46
-                    const double dlo = limb_exact(c0, c1_, c2_, c3);
-                    const double dhi = NA > 2 ? limb_exact(c4, c5, c6, c7) : 0.0;
-                    const double Y = NA > 2 ? __fma_rn(dhi, 0x1p32, dlo) : dlo;    // RN(−y)
-                    const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
-                    if (MODE == MODE_DEBUG && dbg) {
-                        const int i = 12 * hf + j;
-                        const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};
-                        __int128 y = 0;
-#pragma unroll
-                        for (int jj = 7; jj >= 0; --jj) y = y * 256 - (__int128)Cj[jj];
-                        if (p.dbg_C)
-#pragma unroll
-                            for (int jj = 0; jj < 8; ++jj) p.dbg_C[dj * 192 + jj * 24 + i] = -Cj[jj];
-                        if (p.dbg_yhi) p.dbg_yhi[dj * 24 + i] = (long long)(y >> 64);
-                        if (p.dbg_ylo) p.dbg_ylo[dj * 24 + i] = (long long)(unsigned long long)y;
-                        if (p.dbg_fe) p.dbg_fe[dj * 24 + i] = f;
-                    }
-                    fc[j] = f;
-                }
-            }
-            ptx::tc_fence_before();
-            // x-pairs: P(iy) of node (lx, ly) = own (-x,-y) corner + lane lx-1's (+x,-y) corner;
-            // the +y corners give P(iy-1) of node (lx, ly+1), exchanged through smem
-            double(*ys)[EX][3] = S.ysum[L & 1][hf];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const double pm = __shfl_up_sync(0xffffffffu, fc[3 * 1 + c], 1);   // (+x,-y) of lx-1
-                const double pp = __shfl_up_sync(0xffffffffu, fc[3 * 2 + c], 1);   // (+x,+y) of lx-1
-                plo[c] = __dadd_rn(fc[3 * 0 + c], pm);
-                ys[ly][lx][c] = __dadd_rn(fc[3 * 3 + c], pp);
-            }
-        }
-        // ---- park plane L+2 (slot of plane L-2, no longer read) with its node maxima ----
+        // ---- park plane L+2 (slot of plane L-3, no longer read) with its node maxima ----
         if (pf && lrole) {
             unsigned long long m = 0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                S.up[pz & 3][3 * li + c] = pfv[c];
+                S.up[ring5(pz)][3 * li + c] = pfv[c];
                 const unsigned long long b = abs_bits(pfv[c]);
                 m = b > m ? b : m;
             }
-            S.nmax[pz & 3][li] = m;
+            S.nmax[ring5(pz)][li] = m;
         }
-        prev_layer = layer_ok;
         if (L >= Lfirst) {
             mcur = mnxt;
             mnxt = mfar;
