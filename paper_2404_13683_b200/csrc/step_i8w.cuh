@@ -65,35 +65,26 @@ __device__ __forceinline__ void gather16(double (&ue)[16], const double *lo, con
     }
 }
 
-template <int MODE, int M, int HF>
-__device__ __forceinline__ void i8w_convert(const StepParams &p, const double (&ue)[16], double cG, double s,
-                                            bool deg, bool vzero, bool fast, uint8_t *Ab, uint32_t rowoff,
-                                            bool dbg, int64_t dj) {
+template <int MODE, int M, int HF, bool FAST>
+__device__ __forceinline__ void i8w_chunks(const StepParams &p, const double (&ue)[16], double cG, double r, double R,
+                                           bool deg, uint8_t *Ab, uint32_t rowoff, bool dbg, int64_t dj) {
     constexpr int NB = (7 * M + 1 + 7) / 8;
     constexpr int NA = (NB + 1) / 2;
     constexpr double SCALE = (double)(1ull << (7 * M));
     constexpr unsigned long long AOFF = 1ull << (7 * M);
-    const double r = 1.0 / s;                                  // RN(1/s_e), reading Q7
-    const double R = vzero ? 0.0 : __dmul_rn(r, SCALE);        // exact power-of-two scaling
-    const bool wfast = __all_sync(0xffffffffu, fast);
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
         const int ch = HF == 0 ? (cc == 2 ? 3 : cc) : (cc == 0 ? 2 : cc + 3);
         const bool gpart = ch >= 3;
         const int j0 = 8 * (gpart ? ch - 3 : ch) - 8 * HF;     // index into ue of value 0 of the chunk
         long long v[8];
-        if (wfast) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const double ub = gpart ? __dmul_rn(cG, ue[j0 + q]) : ue[j0 + q];
+        for (int q = 0; q < 8; ++q) {
+            const double ub = gpart ? __dmul_rn(cG, ue[j0 + q]) : ue[j0 + q];
+            if (FAST)   // one DMUL + one F2I per value (R = RN(1/s)·2^{7M}, or 0 for a zero image)
                 v[q] = __double2ll_rz(__dmul_rn(ub, R));
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const double ub = gpart ? __dmul_rn(cG, ue[j0 + q]) : ue[j0 + q];
+            else        // tiny-normal or non-finite s: the two roundings of Eq. 10 as written
                 v[q] = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), SCALE));
-            }
         }
         uint32_t lo[8], hi[8];
 #pragma unroll
@@ -129,12 +120,25 @@ __device__ __forceinline__ void i8w_convert(const StepParams &p, const double (&
     }
 }
 
+template <int MODE, int M, int HF>
+__device__ __forceinline__ void i8w_convert(const StepParams &p, const double (&ue)[16], double cG, double s,
+                                            bool deg, bool vzero, bool fast, uint8_t *Ab, uint32_t rowoff,
+                                            bool dbg, int64_t dj) {
+    constexpr double SCALE = (double)(1ull << (7 * M));
+    const double r = 1.0 / s;                                  // RN(1/s_e), reading Q7
+    const double R = vzero ? 0.0 : __dmul_rn(r, SCALE);        // exact power-of-two scaling
+    if (__all_sync(0xffffffffu, fast))
+        i8w_chunks<MODE, M, HF, true>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj);
+    else
+        i8w_chunks<MODE, M, HF, false>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj);
+}
+
 __device__ __forceinline__ int ring5(int x) { return (x + 10) % 5; }   // x >= -10
 __device__ __forceinline__ int ring3(int x) { return (x + 9) % 3; }    // x >= -9
 
-// Skewed M-tiles: in iteration L (one CTA barrier at its end)
-//   M-tile 0: convert(L) -> MMA(L) | post-phase(L-1) | epilogue(L)
-//   M-tile 1: post-phase(L-2) | epilogue(L-1) | convert(L) -> MMA(L)   (its MMAs run across the barrier)
+// Skewed M-tiles: iteration L = half-iterations 2L, 2L+1 (one CTA barrier at its end)
+//   M-tile 0: [convert(L) -> MMA(L)] | [post-phase(L-1), epilogue(L)]
+//   M-tile 1: [post-phase(L-2), epilogue(L-1)] | [convert(L) -> MMA(L)]   (its MMAs run across the barrier)
 // so one M-tile's conversion (F2I / FP64 heavy) overlaps the other's epilogue (integer heavy) and the
 // tensor core work of the two M-tiles is spread over the iteration.  Node row 4 (M-tile 1) reads the
 // x-pairs of element row 3 (M-tile 0) one iteration after they were written.
@@ -435,60 +439,69 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         }
     };
 
-    for (int L = Z0 - 1; L <= Z1 + 1; ++L) {
-        // ---- prefetch: plane L+2, material of layer L+2, update operands of the next post plane ----
-        const int pz = L + 2;
-        const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < nz);
-        double pfv[3] = {0.0, 0.0, 0.0};
-        if (pf && ldn) {
-            const double *src = p.u + 3 * PSTRIDE * pz + ldoff;
+    // half-iterations: h = 2L (even) and 2L+1 (odd); one copy of each phase body, selected per M-tile
+    double pfv[3] = {0.0, 0.0, 0.0};
+    bool pf = false;
+    int mfar = kZeroMat;
+    double upv_n[3] = {0.0, 0.0, 0.0}, wn_n = 0.0;
+    uint8_t dm_n = 0;
+    for (int h = 2 * (Z0 - 1); h <= 2 * (Z1 + 1) + 1; ++h) {
+        const int L = h >> 1;
+        const bool odd = h & 1;
+        if (!odd) {
+            // ---- prefetch: plane L+2, material of layer L+2, update operands of the next post plane ----
+            const int pz = L + 2;
+            pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < nz);
+            if (pf && ldn) {
+                const double *src = p.u + 3 * PSTRIDE * pz + ldoff;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) pfv[c] = __ldg(src + c);
-        }
-        const int mfar = (ein && L + 2 < nz && L >= Lfirst) ? (int)__ldg(matp + mstride * (L + 2)) : kZeroMat;
-        const int Pn = L - mt;                    // plane this thread updates in the next iteration
-        double upv_n[3] = {0.0, 0.0, 0.0}, wn_n = 0.0;
-        uint8_t dm_n = 0;
-        if (MODE == MODE_STEP && upd_role && Pn >= Z0 && Pn <= nz && Pn < Z1) {
-            const int64_t un_next = ucol + PSTRIDE * Pn;
-            upv_n[0] = p.uo[3 * un_next];
-            upv_n[1] = p.uo[3 * un_next + 1];
-            upv_n[2] = p.uo[3 * un_next + 2];
-            wn_n = __ldg(p.w + un_next);
-            dm_n = p.dmask ? __ldg(p.dmask + un_next) : (uint8_t)0;
-        }
-
-        if (mt == 0) {
-            if (layer_ok(L)) convert(L);
-            post_phase(L - 1);
-            if (layer_ok(L)) epilogue(L);
-        } else {
-            post_phase(L - 2);
-            if (layer_ok(L - 1)) epilogue(L - 1);
-            if (layer_ok(L)) convert(L);
-        }
-
-        // ---- park plane L+2 (slot of plane L-3, no longer read) with its node maxima ----
-        if (pf && lrole) {
-            unsigned long long m = 0;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                S.up[ring5(pz)][3 * li + c] = pfv[c];
-                const unsigned long long b = abs_bits(pfv[c]);
-                m = b > m ? b : m;
+                for (int c = 0; c < 3; ++c) pfv[c] = __ldg(src + c);
             }
-            S.nmax[ring5(pz)][li] = m;
+            mfar = (ein && L + 2 < nz && L >= Lfirst) ? (int)__ldg(matp + mstride * (L + 2)) : kZeroMat;
+            const int Pn = L - mt;                    // plane this thread updates in the next iteration
+            if (MODE == MODE_STEP && upd_role && Pn >= Z0 && Pn <= nz && Pn < Z1) {
+                const int64_t un_next = ucol + PSTRIDE * Pn;
+                upv_n[0] = p.uo[3 * un_next];
+                upv_n[1] = p.uo[3 * un_next + 1];
+                upv_n[2] = p.uo[3 * un_next + 2];
+                wn_n = __ldg(p.w + un_next);
+                dm_n = p.dmask ? __ldg(p.dmask + un_next) : (uint8_t)0;
+            }
         }
-        if (L >= Lfirst) {
-            mcur = mnxt;
-            mnxt = mfar;
+        // M-tile 0: convert at even h, post-phase + epilogue at odd h; M-tile 1 the other way round
+        if (odd == (mt == 1)) {
+            if (layer_ok(L)) convert(L);
+        } else {
+            post_phase(L - 1 - mt);
+            if (layer_ok(L - mt)) epilogue(L - mt);
         }
-        upv[0] = upv_n[0];
-        upv[1] = upv_n[1];
-        upv[2] = upv_n[2];
-        wn = wn_n;
-        dm = dm_n;
-        __syncthreads();
+        if (odd) {
+            // ---- park plane L+2 (slot of plane L-3, no longer read) with its node maxima ----
+            const int pz = L + 2;
+            if (pf && lrole) {
+                unsigned long long m = 0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    S.up[ring5(pz)][3 * li + c] = pfv[c];
+                    const unsigned long long b = abs_bits(pfv[c]);
+                    m = b > m ? b : m;
+                }
+                S.nmax[ring5(pz)][li] = m;
+            }
+            if (L >= Lfirst) {
+                mcur = mnxt;
+                mnxt = mfar;
+            }
+            upv[0] = upv_n[0];
+            upv[1] = upv_n[1];
+            upv[2] = upv_n[2];
+            wn = wn_n;
+            dm = dm_n;
+            upv_n[0] = upv_n[1] = upv_n[2] = 0.0;
+            wn_n = 0.0;
+            dm_n = 0;
+            __syncthreads();
+        }
     }
     ptx::tc_fence_after();
     if (warp == 0) ptx::tmem_dealloc<C::TMEM_COLS>(S.tmem);
