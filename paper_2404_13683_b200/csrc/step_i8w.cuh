@@ -49,6 +49,7 @@ struct SmemI8W {
     unsigned long long nmax[5][I8W::NODES];         // max_c |u_c| of each node (bit patterns)
     double ysum[3][2][I8W::EY][EX][3];              // [layer mod 3][face] x-pair P of the +y corners
     double tf[2][I8W::NE][3];                       // [layer parity][tile node] top-face sums T
+    double2 mc[kMaxMat];                            // (cG, c1) per material, staged from c_mat
     uint64_t mbar[I8W::MT];
     uint32_t tmem;
 };
@@ -228,6 +229,10 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     if (t == 0)
         for (int mm = 0; mm < C::MT; ++mm) ptx::mbar_init(&S.mbar[mm], 1);
     for (int i = t; i < 2 * C::NE * 3; i += NT) (&S.tf[0][0][0])[i] = 0.0;
+    for (int i = t; i < p.nmat + 1; i += NT) {      // a per-lane indexed constant-bank load serialises
+        const int id = i < p.nmat ? i : kZeroMat;
+        S.mc[id] = make_double2(c_mat[id].cG, c_mat[id].c1);
+    }
     for (int j = 0; j < 2; ++j) {
         const int iz = Lfirst + j;
         if (lrole) {
@@ -320,7 +325,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         phase ^= 1;
         ptx::tc_fence_after();
         // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
-        const double alpha = edeg ? 0.0 : -__dmul_rn(c_mat[em].c1, __dmul_rn(es, ISCALE));
+        const double alpha = edeg ? 0.0 : -__dmul_rn(S.mc[em].y, __dmul_rn(es, ISCALE));
         const uint32_t tb = S.tmem + ((uint32_t)(qd * 32) << 16) + mt * 256 + 24 * hf;
         double fc[12];                               // [corner][c] of the face
 #pragma unroll
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         ab = max(ab, m1[n0 + PX]);
         ab = max(ab, m1[n0 + PX + 1]);
         const double amax = __longlong_as_double((long long)ab);
-        const double cG = c_mat[mcur].cG;
+        const double cG = S.mc[mcur].x;
         const double s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
         const bool deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
         const bool vzero = !ein || !(s >= 0x1p-1022);
