@@ -58,7 +58,7 @@ def lib() -> ctypes.CDLL:
                                  _i32p, _i32p, _i8p, _int, _int, _dp, _dp]
     L.oracle_run.argtypes = [_i64, _i64, _i64, _d, _u8p, _dp, _dp, _dp, _u8p,
                              _int, _i32p, _i32p, _i8p, _int, _int,
-                             _int, _i64p, _i32p, _i64, _dp, _dp, _dp, _i64p, _i64]
+                             _int, _i64p, _i32p, _i64, _dp, _d, _d, _d, _dp, _dp, _i64p, _i64]
     L.oracle_run.restype = _int
     L.oracle_element_nodes.argtypes = [_i64, _i64, _i64, _i64p]
     L.oracle_digits.argtypes = [_i64, _int, _int, _i32p]
@@ -159,7 +159,8 @@ def run(model, u, u_prev, it: int, nsteps: int, path=PATH_FP64, M=8, digits=DIGI
     """Advance (u, u_prev, it) by nsteps with the model dict produced by workloads.
 
     model keys: nx, ny, nz, ds, mat (uint8 per element), rho/kappa/G (per material),
-    dt, dirichlet (uint8 per node or None), src_node, src_axis, amp (nsrc × n_t).
+    dt, dirichlet (uint8 per node or None), src_node, src_axis, amp (nsrc × n_t),
+    alpha, beta (Rayleigh damping C = alpha M + beta K, reading R1; default 0).
     Returns (u, u_prev, it, status) with new arrays (inputs are not modified).
     """
     K8, Kk, Kg = int_matrices()
@@ -181,5 +182,6 @@ def run(model, u, u_prev, it: int, nsteps: int, path=PATH_FP64, M=8, digits=DIGI
                           None if dm is None else _p(dm, _u8p),
                           path, _p(Kk, _i32p), _p(Kg, _i32p), _p(K8, _i8p), M, digits,
                           len(src_node), _p(src_node, _i64p), _p(src_axis, _i32p), n_t,
-                          _p(amp, _dp), _p(u, _dp), _p(up, _dp), _p(itp, _i64p), nsteps)
+                          _p(amp, _dp), float(model["dt"]), float(model.get("alpha", 0.0)),
+                          float(model.get("beta", 0.0)), _p(u, _dp), _p(up, _dp), _p(itp, _i64p), nsteps)
     return u, up, int(itp[0]), st

@@ -252,6 +252,13 @@ void oracle_apply_K(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t
 /* Central-difference time stepping (Eq. 3, update L263-L266 with the
  * sign of Eq. 3: F − K u, reading Q14):
  *   u^{it+1} = fma(w, F^{it} − f, 2 u^{it} − u^{it−1}),  f = K u^{it},  w = dt²/m
+ * Rayleigh damping ("Rayleigh damping (100–125 kHz) is used"; reading R1,
+ * the SPEC's backward-difference velocity v = (u − u_prev)/dt so the update stays explicit),
+ * one (alpha, beta) for the model, C = alpha M + beta K:
+ *   u^{it+1} = 2u − u_prev + dt² M⁻¹ (F − K u − C v)
+ *            = fma(w, F − K ũ, (2u − u_prev) − ca·d),  d = u − u_prev,
+ *   ũ = u + cb·d,  ca = alpha·dt,  cb = beta/dt   (each operation rounded once, in this order).
+ * alpha = beta = 0 takes the undamped branch (identical results).
  * Dirichlet: bit a of dmask[n] set -> component a forced to 0 after the update.
  * Sources: src_node[k], src_axis[k], amplitude amp[k*n_t + it] (0 beyond n_t).
  * u and u_prev are advanced in place; *it is incremented per step.
@@ -260,19 +267,35 @@ int oracle_run(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat
                const double *kappa, const double *G, const double *w, const uint8_t *dmask,
                int path, const int32_t *Kk, const int32_t *Kg, const int8_t *K8, int M, int digits,
                int nsrc, const int64_t *src_node, const int32_t *src_axis, int64_t n_t,
-               const double *amp, double *u, double *u_prev, int64_t *it, int64_t nsteps) {
+               const double *amp, double dt, double alpha, double beta,
+               double *u, double *u_prev, int64_t *it, int64_t nsteps) {
     int64_t nn = (nx + 1) * (ny + 1) * (nz + 1);
     double *f = (double *)malloc(sizeof(double) * 3 * (size_t)nn);
     double *F = (double *)calloc(3 * (size_t)nn, sizeof(double));
+    int damped = (alpha != 0.0 || beta != 0.0);
+    double ca = alpha * dt, cb = beta / dt;
+    double *ut = damped ? (double *)malloc(sizeof(double) * 3 * (size_t)nn) : NULL;
     int status = 0;
     for (int64_t step = 0; step < nsteps; ++step) {
-        oracle_apply_K(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, u, f);
+        if (damped) {
+            for (int64_t i = 0; i < 3 * nn; ++i) {
+                double d = u[i] - u_prev[i];
+                ut[i] = u[i] + cb * d;
+            }
+            oracle_apply_K(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, ut, f);
+        } else {
+            oracle_apply_K(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, u, f);
+        }
         for (int k = 0; k < nsrc; ++k)
             F[3 * src_node[k] + src_axis[k]] += (*it < n_t) ? amp[(int64_t)k * n_t + *it] : 0.0;
         for (int64_t n = 0; n < nn; ++n) {
             for (int c = 0; c < 3; ++c) {
                 int64_t i = 3 * n + c;
                 double b = 2.0 * u[i] - u_prev[i];
+                if (damped) {
+                    double d = u[i] - u_prev[i];
+                    b = b - ca * d;
+                }
                 double un = fma(w[n], F[i] - f[i], b);
                 if (dmask && (dmask[n] >> c) & 1) un = 0.0;
                 if (!isfinite(un)) status = 3;
@@ -286,6 +309,7 @@ int oracle_run(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat
     }
     free(f);
     free(F);
+    free(ut);
     return status;
 }
 

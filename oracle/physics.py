@@ -43,6 +43,25 @@ def mode_amplitude(lam: float, dt: float, n: int, a0: float = 1.0, am1: float | 
     return a0 * math.cos(n * th) + B * math.sin(n * th)
 
 
+def mode_amplitude_damped(lam: float, dt: float, alpha: float, beta: float, n: int) -> float:
+    """Closed-form a_n of the Rayleigh-damped modal recurrence (reading R1, backward-difference
+    velocity): a_{n+1} = p a_n − q a_{n−1}, p = 2 − α dt − λ dt² − β λ dt, q = 1 − α dt − β λ dt,
+    a_0 = a_{−1} = 1; a_n = A r1^n + B r2^n with r1, r2 the roots of r² − p r + q = 0."""
+    p = 2.0 - alpha * dt - lam * dt * dt - beta * lam * dt
+    q = 1.0 - alpha * dt - beta * lam * dt
+    disc = complex(p * p - 4.0 * q) ** 0.5
+    r1, r2 = (p + disc) / 2.0, (p - disc) / 2.0
+    # A + B = 1,  A/r1 + B/r2 = 1
+    B = (1.0 - 1.0 / r1) / (1.0 / r2 - 1.0 / r1)
+    A = 1.0 - B
+    return (A * r1 ** n + B * r2 ** n).real
+
+
+def rayleigh_zeta(alpha: float, beta: float, w: float) -> float:
+    """Modal damping ratio of C = αM + βK at angular frequency w (continuous time)."""
+    return alpha / (2.0 * w) + beta * w / 2.0
+
+
 def leapfrog_energy(K, m_diag, u_n, u_np1, dt) -> float:
     v = (u_np1 - u_n) / dt
     return 0.5 * float(v @ (m_diag * v)) + 0.5 * float(u_n @ (K @ u_np1))

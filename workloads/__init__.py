@@ -52,6 +52,8 @@ class Model:
     src_axis: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
     amp: np.ndarray = field(default_factory=lambda: np.zeros((0, 1)))
     steps: int = 0
+    alpha: float = 0.0       # Rayleigh damping C = alpha M + beta K (reading R1); 0 = undamped
+    beta: float = 0.0
 
     @property
     def n_nodes(self) -> int:
@@ -67,7 +69,17 @@ class Model:
     def as_dict(self) -> dict:
         return dict(nx=self.nx, ny=self.ny, nz=self.nz, ds=self.ds, rho=self.rho, kappa=self.kappa,
                     G=self.G, mat=self.mat, dt=self.dt, dirichlet=self.dirichlet,
-                    src_node=self.src_node, src_axis=self.src_axis, amp=self.amp)
+                    src_node=self.src_node, src_axis=self.src_axis, amp=self.amp,
+                    alpha=self.alpha, beta=self.beta)
+
+
+def rayleigh_coeffs(f1: float, f2: float, zeta: float) -> tuple[float, float]:
+    """Two-point Rayleigh fit (SPEC rayleigh_coeffs; "Rayleigh damping (100--125 kHz)"):
+    modal damping ratio zeta(w) = alpha/(2w) + beta w/2 equal to zeta at w1 = 2 pi f1, w2 = 2 pi f2."""
+    if not 0 < f1 < f2 or zeta < 0:
+        raise ValueError("need 0 < f1 < f2 and zeta >= 0")
+    w1, w2 = 2 * math.pi * f1, 2 * math.pi * f2
+    return 2 * zeta * w1 * w2 / (w1 + w2), 2 * zeta / (w1 + w2)
 
 
 def _materials(*specs):
