@@ -85,6 +85,14 @@ ovx_status ovx_set_element_materials(ovx_ctx *ctx, const uint8_t *mat);
 ovx_status ovx_set_dirichlet(ovx_ctx *ctx, const uint8_t *mask);
 /* Time step dt > 0 (Eq. 3). */
 ovx_status ovx_set_dt(ovx_ctx *ctx, double dt);
+/* Rayleigh damping C = alpha·M + beta·K ("Rayleigh damping (100--125 kHz) is
+ * used"; coefficients and discretisation unstated — DESIGN.md reading R1): one (alpha, beta) for
+ * the model, both finite and >= 0; (0, 0) (the default) is the undamped Eq. 3.  ovx_step then
+ * advances u^{it+1} = fma(w, F − K ũ, (2u − u_prev) − RN(alpha·dt)·(u − u_prev)) with the EBE
+ * input ũ = u + RN(beta/dt)·(u − u_prev) (backward-difference velocity, explicit).  Allocates a
+ * third state buffer (24 B/node).  Not available on z-slab contexts (OVX_ESTATE).
+ * ovx_apply_K is unaffected (it computes K u). */
+ovx_status ovx_set_damping(ovx_ctx *ctx, double alpha, double beta);
 /* Derive K_e^INT8 on the host in exact rational arithmetic,
  * check that all 1152 entries are integers in [-128,127] (L110; else OVX_EINVAL),
  * build per-material constants and the per-node w = dt²/m (Eq. 6, m_n = Σ ρ_e ds³/8).

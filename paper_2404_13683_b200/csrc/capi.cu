@@ -28,6 +28,8 @@ struct ovx_ctx {
     int path = OVX_INT8, stages = 8;
     uint8_t *d_mat = nullptr, *d_mask = nullptr;
     double *d_u = nullptr, *d_up = nullptr, *d_w = nullptr;
+    double alpha = 0, beta = 0;       // Rayleigh damping (reading R1)
+    double *d_un = nullptr;           // third state buffer of damped steps
     int8_t k8[1152];
     double Ak[576], Ag[576], Kk[576], Kg[576];
     std::vector<MatConst> mc;
@@ -167,6 +169,7 @@ ovx_status ovx_destroy(ovx_ctx *ctx) {
     dfree(ctx->d_mask);
     dfree(ctx->d_u);
     dfree(ctx->d_up);
+    dfree(ctx->d_un);
     dfree(ctx->d_w);
     dfree(ctx->d_mat_below);
     dfree(ctx->d_bot_b);
@@ -207,10 +210,12 @@ ovx_status ovx_set_grid(ovx_ctx *ctx, int64_t nx, int64_t ny, int64_t nz, double
     dfree(ctx->d_mask);
     dfree(ctx->d_u);
     dfree(ctx->d_up);
+    dfree(ctx->d_un);
     dfree(ctx->d_w);
     ctx->d_mat = nullptr;
     ctx->d_mask = nullptr;
-    ctx->d_u = ctx->d_up = ctx->d_w = nullptr;
+    ctx->d_u = ctx->d_up = ctx->d_w = ctx->d_un = nullptr;
+    ctx->alpha = ctx->beta = 0.0;
     dfree(ctx->d_mat_below);
     dfree(ctx->d_bot_b);
     ctx->d_mat_below = nullptr;
@@ -440,9 +445,16 @@ ovx_status ovx_step(ovx_ctx *ctx, int64_t n) {
     }
     CK(cudaEventRecord(ev.a, ctx->stream));
     StepParams p = base_params(ctx);
+    const bool damped = ctx->alpha != 0.0 || ctx->beta != 0.0;
+    if (damped) {
+        p.damped = 1;
+        p.ca = ctx->alpha * ctx->dt;   // RN(alpha·dt), RN(beta/dt): the oracle's roundings
+        p.cb = ctx->beta / ctx->dt;
+    }
     for (int64_t k = 0; k < n; ++k) {
         p.u = ctx->d_u;
         p.uo = ctx->d_up;
+        p.un = damped ? ctx->d_un : nullptr;
         p.nsrc = ctx->nsrc;
         for (int q = 0; q < ctx->nsrc; ++q) {
             p.src_dof[q] = 3 * ctx->src_node[q] + ctx->src_axis[q];
@@ -450,7 +462,14 @@ ovx_status ovx_step(ovx_ctx *ctx, int64_t n) {
         }
         fill_receivers(ctx, p);
         CK(launch_step(ctx->path, MODE_STEP, p, ctx->stream));
-        std::swap(ctx->d_u, ctx->d_up);
+        if (damped) {            // (u_prev, u, u_next) <- (u, u_next, u_prev)
+            double *old_up = ctx->d_up;
+            ctx->d_up = ctx->d_u;
+            ctx->d_u = ctx->d_un;
+            ctx->d_un = old_up;
+        } else {
+            std::swap(ctx->d_u, ctx->d_up);
+        }
         ctx->it += 1;
         ctx->launches += 1;
     }
@@ -459,8 +478,29 @@ ovx_status ovx_step(ovx_ctx *ctx, int64_t n) {
     return OVX_OK;
 }
 
+ovx_status ovx_set_damping(ovx_ctx *ctx, double alpha, double beta) {
+    if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
+    if (!ctx->have_grid) return fail(ctx, OVX_ESTATE, "set the grid first");
+    if (!(alpha >= 0) || !(beta >= 0) || !std::isfinite(alpha) || !std::isfinite(beta))
+        return fail(ctx, OVX_EINVAL, "Rayleigh coefficients must be finite and >= 0");
+    if (ctx->slab_flags && (alpha != 0.0 || beta != 0.0))
+        return fail(ctx, OVX_ESTATE, "damping is not supported on z-slab contexts");
+    cudaSetDevice(ctx->device);
+    if ((alpha != 0.0 || beta != 0.0) && !ctx->d_un) {
+        if (cudaMalloc(&ctx->d_un, 24 * ctx->nn()) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, OVX_ENOMEM, "device allocation failed for the third state buffer");
+        }
+    }
+    ctx->alpha = alpha;
+    ctx->beta = beta;
+    return OVX_OK;
+}
+
 ovx_status ovx_set_slab(ovx_ctx *ctx, int flags, const uint8_t *mat_below) {
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
+    if (flags && (ctx->alpha != 0.0 || ctx->beta != 0.0))
+        return fail(ctx, OVX_ESTATE, "damping is not supported on z-slab contexts");
     if (!ctx->have_grid || ctx->nmat == 0) return fail(ctx, OVX_ESTATE, "set grid and materials first");
     if (flags < 0 || flags > 3) return fail(ctx, OVX_EINVAL, "slab flags must be in 0..3");
     if ((flags & 1) && !mat_below) return fail(ctx, OVX_EINVAL, "a lower neighbour needs the halo materials");

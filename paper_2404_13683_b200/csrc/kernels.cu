@@ -161,59 +161,62 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 
 #include "step_i8w.cuh"
 
-template <int MODE, int M>
+template <int MODE, int M, bool DAMP>
 cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
     const int smem = (int)sizeof(SmemI8W);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_i8w<MODE, M><<<(unsigned)ctas, I8W::NT, smem, st>>>(p);
+    step_i8w<MODE, M, DAMP><<<(unsigned)ctas, I8W::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
 template <int M>
 cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
-    if (mode == MODE_STEP) return launch_i8w<MODE_STEP, M>(p, ctas, st);
-    if (mode == MODE_APPLY) return launch_i8w<MODE_APPLY, M>(p, ctas, st);
-    return launch_i8w<MODE_DEBUG, M>(p, ctas, st);
+    if (mode == MODE_STEP)
+        return p.damped ? launch_i8w<MODE_STEP, M, true>(p, ctas, st) : launch_i8w<MODE_STEP, M, false>(p, ctas, st);
+    if (mode == MODE_APPLY) return launch_i8w<MODE_APPLY, M, false>(p, ctas, st);
+    return launch_i8w<MODE_DEBUG, M, false>(p, ctas, st);
 }
 
-template <int PATH, int MODE>
+template <int PATH, int MODE, bool DAMP = false>
 cudaError_t launch_t(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
     const int smem = (int)sizeof(SmemV1<PATH>);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_v1<PATH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_v1<PATH, MODE, DAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_v1<PATH, MODE><<<(unsigned)ctas, V1<PATH>::NT, smem, st>>>(p);
+    step_v1<PATH, MODE, DAMP><<<(unsigned)ctas, V1<PATH>::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-template <int MODE>
+template <int MODE, bool DAMP>
 cudaError_t launch_f64(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
     const int smem = (int)sizeof(SmemF2);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_f64<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_f64<MODE, DAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_f64<MODE><<<(unsigned)ctas, F2::NT, smem, st>>>(p);
+    step_f64<MODE, DAMP><<<(unsigned)ctas, F2::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
 template <int PATH>
 cudaError_t launch_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
     if constexpr (PATH == OVX_FP64) {   // dedicated shuffle/register kernel; debug records via step_v1
-        if (mode == MODE_STEP && p.slab_flags == 0) return launch_f64<MODE_STEP>(p, ctas, st);
-        if (mode == MODE_APPLY) return launch_f64<MODE_APPLY>(p, ctas, st);
+        if (mode == MODE_STEP && p.slab_flags == 0)
+            return p.damped ? launch_f64<MODE_STEP, true>(p, ctas, st) : launch_f64<MODE_STEP, false>(p, ctas, st);
+        if (mode == MODE_APPLY) return launch_f64<MODE_APPLY, false>(p, ctas, st);
     }
-    if (mode == MODE_STEP) return launch_t<PATH, MODE_STEP>(p, ctas, st);
+    if (mode == MODE_STEP)
+        return p.damped ? launch_t<PATH, MODE_STEP, true>(p, ctas, st) : launch_t<PATH, MODE_STEP, false>(p, ctas, st);
     if (mode == MODE_APPLY) return launch_t<PATH, MODE_APPLY>(p, ctas, st);
     return launch_t<PATH, MODE_DEBUG>(p, ctas, st);
 }

@@ -42,6 +42,12 @@ struct StepParams {
     // z-slab decomposition (multi-GPU): bit 0 = local plane 0 is an interface
     // owned by this rank (its lower-layer partial arrives from below), bit 1 = the top local
     // plane is an interface owned by the rank above (send its partial, do not update it)
+    // Rayleigh damping (reading R1, MODE_STEP only): the EBE input is ũ = u + cb·(u − u_prev) and
+    // u^{it+1} = fma(w, F − K ũ, (2u − u_prev) − ca·(u − u_prev)), written to un (a third buffer:
+    // halo nodes read u_prev, so the update cannot be in place)
+    int damped;
+    double ca, cb;         // RN(alpha·dt), RN(beta/dt)
+    double *un;
     int stages;            // INT8 path: M (4, 6 or 8)
     int nmat;              // materials in c_mat[0, nmat) (ids < 255; 255 = zero material)
     int slab_flags;

@@ -33,7 +33,9 @@ struct SmemF2 {
     MatW mw[kMaxMat];                 // [0, nmat) and the zero material kZeroMat
 };
 
-template <int MODE>
+// DAMP (MODE_STEP only): Rayleigh damping, reading R1 — the planes hold ũ = u + cb·(u − u_prev),
+// the update reads u and u_prev from global memory and writes u^{it+1} to p.un.
+template <int MODE, bool DAMP>
 __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     constexpr int NT = F2::NT, TY = F2::TY, PLANE = F2::PLANE, PF = F2::PF;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -91,6 +93,16 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
             has_rec |= (ix >= X0 && ix < X0 + TX && iy >= Y0 && iy < Y0 + TY);
         }
 
+    // u (undamped) or ũ = u + cb·(u − u_prev) (damped) at global offset o
+    auto load_in = [&](int64_t o) {
+        const double uu = __ldg(p.u + o);
+        if constexpr (DAMP) {
+            const double pp = __ldg(p.uo + o);    // u_prev is read-only in a damped step
+            return __dadd_rn(uu, __dmul_rn(p.cb, __dsub_rn(uu, pp)));
+        } else {
+            return uu;
+        }
+    };
     for (int i = t; i < p.nmat + 1; i += NT) {
         const int id = i < p.nmat ? i : kZeroMat;
         const MatConst &m = c_mat[id];
@@ -109,7 +121,7 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
             const int px = rem / 3, c = rem - px * 3;
             const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
             dst[idx] = (iz <= nz && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1)
-                           ? __ldg(p.u + 3 * (ix + NX1 * (iy + NY1 * iz)) + c) : 0.0;
+                           ? load_in(3 * (ix + NX1 * (iy + NY1 * iz)) + c) : 0.0;
         }
     }
     __syncthreads();
@@ -132,7 +144,7 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     // material ids of the current and next layer; the one after is fetched two layers ahead
     int mcur = (ein && Lfirst < nz) ? (int)__ldg(matcol + mstride * Lfirst) : kZeroMat;
     int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matcol + mstride * (Lfirst + 1)) : kZeroMat;
-    double nupv[3] = {0.0, 0.0, 0.0}, nwn = 0.0;
+    double nupv[3] = {0.0, 0.0, 0.0}, nwn = 0.0, nuv[3] = {0.0, 0.0, 0.0};
     uint8_t ndm = 0;
     for (int L = Z0 - 1; L < Z1; ++L) {
         const bool layer_ok = (L >= 0 && L < nz);
@@ -142,14 +154,15 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         const int pz = L + 3;
         const bool pf = (pz > Lfirst + 2) && (L + 2 < Z1) && (L + 2 < nz);
         double pfv[PF];
-        const double *uplane = p.u + 3 * PSTRIDE * pz;
+        const int64_t uplane = 3 * PSTRIDE * pz;
 #pragma unroll
         for (int j = 0; j < PF; ++j)
-            if (pf && pfok[j]) pfv[j] = __ldg(uplane + pfoff[j]);
+            if (pf && pfok[j]) pfv[j] = load_in(uplane + pfoff[j]);
         const bool upd = plane_done && own;
         const int64_t un_id = ucol + PSTRIDE * L;
         // update operands of plane L were loaded one layer ahead; fetch those of plane L+1
         double upv[3] = {nupv[0], nupv[1], nupv[2]};
+        const double uv[3] = {nuv[0], nuv[1], nuv[2]};
         const double wn = nwn;
         const uint8_t dm = ndm;
         if (MODE == MODE_STEP) {
@@ -159,6 +172,10 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
                 nupv[0] = p.uo[3 * nid];
                 nupv[1] = p.uo[3 * nid + 1];
                 nupv[2] = p.uo[3 * nid + 2];
+                if constexpr (DAMP) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) nuv[c] = __ldg(p.u + 3 * nid + c);
+                }
                 nwn = __ldg(p.w + nid);
                 ndm = p.dmask ? __ldg(p.dmask + nid) : (uint8_t)0;
             }
@@ -213,9 +230,12 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
                     if (has_src)
                         for (int k = 0; k < p.nsrc; ++k)
                             if (p.src_dof[k] == dof) F += p.src_val[k];
-                    double un = fma(wn, F - facc[c], 2.0 * up[c] - upv[c]);
+                    const double uc = DAMP ? uv[c] : up[c];
+                    double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
+                    if constexpr (DAMP) b = __dsub_rn(b, __dmul_rn(p.ca, __dsub_rn(uc, upv[c])));
+                    double un = __fma_rn(wn, __dsub_rn(F, facc[c]), b);
                     if ((dm >> c) & 1) un = 0.0;
-                    p.uo[dof] = un;
+                    (DAMP ? p.un : p.uo)[dof] = un;
                     if (has_rec)
                         for (int k = 0; k < p.nrec; ++k)
                             if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;

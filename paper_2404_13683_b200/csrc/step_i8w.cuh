@@ -143,7 +143,10 @@ __device__ __forceinline__ int ring3(int x) { return (x + 9) % 3; }    // x >= -
 // so one M-tile's conversion (F2I / FP64 heavy) overlaps the other's epilogue (integer heavy) and the
 // tensor core work of the two M-tiles is spread over the iteration.  Node row 4 (M-tile 1) reads the
 // x-pairs of element row 3 (M-tile 0) one iteration after they were written.
-template <int MODE, int M>
+// DAMP (MODE_STEP only): Rayleigh damping, reading R1 — the smem planes hold the EBE input
+// ũ = u + cb·(u − u_prev) (node maxima of ũ), the update reads u and u_prev from global memory and
+// writes u^{it+1} to p.un.
+template <int MODE, int M, bool DAMP>
 __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     using C = I8W;
     constexpr int NB = (7 * M + 1 + 7) / 8;
@@ -185,6 +188,16 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     const int64_t ucol = own ? ex + NX1 * ey : 0;
     const bool upd_role = own && hf == 0;
 
+    // u (undamped) or ũ = u + cb·(u − u_prev) (damped) of one node component (global offset o)
+    auto load_in = [&](int64_t o) {
+        const double uu = __ldg(p.u + o);
+        if constexpr (DAMP) {
+            const double pp = __ldg(p.uo + o);    // u_prev is read-only in a damped step
+            return __dadd_rn(uu, __dmul_rn(p.cb, __dsub_rn(uu, pp)));
+        } else {
+            return uu;
+        }
+    };
     // plane loader role: node li of the smem plane, taken by the last NODES threads
     const int li = t - (NT - NODES);
     const bool lrole = li >= 0;
@@ -239,7 +252,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             double v3[3] = {0.0, 0.0, 0.0};
             if (ldn && iz <= nz)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) v3[c] = __ldg(p.u + 3 * PSTRIDE * iz + ldoff + c);
+                for (int c = 0; c < 3; ++c) v3[c] = load_in(3 * PSTRIDE * iz + ldoff + c);
             unsigned long long m = 0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -259,6 +272,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     int mcur = (ein && Lfirst < nz) ? (int)__ldg(matp + mstride * Lfirst) : kZeroMat;
     int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matp + mstride * (Lfirst + 1)) : kZeroMat;
     double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;   // update operands of this M-tile's post-phase plane
+    double uv[3] = {0.0, 0.0, 0.0};              // DAMP: u of the owned node (the plane holds ũ)
     uint8_t dm = 0;
     double plo[3] = {0.0, 0.0, 0.0};             // x-pair P(iy) of this thread's face, last epilogue layer
     // conversion -> epilogue hand-over (the same iteration for M-tile 0, the next one for M-tile 1)
@@ -303,10 +317,12 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
                         if (has_src)
                             for (int k = 0; k < p.nsrc; ++k)
                                 if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
-                        const double b = __dsub_rn(__dmul_rn(2.0, up[c]), upv[c]);
+                        const double uc = DAMP ? uv[c] : up[c];
+                        double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
+                        if constexpr (DAMP) b = __dsub_rn(b, __dmul_rn(p.ca, __dsub_rn(uc, upv[c])));
                         double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
                         if ((dm >> c) & 1) un = 0.0;
-                        p.uo[dof] = un;
+                        (DAMP ? p.un : p.uo)[dof] = un;
                         if (has_rec)
                             for (int k = 0; k < p.nrec; ++k)
                                 if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
@@ -448,7 +464,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     double pfv[3] = {0.0, 0.0, 0.0};
     bool pf = false;
     int mfar = kZeroMat;
-    double upv_n[3] = {0.0, 0.0, 0.0}, wn_n = 0.0;
+    double upv_n[3] = {0.0, 0.0, 0.0}, wn_n = 0.0, uv_n[3] = {0.0, 0.0, 0.0};
     uint8_t dm_n = 0;
     for (int h = 2 * (Z0 - 1); h <= 2 * (Z1 + 1) + 1; ++h) {
         const int L = h >> 1;
@@ -458,9 +474,8 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             const int pz = L + 2;
             pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < nz);
             if (pf && ldn) {
-                const double *src = p.u + 3 * PSTRIDE * pz + ldoff;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) pfv[c] = __ldg(src + c);
+                for (int c = 0; c < 3; ++c) pfv[c] = load_in(3 * PSTRIDE * pz + ldoff + c);
             }
             mfar = (ein && L + 2 < nz && L >= Lfirst) ? (int)__ldg(matp + mstride * (L + 2)) : kZeroMat;
             const int Pn = L - mt;                    // plane this thread updates in the next iteration
@@ -469,6 +484,10 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
                 upv_n[0] = p.uo[3 * un_next];
                 upv_n[1] = p.uo[3 * un_next + 1];
                 upv_n[2] = p.uo[3 * un_next + 2];
+                if constexpr (DAMP) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) uv_n[c] = __ldg(p.u + 3 * un_next + c);
+                }
                 wn_n = __ldg(p.w + un_next);
                 dm_n = p.dmask ? __ldg(p.dmask + un_next) : (uint8_t)0;
             }
@@ -500,6 +519,9 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             upv[0] = upv_n[0];
             upv[1] = upv_n[1];
             upv[2] = upv_n[2];
+            uv[0] = uv_n[0];
+            uv[1] = uv_n[1];
+            uv[2] = uv_n[2];
             wn = wn_n;
             dm = dm_n;
             upv_n[0] = upv_n[1] = upv_n[2] = 0.0;

@@ -34,7 +34,19 @@ struct SmemV1F64 {
 template <int PATH>
 using SmemV1 = SmemV1F64;
 
-template <int PATH>
+// u (undamped) or the damped EBE input ũ = u + cb·(u − u_prev) (reading R1) at global offset o
+template <bool DAMP>
+__device__ __forceinline__ double v1_load_in(const StepParams &p, int64_t o) {
+    const double uu = __ldg(p.u + o);
+    if constexpr (DAMP) {
+        const double pp = __ldg(p.uo + o);    // u_prev is read-only in a damped step
+        return __dadd_rn(uu, __dmul_rn(p.cb, __dsub_rn(uu, pp)));
+    } else {
+        return uu;
+    }
+}
+
+template <int PATH, bool DAMP>
 __device__ __forceinline__ void v1_load_plane_sync(double *dst, const StepParams &p, int64_t X0, int64_t Y0,
                                                    int64_t iz) {
     using C = V1<PATH>;
@@ -45,12 +57,14 @@ __device__ __forceinline__ void v1_load_plane_sync(double *dst, const StepParams
         const int px = rem / 3, c = rem - px * 3;
         const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
         double v = 0.0;
-        if (iz <= p.nz && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1) v = __ldg(p.u + 3 * (ix + NX1 * (iy + NY1 * iz)) + c);
+        if (iz <= p.nz && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1) v = v1_load_in<DAMP>(p, 3 * (ix + NX1 * (iy + NY1 * iz)) + c);
         dst[idx] = v;
     }
 }
 
-template <int PATH, int MODE>
+// DAMP (MODE_STEP only): Rayleigh damping, reading R1 (planes hold ũ; update reads u, u_prev from
+// global memory and writes u^{it+1} to p.un).
+template <int PATH, int MODE, bool DAMP>
 __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const StepParams p) {
     using C = V1<PATH>;
     constexpr int NT = C::NT, TY = C::TY, NOWN = C::NOWN, PLANE = C::PLANE, PF = C::PF;
@@ -115,8 +129,8 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
 
     for (int i = t; i < 2 * NOWN * 3; i += NT) (&S.facc[0][0])[i] = 0.0;
     const int64_t Lfirst = max(Z0 - 1, (int64_t)0);
-    v1_load_plane_sync<PATH>(S.up[Lfirst % 3], p, X0, Y0, Lfirst);
-    v1_load_plane_sync<PATH>(S.up[(Lfirst + 1) % 3], p, X0, Y0, Lfirst + 1);
+    v1_load_plane_sync<PATH, DAMP>(S.up[Lfirst % 3], p, X0, Y0, Lfirst);
+    v1_load_plane_sync<PATH, DAMP>(S.up[(Lfirst + 1) % 3], p, X0, Y0, Lfirst + 1);
     __syncthreads();
 
     // material of this thread's element in the current layer (prefetched one layer ahead;
@@ -130,17 +144,21 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
         const int64_t pz = L + 2;
         const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < p.nz);
         double pfv[PF];
-        const double *uplane = p.u + 3 * PSTRIDE * pz;
+        const int64_t uplane = 3 * PSTRIDE * pz;
 #pragma unroll
-        for (int j = 0; j < PF; ++j) pfv[j] = (pf && pfok[j]) ? __ldg(uplane + pfoff[j]) : 0.0;
+        for (int j = 0; j < PF; ++j) pfv[j] = (pf && pfok[j]) ? v1_load_in<DAMP>(p, uplane + pfoff[j]) : 0.0;
         const bool upd = plane_done && own;
         const int64_t un_id = ucol + PSTRIDE * L;
-        double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;
+        double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0, uv[3] = {0.0, 0.0, 0.0};
         uint8_t dm = 0;
         if (MODE == MODE_STEP && upd) {
             upv[0] = p.uo[3 * un_id];
             upv[1] = p.uo[3 * un_id + 1];
             upv[2] = p.uo[3 * un_id + 2];
+            if constexpr (DAMP) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) uv[c] = __ldg(p.u + 3 * un_id + c);
+            }
             wn = __ldg(p.w + un_id);
             dm = p.dmask ? __ldg(p.dmask + un_id) : (uint8_t)0;
         }
@@ -221,10 +239,12 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                         if (has_src)
                             for (int k = 0; k < p.nsrc; ++k)
                                 if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
-                        const double b = __dsub_rn(__dmul_rn(2.0, up[c]), upv[c]);
+                        const double uc = DAMP ? uv[c] : up[c];
+                        double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
+                        if constexpr (DAMP) b = __dsub_rn(b, __dmul_rn(p.ca, __dsub_rn(uc, upv[c])));
                         double un = __fma_rn(wn, __dsub_rn(F, fl[c]), b);
                         if ((dm >> c) & 1) un = 0.0;
-                        p.uo[dof] = un;
+                        (DAMP ? p.un : p.uo)[dof] = un;
                         if (has_rec)
                             for (int k = 0; k < p.nrec; ++k)
                                 if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;

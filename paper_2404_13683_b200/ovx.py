@@ -39,6 +39,7 @@ _SIGS = {
     "ovx_set_element_materials": [_vp, _vp],
     "ovx_set_dirichlet": [_vp, _vp],
     "ovx_set_dt": [_vp, _d],
+    "ovx_set_damping": [_vp, _d, _d],
     "ovx_setup_elements": [_vp, _int, _int],
     "ovx_get_int8_matrix": [_vp, _vp],
     "ovx_critical_dt": [_vp, _vp],
@@ -172,6 +173,10 @@ class Ovx:
 
     def set_dt(self, dt: float) -> None:
         self._call("ovx_set_dt", dt)
+
+    def set_damping(self, alpha: float, beta: float) -> None:
+        """Rayleigh damping C = alpha M + beta K (ovx_set_damping; reading R1)."""
+        self._call("ovx_set_damping", float(alpha), float(beta))
 
     def setup_elements(self, path: int = OVX_INT8, stages: int = 8) -> None:
         self._call("ovx_setup_elements", path, stages)
@@ -311,6 +316,8 @@ class Ovx:
         self.set_dt(m.dt)
         if len(m.src_node):
             self.set_sources(m.src_node, m.src_axis, m.amp)
+        if getattr(m, "alpha", 0.0) or getattr(m, "beta", 0.0):
+            self.set_damping(m.alpha, m.beta)
 
 
 def version() -> str:

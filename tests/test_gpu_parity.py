@@ -288,3 +288,48 @@ def test_table3_hierarchy_on_gpu(ovxmod):
         errs[M] = np.linalg.norm(s.apply_K(u) - ref) / np.linalg.norm(ref)
     assert errs[8] < 1e-14 and errs[6] < 1e-11 and 1e-10 < errs[4] < 1e-6
     assert errs[8] < errs[6] < errs[4]
+
+
+@pytest.mark.parametrize("name,path", PATHS)
+def test_damped_c1_trajectory(ovxmod, name, path):
+    """NEXT-1: Rayleigh damping (reading R1), C1 cube with the paper's 100-125 kHz band (ζ = 0.05),
+    100 steps against the damped oracle run; bit-exact on the INT8 and dense paths."""
+    m = wl.c1_cube(8, steps=100)
+    m.alpha, m.beta = wl.rayleigh_coeffs(100e3, 125e3, 0.05)
+    z = np.zeros(3 * m.n_nodes)
+    s = _solver(ovxmod, m, path)
+    s.set_state(z, z, 0)
+    s.step(100)
+    u, up, it = s.get_state()
+    ru, rup, rit, st = oracle.run(m.as_dict(), z, z, 0, 100, path=ORACLE_PATH[path])
+    assert st == 0 and it == rit == 100
+    assert _close(u, ru, path, 1e-12) and _close(up, rup, path, 1e-12)
+    u0, _, _, _ = oracle.run(wl.c1_cube(8, steps=100).as_dict(), z, z, 0, 100, path=ORACLE_PATH[path])
+    assert np.linalg.norm(u - u0) > 1e-6 * np.linalg.norm(u0)      # damping changed the answer
+
+
+def test_damped_ragged_multichunk_bit_exact(ovxmod):
+    """Damped steps read u_prev at halo nodes of neighbouring tiles and z-chunks: the update goes to
+    a third buffer; several tiles in x and y, two z-chunks, ragged tails, a source; INT8 path."""
+    m = _ragged()
+    wl.point_source(m, 17, 3, 35, 1, 1e5, 2e-5, 40, scale=1.0)
+    m.alpha, m.beta = 0.02 / m.dt, 0.03 * m.dt
+    rng = np.random.default_rng(3)
+    u0 = wl.random_field(m) * 1e-3
+    up0 = u0 + rng.standard_normal(u0.size) * 1e-6
+    for path in (0, 2):
+        s = _solver(ovxmod, m, path)
+        s.set_state(u0, up0, 0)
+        s.step(12)
+        u, up, _ = s.get_state()
+        ru, rup, _, st = oracle.run(m.as_dict(), u0, up0, 0, 12, path=ORACLE_PATH[path])
+        assert st == 0
+        assert np.array_equal(u, ru) and np.array_equal(up, rup), path
+
+
+def test_damping_rejected_on_slabs(ovxmod):
+    m = wl.small_random(4, 3, 4, ds=0.01)
+    s = _solver(ovxmod, m, 0)
+    s.set_damping(1.0, 1e-9)
+    with pytest.raises(ovxmod.OvxError):
+        s.set_slab(1, np.zeros(m.nx * m.ny, np.uint8))
