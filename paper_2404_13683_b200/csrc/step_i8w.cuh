@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     const int wu = __shfl_sync(0xffffffffu, warp, 0);   // the warp index as a uniform value
-    const int mt = warp >> 3, hf = (warp >> 2) & 1, qd = warp & 3;
+    const int mt = wu >> 3, hf = (wu >> 2) & 1, qd = wu & 3;   // warp-uniform roles (uniform registers)
     const int row = 32 * qd + lane;                      // MMA row = TMEM lane
 
     int bid = blockIdx.x;
@@ -282,14 +282,14 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     int64_t edj = -1;
 
     // ---- post-phase of layer / plane Lp: face sums, f_n = T + B, update ----
-    auto post_phase = [&](int Lp) {
+    auto post_phase = [&](int Lp, int s3, int s5) {   // s3, s5: ring slots of Lp
         if (!tnode) return;
         const bool plane_done = (Lp >= Z0 && Lp <= nz && Lp < Z1);
         const bool bot_iface = (p.slab_flags & 1) && Lp == 0;
         const bool top_iface = (p.slab_flags & 2) && Lp == nz;
         double face[3] = {0.0, 0.0, 0.0};
         if (layer_ok(Lp)) {
-            const double(*ys)[EX][3] = S.ysum[ring3(Lp)][hf];
+            const double(*ys)[EX][3] = S.ysum[s3][hf];
 #pragma unroll
             for (int c = 0; c < 3; ++c) face[c] = __dadd_rn(plo[c], ys[ly - 1][lx][c]);   // P(iy) + P(iy-1)
         }
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
 #pragma unroll
                     for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = f[c];
                 } else if (MODE == MODE_STEP) {
-                    const double *up = &S.up[ring5(Lp)][(ly * PX + lx) * 3];
+                    const double *up = &S.up[s5][(ly * PX + lx) * 3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         const int64_t dof = 3 * un_id + c;
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     };
 
     // ---- epilogue of layer Le: the 4 corner nodes of this thread's face ----
-    auto epilogue = [&](int Le) {
+    auto epilogue = [&](int Le, int s3) {              // s3: ysum slot of Le
         ptx::mbar_wait(&S.mbar[mt], phase);
         phase ^= 1;
         ptx::tc_fence_after();
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         ptx::tc_fence_before();
         // x-pairs: P(iy) of node (lx, ly) = own (-x,-y) corner + lane lx-1's (+x,-y) corner;
         // the +y corners give P(iy-1) of node (lx, ly+1), exchanged through smem
-        double(*ys)[EX][3] = S.ysum[ring3(Le)][hf];
+        double(*ys)[EX][3] = S.ysum[s3][hf];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const double pm = __shfl_up_sync(0xffffffffu, fc[3 * 1 + c], 1);   // (+x,-y) of lx-1
@@ -394,13 +394,13 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     };
 
     // ---- conversion of layer L (this thread's three chunks) and the MMA hand-off ----
-    auto convert = [&](int L) {
+    auto convert = [&](int L, int sL, int sL1) {       // ring slots of planes L, L+1
         const int64_t eid = ex + p.nx * (ey + p.ny * (int64_t)L);
         const int64_t dj = eid - p.dbg_e0;
         const bool dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < C::TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
                          dj >= 0 && dj < p.dbg_ne;
         // s_e from the per-node maxima of the two planes
-        const unsigned long long *m0 = S.nmax[ring5(L)], *m1 = S.nmax[ring5(L + 1)];
+        const unsigned long long *m0 = S.nmax[sL], *m1 = S.nmax[sL1];
         const int n0 = ly * PX + lx;
         unsigned long long ab = m0[n0];
         ab = max(ab, m0[n0 + 1]);
@@ -420,11 +420,11 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
         double ue[16];
         if (hf == 0) {
-            gather16<0>(ue, S.up[ring5(L)], S.up[ring5(L + 1)], lx, ly);
+            gather16<0>(ue, S.up[sL], S.up[sL1], lx, ly);
             i8w_convert<MODE, M, 0>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
             if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
         } else {
-            gather16<1>(ue, S.up[ring5(L)], S.up[ring5(L + 1)], lx, ly);
+            gather16<1>(ue, S.up[sL], S.up[sL1], lx, ly);
             i8w_convert<MODE, M, 1>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
         }
         es = s;
@@ -460,6 +460,9 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         }
     };
 
+    // ring slots of planes / layers L-2 .. L+2 (q5_k = (L-2+k) mod 5) and L-2 .. L (q3_k = (L-2+k) mod 3)
+    int q5_0 = ring5(Z0 - 3), q5_1 = ring5(Z0 - 2), q5_2 = ring5(Z0 - 1), q5_3 = ring5(Z0), q5_4 = ring5(Z0 + 1);
+    int q3_0 = ring3(Z0 - 3), q3_1 = ring3(Z0 - 2), q3_2 = ring3(Z0 - 1);
     // half-iterations: h = 2L (even) and 2L+1 (odd); one copy of each phase body, selected per M-tile
     double pfv[3] = {0.0, 0.0, 0.0};
     bool pf = false;
@@ -494,10 +497,10 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         }
         // M-tile 0: convert at even h, post-phase + epilogue at odd h; M-tile 1 the other way round
         if (odd == (mt == 1)) {
-            if (layer_ok(L)) convert(L);
+            if (layer_ok(L)) convert(L, q5_2, q5_3);
         } else {
-            post_phase(L - 1 - mt);
-            if (layer_ok(L - mt)) epilogue(L - mt);
+            post_phase(L - 1 - mt, mt ? q3_0 : q3_1, mt ? q5_0 : q5_1);
+            if (layer_ok(L - mt)) epilogue(L - mt, mt ? q3_1 : q3_2);
         }
         if (odd) {
             // ---- park plane L+2 (slot of plane L-3, no longer read) with its node maxima ----
@@ -506,11 +509,11 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
                 unsigned long long m = 0;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    S.up[ring5(pz)][3 * li + c] = pfv[c];
+                    S.up[q5_4][3 * li + c] = pfv[c];
                     const unsigned long long b = abs_bits(pfv[c]);
                     m = b > m ? b : m;
                 }
-                S.nmax[ring5(pz)][li] = m;
+                S.nmax[q5_4][li] = m;
             }
             if (L >= Lfirst) {
                 mcur = mnxt;
@@ -525,6 +528,12 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             wn = wn_n;
             dm = dm_n;
             upv_n[0] = upv_n[1] = upv_n[2] = 0.0;
+            {   // advance the ring slots to L+1 (rotation instead of a modulo per use)
+                const int t5 = q5_0;
+                q5_0 = q5_1; q5_1 = q5_2; q5_2 = q5_3; q5_3 = q5_4; q5_4 = t5;
+                const int t3 = q3_0;
+                q3_0 = q3_1; q3_1 = q3_2; q3_2 = t3;
+            }
             wn_n = 0.0;
             dm_n = 0;
             __syncthreads();

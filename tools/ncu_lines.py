@@ -36,6 +36,13 @@ print("total warp-instr", tot)
 for key, v in sorted(ins.items(), key=lambda kv: -kv[1])[:n]:
     top = ", ".join(f"{o}:{c*100//v}" for o, c in ops[key].most_common(3))
     print(f"{key[0]}:{key[1]:<4d} {v/tot*100:5.1f}% st {stall[key]/tots*100:5.1f}%  {src.get(key,'')[:60]:60s} [{top}]")
+for a in sys.argv:
+    if a.startswith("--op="):
+        want = a[5:]
+        print(f"\ntop lines by {want} count:")
+        for key, v in sorted(ops.items(), key=lambda kv: -kv[1][want])[:n]:
+            if v[want]:
+                print(f"{key[0]}:{key[1]:<4d} {v[want]/tot*100:5.2f}%  {src.get(key,'')[:80]}")
 if "--stalls" in sys.argv:
     print("\ntop lines by stall samples (main reasons):")
     for key, v in sorted(stall.items(), key=lambda kv: -kv[1])[:n]:
