@@ -146,20 +146,22 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matcol + mstride * (Lfirst + 1)) : kZeroMat;
     double nupv[3] = {0.0, 0.0, 0.0}, nwn = 0.0, nuv[3] = {0.0, 0.0, 0.0};
     uint8_t ndm = 0;
-    for (int L = Z0 - 1; L < Z1; ++L) {
+    // running offsets (advanced once per layer instead of 64-bit products per use)
+    const uint8_t *mfar_p = matcol + mstride * (int64_t)(Z0 + 1);      // material of layer L+2
+    int64_t uplane = 3 * PSTRIDE * (int64_t)(Z0 + 2);                  // plane L+3 of u
+    int64_t un_id = ucol + PSTRIDE * (int64_t)(Z0 - 1);                // node of plane L
+    for (int L = Z0 - 1; L < Z1; ++L, mfar_p += mstride, uplane += 3 * PSTRIDE, un_id += PSTRIDE) {
         const bool layer_ok = (L >= 0 && L < nz);
         const bool plane_done = (L >= Z0 && L <= nz);
-        const int mfar = (ein && L >= Lfirst && L + 2 < nz) ? (int)__ldg(matcol + mstride * (L + 2)) : kZeroMat;
+        const int mfar = (ein && L >= Lfirst && L + 2 < nz) ? (int)__ldg(mfar_p) : kZeroMat;
         // ---- prefetch plane L+3 (parked next iteration) and the update operands of plane L ----
         const int pz = L + 3;
         const bool pf = (pz > Lfirst + 2) && (L + 2 < Z1) && (L + 2 < nz);
         double pfv[PF];
-        const int64_t uplane = 3 * PSTRIDE * pz;
 #pragma unroll
         for (int j = 0; j < PF; ++j)
             if (pf && pfok[j]) pfv[j] = load_in(uplane + pfoff[j]);
         const bool upd = plane_done && own;
-        const int64_t un_id = ucol + PSTRIDE * L;
         // update operands of plane L were loaded one layer ahead; fetch those of plane L+1
         double upv[3] = {nupv[0], nupv[1], nupv[2]};
         const double uv[3] = {nuv[0], nuv[1], nuv[2]};

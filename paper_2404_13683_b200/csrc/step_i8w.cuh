@@ -463,6 +463,11 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     // ring slots of planes / layers L-2 .. L+2 (q5_k = (L-2+k) mod 5) and L-2 .. L (q3_k = (L-2+k) mod 3)
     int q5_0 = ring5(Z0 - 3), q5_1 = ring5(Z0 - 2), q5_2 = ring5(Z0 - 1), q5_3 = ring5(Z0), q5_4 = ring5(Z0 + 1);
     int q3_0 = ring3(Z0 - 3), q3_1 = ring3(Z0 - 2), q3_2 = ring3(Z0 - 1);
+    // running offsets of the prefetch (advanced once per iteration): plane L+2 of u, the material of
+    // layer L+2, the owned node of plane L - mt
+    int64_t ro_plane = 3 * PSTRIDE * (int64_t)(Z0 + 1);
+    const uint8_t *ro_mat = matp + mstride * (int64_t)(Z0 + 1);
+    int64_t ro_node = ucol + PSTRIDE * (int64_t)(Z0 - 1 - mt);
     // half-iterations: h = 2L (even) and 2L+1 (odd); one copy of each phase body, selected per M-tile
     double pfv[3] = {0.0, 0.0, 0.0};
     bool pf = false;
@@ -478,12 +483,12 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < nz);
             if (pf && ldn) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) pfv[c] = load_in(3 * PSTRIDE * pz + ldoff + c);
+                for (int c = 0; c < 3; ++c) pfv[c] = load_in(ro_plane + ldoff + c);
             }
-            mfar = (ein && L + 2 < nz && L >= Lfirst) ? (int)__ldg(matp + mstride * (L + 2)) : kZeroMat;
+            mfar = (ein && L + 2 < nz && L >= Lfirst) ? (int)__ldg(ro_mat) : kZeroMat;
             const int Pn = L - mt;                    // plane this thread updates in the next iteration
             if (MODE == MODE_STEP && upd_role && Pn >= Z0 && Pn <= nz && Pn < Z1) {
-                const int64_t un_next = ucol + PSTRIDE * Pn;
+                const int64_t un_next = ro_node;
                 upv_n[0] = p.uo[3 * un_next];
                 upv_n[1] = p.uo[3 * un_next + 1];
                 upv_n[2] = p.uo[3 * un_next + 2];
@@ -528,6 +533,9 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             wn = wn_n;
             dm = dm_n;
             upv_n[0] = upv_n[1] = upv_n[2] = 0.0;
+            ro_plane += 3 * PSTRIDE;
+            ro_mat += mstride;
+            ro_node += PSTRIDE;
             {   // advance the ring slots to L+1 (rotation instead of a modulo per use)
                 const int t5 = q5_0;
                 q5_0 = q5_1; q5_1 = q5_2; q5_2 = q5_3; q5_3 = q5_4; q5_4 = t5;
