@@ -51,6 +51,7 @@ def lib() -> ctypes.CDLL:
     L = ctypes.CDLL(build())
     L.oracle_node_w.argtypes = [_i64, _i64, _i64, _d, _u8p, _dp, _d, _dp]
     L.oracle_element_fp64.argtypes = [_dp, _d, _d, _d, _i32p, _i32p, _dp]
+    L.oracle_element_vfem.argtypes = [_dp, _d, _d, _d, _i32p, _i32p, _dp]
     L.oracle_element_int8.argtypes = [_dp, _d, _d, _d, _i8p, _int, _int,
                                       _dp, _i64p, _i32p, _i64p, _i64p, _i64p, _dp]
     L.oracle_element_int8.restype = _int
@@ -79,7 +80,25 @@ def int_matrices():
     return K8, np.array(Kk, dtype=np.int32), np.array(Kg, dtype=np.int32)
 
 
-PATH_FP64, PATH_INT8 = 0, 1
+PATH_FP64, PATH_INT8, PATH_VFEM = 0, 1, 2     # VFEM: the paper's conventional element (NEXT-3)
+
+
+@lru_cache(maxsize=1)
+def vfem_matrices():
+    """(Vk, Vg) int32 24×24: K_e^V = κ ds Vk/72 + G ds Vg/216 (oracle/element.py, exact)."""
+    from .element import vfem_int_matrices
+    Vk, Vg = vfem_int_matrices()
+    return np.array(Vk, dtype=np.int32), np.array(Vg, dtype=np.int32)
+
+
+def element_vfem(ue, kappa: float, G: float, ds: float) -> np.ndarray:
+    """VFEM element force K_e^V u_e, the C oracle's operation order."""
+    Vk, Vg = vfem_matrices()
+    ue = np.ascontiguousarray(ue, dtype=np.float64)
+    fe = np.zeros(24)
+    lib().oracle_element_vfem(_p(ue, _dp), float(kappa), float(G), float(ds), _p(Vk, _i32p), _p(Vg, _i32p),
+                              _p(fe, _dp))
+    return fe
 DIGITS_PAPER, DIGITS_BYTES = 0, 1
 DIGITS_BYTES_FOLD = 3      # byte slices + Eq. 9 diagonal term in the integer product (variant D)
 
@@ -142,8 +161,16 @@ def element_int8(ue, kappa, G, ds, M: int = 8, digits: int = DIGITS_BYTES_FOLD) 
                 degenerate=bool(deg))
 
 
-def apply_K(nx, ny, nz, ds, mat, kappa, G, u, path=PATH_FP64, M=8, digits=DIGITS_BYTES_FOLD) -> np.ndarray:
+def _path_matrices(path):
+    """(K8, Kk, Kg) for the C oracle: for PATH_VFEM, Kk / Kg carry the VFEM matrices Vk / Vg."""
     K8, Kk, Kg = int_matrices()
+    if path == PATH_VFEM:
+        Kk, Kg = vfem_matrices()
+    return K8, Kk, Kg
+
+
+def apply_K(nx, ny, nz, ds, mat, kappa, G, u, path=PATH_FP64, M=8, digits=DIGITS_BYTES_FOLD) -> np.ndarray:
+    K8, Kk, Kg = _path_matrices(path)
     mat = np.ascontiguousarray(mat, dtype=np.uint8)
     kappa = np.ascontiguousarray(kappa, dtype=np.float64)
     G = np.ascontiguousarray(G, dtype=np.float64)
@@ -163,7 +190,7 @@ def run(model, u, u_prev, it: int, nsteps: int, path=PATH_FP64, M=8, digits=DIGI
     alpha, beta (Rayleigh damping C = alpha M + beta K, reading R1; default 0).
     Returns (u, u_prev, it, status) with new arrays (inputs are not modified).
     """
-    K8, Kk, Kg = int_matrices()
+    K8, Kk, Kg = _path_matrices(path)
     nx, ny, nz, ds = model["nx"], model["ny"], model["nz"], model["ds"]
     mat = np.ascontiguousarray(model["mat"], dtype=np.uint8)
     kappa = np.ascontiguousarray(model["kappa"], dtype=np.float64)

@@ -214,3 +214,75 @@ def element_mass_full(rho: Fr, ds: Fr) -> list[list[Fr]]:
             v *= Fr(1) if CORNERS[a][j] == CORNERS[b][j] else Fr(0)
         M[a][b] = Fr(rho) * (Fr(ds) / 2) ** 3 * v
     return M
+
+
+# ---------------------------------------------------------------------------
+# VFEM: the paper's conventional voxel element (NEXT-3).
+# Trilinear basis φ^β = Π_j (1 + r̄_j^β r_j)/2 on the reference cube r ∈ [-1, 1]³ (the printed
+# "−1/8(r1+r̄1)(r2+r̄2)(r3+r̄3)" is sign-garbled, reading Q2; this is the standard form it
+# names), the same isotropic c, K_e^V = ∫ Bᵀ c B dv integrated exactly (the paper's 2×2×2 Gauss
+# rule is exact for this degree-2-per-variable integrand), lumped mass ρ ds³/8 per node
+# ("diagonal terms are approximated as ρ/8(1)_e"), the same as OVFEM.
+# ---------------------------------------------------------------------------
+
+def _lin_pair_integral(s: int, t: int) -> Fr:
+    """∫_{-1}^{1} (1 + s r)/2 · (1 + t r)/2 dr = (1 + s t/3)/2."""
+    return (1 + Fr(s * t, 3)) / 2
+
+
+def vfem_grad_gram(ds: Fr = Fr(1)) -> list[list[list[list[Fr]]]]:
+    """G[a][b][i][k] = ∫_e ∂_i φ^a ∂_k φ^b dv for the trilinear basis on a cube of side ds."""
+    ds = Fr(ds)
+    G = [[[[Fr(0)] * 3 for _ in range(3)] for _ in range(8)] for _ in range(8)]
+    for a, b in product(range(8), range(8)):
+        sa, sb = CORNERS[a], CORNERS[b]
+        for i, k in product(range(3), range(3)):
+            # ∂_i φ^a = (2/ds)(r̄_i^a/2) Π_{j≠i} (1 + r̄_j^a r_j)/2 ;  dv = (ds/2)³ dr
+            v = (2 / ds) * Fr(sa[i], 2) * (2 / ds) * Fr(sb[k], 2) * (ds / 2) ** 3
+            for j in range(3):
+                fa, fb = j != i, j != k
+                if fa and fb:
+                    v *= _lin_pair_integral(sa[j], sb[j])
+                elif fa or fb:
+                    v *= 1          # ∫ (1 + s r)/2 dr = 1
+                else:
+                    v *= 2          # ∫ dr
+            G[a][b][i][k] = v
+    return G
+
+
+def vfem_stiffness_parts(ds: Fr = Fr(1)) -> tuple[list[list[Fr]], list[list[Fr]]]:
+    """(A_κ^V, A_G^V) with K_e^V = κ A_κ^V + G A_G^V.  With λ = κ − 2G/3, μ = G:
+    K[ap][bq] = λ G_ab[p][q] + μ (G_ab[q][p] + δ_pq Σ_r G_ab[r][r])."""
+    G = vfem_grad_gram(ds)
+    Ak = [[Fr(0)] * 24 for _ in range(24)]
+    Ag = [[Fr(0)] * 24 for _ in range(24)]
+    for a, b in product(range(8), range(8)):
+        tr = sum(G[a][b][r][r] for r in range(3))
+        for p, q in product(range(3), range(3)):
+            lam_part = G[a][b][p][q]
+            mu_part = G[a][b][q][p] + (tr if p == q else 0)
+            Ak[3 * a + p][3 * b + q] = lam_part                        # κ multiplies λ's matrix
+            Ag[3 * a + p][3 * b + q] = mu_part - Fr(2, 3) * lam_part   # G: μ part − (2/3) λ part
+    return Ak, Ag
+
+
+VFEM_DK, VFEM_DG = 72, 216    # common denominators of A_κ^V, A_G^V at ds = 1
+
+
+def vfem_int_matrices() -> tuple[list[list[int]], list[list[int]]]:
+    """Integer (Vk, Vg) with A_κ^V = ds·Vk/72, A_G^V = ds·Vg/216 (checked exact)."""
+    Ak, Ag = vfem_stiffness_parts(Fr(1))
+    Vk = [[Ak[r][c] * VFEM_DK for c in range(24)] for r in range(24)]
+    Vg = [[Ag[r][c] * VFEM_DG for c in range(24)] for r in range(24)]
+    for M in (Vk, Vg):
+        for row in M:
+            for x in row:
+                if x.denominator != 1:
+                    raise ValueError("VFEM matrix not integral at the stated denominator")
+    return [[int(x) for x in row] for row in Vk], [[int(x) for x in row] for row in Vg]
+
+
+def vfem_element_stiffness(kappa: Fr, G: Fr, ds: Fr) -> list[list[Fr]]:
+    Ak, Ag = vfem_stiffness_parts(Fr(ds))
+    return [[Fr(kappa) * Ak[r][c] + Fr(G) * Ag[r][c] for c in range(24)] for r in range(24)]

@@ -76,6 +76,24 @@ void oracle_element_fp64(const double *ue, double kappa, double G, double ds,
 }
 
 /* ---------------------------------------------------------------------------
+ * (iii) VFEM (NEXT-3, the paper's conventional trilinear voxel element
+ * with lumped mass): f_e = κ ds A_κ^V u_e + G ds A_G^V u_e with A_κ^V = Vk/72 and
+ * A_G^V = Vg/216 (oracle/element.py derives Vk, Vg exactly); same operation order as (i).
+ * ------------------------------------------------------------------------- */
+void oracle_element_vfem(const double *ue, double kappa, double G, double ds,
+                         const int32_t *Vk, const int32_t *Vg, double *fe) {
+    double ck = kappa * ds / 72.0, cg = G * ds / 216.0;
+    for (int r = 0; r < 24; ++r) {
+        double a = 0.0, b = 0.0;
+        for (int c = 0; c < 24; ++c) {
+            a = a + (double)Vk[r * 24 + c] * ue[c];
+            b = b + (double)Vg[r * 24 + c] * ue[c];
+        }
+        fe[r] = ck * a + cg * b;
+    }
+}
+
+/* ---------------------------------------------------------------------------
  * (ii) Integer path (Eqs. 10-17), per element.
  *   digits == 0 : the paper's b = 2^7, M stages of signed 7-bit slices with a
  *                 signed top digit; v clamped to ±(2^(7M)-1) (reading Q9).
@@ -199,7 +217,8 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
  *   P(iy)   = f(ix, iy,   ez)[(-x,-y,z)] + f(ix-1, iy,   ez)[(+x,-y,z)],
  *   P(iy-1) = f(ix, iy-1, ez)[(-x,+y,z)] + f(ix-1, iy-1, ez)[(+x,+y,z)],
  * where a missing element (outside the grid) contributes 0.0.
- * path 0: FP64 (Kk, Kg);  path 1: integer path (K8, M, digits). */
+ * path 0: FP64 (Kk, Kg);  path 1: integer path (K8, M, digits);  path 2: VFEM (Kk, Kg hold
+ * the VFEM integer matrices Vk, Vg). */
 static double face_sum(const double *fe_all, int64_t nx, int64_t ny, int64_t nz, int64_t ix, int64_t iy,
                        int64_t ez, int top, int c) {
     /* corner (local node) of element (ix - dx, iy - dy) that is node (ix, iy): Q1 order */
@@ -233,6 +252,7 @@ void oracle_apply_K(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t
             for (int c = 0; c < 3; ++c) ue[3 * a + c] = u[3 * nodes[a] + c];
         int m = mat[e];
         if (path == 0) oracle_element_fp64(ue, kappa[m], G[m], ds, Kk, Kg, fe_all + 24 * e);
+        else if (path == 2) oracle_element_vfem(ue, kappa[m], G[m], ds, Kk, Kg, fe_all + 24 * e);
         else oracle_element_int8(ue, kappa[m], G[m], ds, K8, M, digits,
                                  NULL, NULL, NULL, NULL, NULL, NULL, fe_all + 24 * e);
     }
