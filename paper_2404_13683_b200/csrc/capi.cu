@@ -302,17 +302,29 @@ ovx_status ovx_set_dt(ovx_ctx *ctx, double dt) {
 ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
     if (!ctx->have_grid || !ctx->have_emat) return fail(ctx, OVX_ESTATE, "set grid and element materials first");
-    if (path != OVX_INT8 && path != OVX_FP64 && path != OVX_FP64_DENSE)
-        return fail(ctx, OVX_EINVAL, "path must be OVX_INT8, OVX_FP64 or OVX_FP64_DENSE");
+    if (path != OVX_INT8 && path != OVX_FP64 && path != OVX_FP64_DENSE && path != OVX_VFEM)
+        return fail(ctx, OVX_EINVAL, "path must be OVX_INT8, OVX_FP64, OVX_FP64_DENSE or OVX_VFEM");
     if (stages != 8 && !(path == OVX_INT8 && (stages == 4 || stages == 6)))
         return fail(ctx, OVX_EINVAL, "stages: M = 8 (all paths), or M = 4 / 6 on the INT8 path");
     if (derive_element_matrices(ctx->k8, ctx->Ak, ctx->Ag) != 0)
         return fail(ctx, OVX_EINVAL, "K_e^INT8 derivation produced a non-INT8 entry (PAPER.md L110 violated)");
-    for (int r = 0; r < 24; ++r)
-        for (int c = 0; c < 24; ++c) {
-            ctx->Kk[r * 24 + c] = (double)ctx->k8[r * 48 + c];
-            ctx->Kg[r * 24 + c] = (double)ctx->k8[r * 48 + 24 + c] + (r == c ? 128.0 : 0.0);
+    double dk = 256.0, dg = 384.0;        // K_e = κ ds Kk/dk + G ds Kg/dg for the dense kernel
+    if (path == OVX_VFEM) {
+        if (derive_vfem_matrices(ctx->Kk, ctx->Kg) != 0)
+            return fail(ctx, OVX_EINVAL, "VFEM matrices are not integral at denominators 72 / 216");
+        dk = 72.0;
+        dg = 216.0;
+        for (int i = 0; i < 576; ++i) {   // element spectrum (critical dt) from the VFEM matrices
+            ctx->Ak[i] = ctx->Kk[i] / dk;
+            ctx->Ag[i] = ctx->Kg[i] / dg;
         }
+    } else {
+        for (int r = 0; r < 24; ++r)
+            for (int c = 0; c < 24; ++c) {
+                ctx->Kk[r * 24 + c] = (double)ctx->k8[r * 48 + c];
+                ctx->Kg[r * 24 + c] = (double)ctx->k8[r * 48 + 24 + c] + (r == c ? 128.0 : 0.0);
+            }
+    }
     ctx->mc.resize(ctx->nmat);
     const double ds = ctx->ds;
     const double vol8 = ds * ds * ds / 8.0;
@@ -322,8 +334,8 @@ ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
         c.cG = (2.0 * g) / (3.0 * k);
         c.c1 = k * ds / 256.0;
         c.c2 = (256.0 * g) / (3.0 * k);
-        c.ck = k * ds / 256.0;
-        c.cg = g * ds / 384.0;
+        c.ck = k * ds / dk;               // the oracle's κ ds / 256 (OVFEM) or κ ds / 72 (VFEM)
+        c.cg = g * ds / dg;
         c.rho_vol8 = ctx->rho[m] * vol8;
         const double lam = k - 2.0 * g / 3.0, s0 = ds / 16.0, s1 = s0 * 0.75, s2 = s1 * 0.75;
         c.L0 = s0 * lam;

@@ -137,4 +137,46 @@ double sym_lambda_max(const double *A) {
     return lam;
 }
 
+// VFEM (NEXT-3): the conventional trilinear voxel element.  φ^a = Π_j (1 + r̄_j^a r_j)/2
+// on r ∈ [-1,1]³; K_e^V = ∫ Bᵀ c B dv, integrated exactly here (the paper's 2×2×2 Gauss rule is
+// exact for this integrand): with λ = κ − 2G/3, μ = G and g_ab[i][k] = ∫ ∂_i φ^a ∂_k φ^b dv,
+//   K[3a+p][3b+q] = λ g[p][q] + μ (g[q][p] + δ_pq Σ_r g[r][r]).
+// Written as K_e^V = κ ds Vk/72 + G ds Vg/216 with integer Vk, Vg (checked).  Lumped mass ρ ds³/8 per
+// node, the same as OVFEM.  Returns 0, or -1 if an entry is not an integer.
+int derive_vfem_matrices(double *Vk /*24x24*/, double *Vg /*24x24*/) {
+    Q g[8][8][3][3];
+    for (int a = 0; a < 8; ++a)
+        for (int b = 0; b < 8; ++b)
+            for (int i = 0; i < 3; ++i)
+                for (int k = 0; k < 3; ++k) {
+                    // ds = 1: ∂_i φ^a = r̄_i^a Π_{j≠i} (1 + r̄_j^a r_j)/2, dv = dr/8
+                    Q v = mul(mk(SG[a][i] * SG[b][k]), mk(1, 8));
+                    for (int j = 0; j < 3; ++j) {
+                        const bool fa = j != i, fb = j != k;
+                        if (fa && fb)      // ∫ (1 + s r)(1 + t r)/4 dr = (1 + st/3)/2
+                            v = mul(v, mul(add(mk(1), mk(SG[a][j] * SG[b][j], 3)), mk(1, 2)));
+                        else if (!fa && !fb)
+                            v = mul(v, mk(2));   // ∫ dr
+                        // exactly one factor present: ∫ (1 + s r)/2 dr = 1
+                    }
+                    g[a][b][i][k] = v;
+                }
+    for (int a = 0; a < 8; ++a)
+        for (int b = 0; b < 8; ++b) {
+            const Q tr = add(add(g[a][b][0][0], g[a][b][1][1]), g[a][b][2][2]);
+            for (int p = 0; p < 3; ++p)
+                for (int q = 0; q < 3; ++q) {
+                    const Q lam = g[a][b][p][q];
+                    Q mu = g[a][b][q][p];
+                    if (p == q) mu = add(mu, tr);
+                    const Q kk = mul(lam, mk(72));                                  // κ part × 72
+                    const Q gg = mul(add(mu, mul(mk(-2, 3), lam)), mk(216));        // G part × 216
+                    if (kk.d != 1 || gg.d != 1) return -1;
+                    Vk[(3 * a + p) * 24 + 3 * b + q] = (double)kk.n;
+                    Vg[(3 * a + p) * 24 + 3 * b + q] = (double)gg.n;
+                }
+        }
+    return 0;
+}
+
 }  // namespace ovx

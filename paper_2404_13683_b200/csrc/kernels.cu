@@ -332,7 +332,7 @@ cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
         return launch_i8_mode<8>(mode, p, ctas, st);
     }
     if (path == OVX_FP64) return launch_mode<OVX_FP64>(mode, p, ctas, st);
-    return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);
+    return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);   // OVX_FP64_DENSE and OVX_VFEM (its matrices)
 }
 
 cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, const uint8_t *mat_below,

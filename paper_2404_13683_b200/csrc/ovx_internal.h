@@ -83,6 +83,7 @@ cudaError_t launch_finite_check(const double *u, int64_t n, int *flag, cudaStrea
 
 // element_setup.cpp
 int derive_element_matrices(int8_t *k8, double *Ak, double *Ag);
+int derive_vfem_matrices(double *Vk, double *Vg);
 double sym_lambda_max(const double *A);
 
 }  // namespace ovx
