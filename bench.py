@@ -2,7 +2,7 @@
 """Benchmark of the OVFEM / TCOVFEM explicit time step on B200 (BASELINE.json metric:
 element-updates/s at 1/2/4/8 B200; INT8 tensor-pipe use; error vs FP64).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--path int8|fp64|fp64_dense|vfem] [--impl ovx|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--path int8|fp64|fp64_dense|vfem|vfem_dense] [--impl ovx|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 A "step" is one full time step of the hot path (element-by-element product Σ_e K_e u_e through
@@ -138,11 +138,11 @@ def cpu_oracle_sample(path_name: str, steps: int, n: int = 64) -> dict:
     """Time the oracle as it stands (single thread) on an n³ block of the C2 workload."""
     import oracle
     m, u0 = _workload(n)
-    po = {"int8": oracle.PATH_INT8, "vfem": oracle.PATH_VFEM}.get(path_name, oracle.PATH_FP64)
+    po = {"int8": oracle.PATH_INT8, "vfem": oracle.PATH_VFEM, "vfem_dense": oracle.PATH_VFEM}.get(path_name, oracle.PATH_FP64)
     t0 = time.perf_counter()
     oracle.run(m.as_dict(), u0, u0, 0, steps, path=po)
     dt = time.perf_counter() - t0
-    what = {"int8": "INT8-path emulation (int128)", "vfem": "VFEM path"}.get(path_name, "FP64 path")
+    what = {"int8": "INT8-path emulation (int128)", "vfem": "VFEM path", "vfem_dense": "VFEM path"}.get(path_name, "FP64 path")
     return {"value": m.n_elems * steps / dt, "unit": METRIC, "cores": 1, "kind": "oracle",
             "sample": f"{n}^3 block of the C2 workload (ν=0.25 roller box, standing P wave), {steps} steps, "
                       f"{what}, 1 thread, {dt:.1f} s"}
@@ -155,7 +155,7 @@ def run_reference(args) -> None:
     n = 48
     import oracle
     m, u0 = _workload(n)
-    po = {"int8": oracle.PATH_INT8, "vfem": oracle.PATH_VFEM}.get(args.path, oracle.PATH_FP64)
+    po = {"int8": oracle.PATH_INT8, "vfem": oracle.PATH_VFEM, "vfem_dense": oracle.PATH_VFEM}.get(args.path, oracle.PATH_FP64)
     u, up = u0, u0
     for _ in range(args.warmup):
         u, up, _, _ = oracle.run(m.as_dict(), u, up, 0, 1, path=po)
@@ -231,7 +231,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ovx", choices=["ovx", "reference"])
-    ap.add_argument("--path", default="int8", choices=["int8", "fp64", "fp64_dense", "vfem"])
+    ap.add_argument("--path", default="int8", choices=["int8", "fp64", "fp64_dense", "vfem", "vfem_dense"])
     ap.add_argument("--n", type=int, default=N_EDGE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp64-companion", action="store_true")
@@ -243,7 +243,7 @@ def main() -> None:
 
     import torch
     import torch.distributed as dist
-    from paper_2404_13683_b200 import OVX_INT8, OVX_FP64, OVX_FP64_DENSE, OVX_VFEM
+    from paper_2404_13683_b200 import OVX_INT8, OVX_FP64, OVX_FP64_DENSE, OVX_VFEM, OVX_VFEM_DENSE
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -251,7 +251,8 @@ def main() -> None:
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    paths = {"int8": OVX_INT8, "fp64": OVX_FP64, "fp64_dense": OVX_FP64_DENSE, "vfem": OVX_VFEM}
+    paths = {"int8": OVX_INT8, "fp64": OVX_FP64, "fp64_dense": OVX_FP64_DENSE, "vfem": OVX_VFEM,
+             "vfem_dense": OVX_VFEM_DENSE}
     path = paths[args.path]
     stream = torch.cuda.current_stream()
 
@@ -336,7 +337,8 @@ def main() -> None:
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_src": pk["src"],
                 "bytes_per_launch": bytes_launch, "kernel_ms_per_launch": kernel_ms,
-                "kernel": {0: "step_i8w<M=8>", 1: "step_f64", 2: "step_v1<FP64_DENSE>", 3: "step_v1<FP64_DENSE> (VFEM matrices)"}[path]}
+                "kernel": {0: "step_i8w<M=8>", 1: "step_f64", 2: "step_v1<FP64_DENSE>", 3: "step_f64<VF>",
+                           4: "step_v1<FP64_DENSE> (VFEM matrices)"}[path]}
     nodes_total = (args.n + 1) ** 2 * (args.n * world + 1)
     out = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,

@@ -56,8 +56,10 @@ enum {
     OVX_FP64 = 1,       /* FP64 CUDA-core reference, factored form of Eq. 5 (Walsh-Hadamard of the
                            corner values, ≈180 FP64 ops/element); equal to K_e^o u_e up to rounding */
     OVX_VFEM = 3,       /* NEXT-3: the paper's conventional VFEM element (trilinear hex, exact = 2x2x2
-                           Gauss integration, lumped mass) through the dense FP64
-                           kernel: f_e = (κds/72)(Vk u_e) + (Gds/216)(Vg u_e), sequential sums */
+                           Gauss integration, lumped mass), factored FP64 form
+                           (Walsh-Hadamard modes) */
+    OVX_VFEM_DENSE = 4, /* VFEM, literal dense form f_e = (κds/72)(Vk u_e) + (Gds/216)(Vg u_e) with
+                           sequential sums (bit-exact mirror of the oracle's VFEM path) */
     OVX_FP64_DENSE = 2  /* FP64, literal dense form f_e = (κds/256)(K^κ u_e) + (Gds/384)((K̄^G+128I)u_e)
                            with sequential sums: bit-identical to the oracle's FP64 definition */
 };
@@ -99,7 +101,7 @@ ovx_status ovx_set_damping(ovx_ctx *ctx, double alpha, double beta);
 /* Derive K_e^INT8 on the host in exact rational arithmetic,
  * check that all 1152 entries are integers in [-128,127] (L110; else OVX_EINVAL),
  * build per-material constants and the per-node w = dt²/m (Eq. 6, m_n = Σ ρ_e ds³/8).
- * path: OVX_INT8, OVX_FP64, OVX_FP64_DENSE or OVX_VFEM.  stages: M, the number of INT8 stages (a = 2^{7M},
+ * path: OVX_INT8, OVX_FP64, OVX_FP64_DENSE, OVX_VFEM or OVX_VFEM_DENSE.  stages: M, the number of INT8 stages (a = 2^{7M},
  * PAPER.md Eq. 16, Table 3): 8 (FP64-class), or 4 / 6 on the INT8 path (the paper's M = 4 is
  * FP32-class); the FP64 paths require 8. */
 ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages);

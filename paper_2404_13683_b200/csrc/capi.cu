@@ -302,14 +302,14 @@ ovx_status ovx_set_dt(ovx_ctx *ctx, double dt) {
 ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
     if (!ctx->have_grid || !ctx->have_emat) return fail(ctx, OVX_ESTATE, "set grid and element materials first");
-    if (path != OVX_INT8 && path != OVX_FP64 && path != OVX_FP64_DENSE && path != OVX_VFEM)
-        return fail(ctx, OVX_EINVAL, "path must be OVX_INT8, OVX_FP64, OVX_FP64_DENSE or OVX_VFEM");
+    if (path != OVX_INT8 && path != OVX_FP64 && path != OVX_FP64_DENSE && path != OVX_VFEM && path != OVX_VFEM_DENSE)
+        return fail(ctx, OVX_EINVAL, "path must be OVX_INT8, OVX_FP64, OVX_FP64_DENSE, OVX_VFEM or OVX_VFEM_DENSE");
     if (stages != 8 && !(path == OVX_INT8 && (stages == 4 || stages == 6)))
         return fail(ctx, OVX_EINVAL, "stages: M = 8 (all paths), or M = 4 / 6 on the INT8 path");
     if (derive_element_matrices(ctx->k8, ctx->Ak, ctx->Ag) != 0)
         return fail(ctx, OVX_EINVAL, "K_e^INT8 derivation produced a non-INT8 entry (PAPER.md L110 violated)");
     double dk = 256.0, dg = 384.0;        // K_e = κ ds Kk/dk + G ds Kg/dg for the dense kernel
-    if (path == OVX_VFEM) {
+    if (path == OVX_VFEM || path == OVX_VFEM_DENSE) {
         if (derive_vfem_matrices(ctx->Kk, ctx->Kg) != 0)
             return fail(ctx, OVX_EINVAL, "VFEM matrices are not integral at denominators 72 / 216");
         dk = 72.0;
@@ -345,6 +345,11 @@ ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
         c.M1 = s1 * g;
         c.M1x3 = 3.0 * c.M1;
         c.C2 = s2 * lam + 4.0 * (s2 * g);
+        for (int q = 0; q < 3; ++q) {    // factored VFEM weights w_T = (ds/16) 3^{-|T|}
+            const double wq = (ds / 16.0) / (q == 0 ? 1.0 : q == 1 ? 3.0 : 9.0);
+            c.vl[q] = wq * lam;
+            c.vm[q] = wq * g;
+        }
     }
     ctx->path = path;
     ctx->stages = stages;

@@ -139,6 +139,63 @@ __device__ __forceinline__ void element_force_wht(const double (&ue)[24], const 
     }
 }
 
+// ---- factored VFEM element force (OVX_VFEM, NEXT-3) ---------------------------
+// The trilinear field of the corner values is u_c(r) = (1/8) Σ_S h_c[S] Π_{j∈S} r_j with the same
+// Walsh-Hadamard transform h_c[S] as above, so ∂_i u_c = (1/(4ds)) Σ_{T ∌ i} h_c[T ∪ {i}] m_T(r),
+// m_T = Π_{j∈T} r_j.  The monomials are orthogonal on the cube (∫ m_T m_T' dv = δ ds³ 3^{-|T|}),
+// hence the strain energy of K_e^V (exact integration = the paper's 2×2×2 Gauss rule) splits per
+// monomial T, and  F_c[S] = ∂E/∂h_c[S] = Σ_{i∈S, T = S∖{i}} w_T ·
+//     (c = i:  λ Σ_{j∉T} h_j[T ∪ {j}] + 2μ h_i[S];   c ≠ i:  μ (h_c[S] + h_i[T ∪ {c}]·[c ∉ T])),
+// w_T = (ds/16) 3^{-|T|}; then f_c^α = Σ_S F_c[S] Π_{j∈S} r̄_j^α (inverse transform).
+// Equal to K_e^V u_e in exact arithmetic (≈250 FP64 operations instead of 1152 FMAs).
+template <class MC>   // anything with vl[3] = w_T λ, vm[3] = w_T μ for |T| = 0, 1, 2
+__device__ __forceinline__ void element_force_vfem_wht(const double (&ue)[24], const MC &m, double (&fe)[24]) {
+    constexpr int BORD[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // local node -> bit index x | y<<1 | z<<2
+    double h[3][8];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) h[c][BORD[a]] = ue[3 * a + c];
+        wht8(h[c]);
+    }
+    double F[3][8];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int S = 0; S < 8; ++S) F[c][S] = 0.0;
+#pragma unroll
+    for (int T = 0; T < 8; ++T) {
+        const int nT = (T & 1) + ((T >> 1) & 1) + ((T >> 2) & 1);
+        if (nT == 3) continue;
+        const double lam = m.vl[nT], mu = m.vm[nT];
+        double div = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            if (!((T >> j) & 1)) div += h[j][T | (1 << j)];
+        const double ldiv = lam * div;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if ((T >> i) & 1) continue;
+            const int S = T | (1 << i);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (c == i) {
+                    F[c][S] += fma(2.0 * mu, h[i][S], ldiv);
+                } else {
+                    const double gic = ((T >> c) & 1) ? 0.0 : h[i][T | (1 << c)];
+                    F[c][S] += mu * (h[c][S] + gic);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        iwht8(F[c]);
+#pragma unroll
+        for (int a = 0; a < 8; ++a) fe[3 * a + c] = F[c][BORD[a]];
+    }
+}
+
 // Exact double of the limb c0 + 2^8 c1 + 2^16 c2 + 2^24 c3 of the stage products (|c_j| < 2^21,
 // so the pairs p0, p1 fit 32 bits and the limb |.| < 2^46): p0 + 2^16 p1 is formed in the low
 // bits of the double 1.5·2^52 (one IMAD.WIDE; the multiplier is read from constant memory so
@@ -195,25 +252,26 @@ cudaError_t launch_t(const StepParams &p, int64_t ctas, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int MODE, bool DAMP>
+template <int MODE, bool DAMP, bool VF>
 cudaError_t launch_f64(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
     const int smem = (int)sizeof(SmemF2);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_f64<MODE, DAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_f64<MODE, DAMP, VF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_f64<MODE, DAMP><<<(unsigned)ctas, F2::NT, smem, st>>>(p);
+    step_f64<MODE, DAMP, VF><<<(unsigned)ctas, F2::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
 template <int PATH>
 cudaError_t launch_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
-    if constexpr (PATH == OVX_FP64) {   // dedicated shuffle/register kernel; debug records via step_v1
+    if constexpr (PATH == OVX_FP64 || PATH == OVX_VFEM) {   // dedicated shuffle/register kernel;
+        constexpr bool VF = PATH == OVX_VFEM;                   // debug records and slabs via step_v1
         if (mode == MODE_STEP && p.slab_flags == 0)
-            return p.damped ? launch_f64<MODE_STEP, true>(p, ctas, st) : launch_f64<MODE_STEP, false>(p, ctas, st);
-        if (mode == MODE_APPLY) return launch_f64<MODE_APPLY, false>(p, ctas, st);
+            return p.damped ? launch_f64<MODE_STEP, true, VF>(p, ctas, st) : launch_f64<MODE_STEP, false, VF>(p, ctas, st);
+        if (mode == MODE_APPLY) return launch_f64<MODE_APPLY, false, VF>(p, ctas, st);
     }
     if (mode == MODE_STEP)
         return p.damped ? launch_t<PATH, MODE_STEP, true>(p, ctas, st) : launch_t<PATH, MODE_STEP, false>(p, ctas, st);
@@ -284,7 +342,7 @@ LaunchInfo info_t(int64_t nx, int64_t ny, int64_t nz) {
     const int zc = choose_zchunk(nz + 1, tx * ty, 2);
     li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
     li.threads = C::NT;
-    li.smem = PATH == OVX_FP64 ? (int)sizeof(SmemF2) : (int)sizeof(SmemV1<PATH>);
+    li.smem = (PATH == OVX_FP64 || PATH == OVX_VFEM) ? (int)sizeof(SmemF2) : (int)sizeof(SmemV1<PATH>);
     return li;
 }
 
@@ -316,6 +374,7 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
         return li;
     }
     if (path == OVX_FP64) return info_t<OVX_FP64>(nx, ny, nz);
+    if (path == OVX_VFEM) return info_t<OVX_VFEM>(nx, ny, nz);
     return info_t<OVX_FP64_DENSE>(nx, ny, nz);
 }
 
@@ -332,7 +391,8 @@ cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
         return launch_i8_mode<8>(mode, p, ctas, st);
     }
     if (path == OVX_FP64) return launch_mode<OVX_FP64>(mode, p, ctas, st);
-    return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);   // OVX_FP64_DENSE and OVX_VFEM (its matrices)
+    if (path == OVX_VFEM) return launch_mode<OVX_VFEM>(mode, p, ctas, st);
+    return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);   // OVX_FP64_DENSE and OVX_VFEM_DENSE (its matrices)
 }
 
 cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, const uint8_t *mat_below,

@@ -18,6 +18,7 @@ constexpr int kMaxRec = 32;
 struct MatConst {
     double cG, c1, c2, ck, cg, rho_vol8;
     double L0, M0, M0x2, L1, M1, M1x3, C2;
+    double vl[3], vm[3];   // factored VFEM: (ds/16)·3^{-|T|}·λ and ·μ for |T| = 0, 1, 2
 };
 
 enum Mode { MODE_STEP = 0, MODE_APPLY = 1, MODE_DEBUG = 2 };

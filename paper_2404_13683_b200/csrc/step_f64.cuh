@@ -27,15 +27,25 @@ struct MatW {
     double L0, M0, M0x2, L1, M1, M1x3, C2, pad;
 };
 
+// factored VFEM constants (OVX_VFEM): w_T λ, w_T μ for |T| = 0, 1, 2
+struct MatV {
+    double vl[3], vm[3], pad[2];
+};
+union MatU {
+    MatW w;
+    MatV v;
+};
+
 struct SmemF2 {
     double up[4][F2::PLANE];          // ring: planes L, L+1 in use, L+2 parked, L+3 in flight
     double ysum[2][F2::EY][EX][6];    // +y-corner x-sums of each element row (double-buffered)
-    MatW mw[kMaxMat];                 // [0, nmat) and the zero material kZeroMat
+    MatU mw[kMaxMat];                 // [0, nmat) and the zero material kZeroMat
 };
 
 // DAMP (MODE_STEP only): Rayleigh damping, reading R1 — the planes hold ũ = u + cb·(u − u_prev),
 // the update reads u and u_prev from global memory and writes u^{it+1} to p.un.
-template <int MODE, bool DAMP>
+// VF: the factored VFEM element (OVX_VFEM, NEXT-3) instead of the factored OVFEM element.
+template <int MODE, bool DAMP, bool VF = false>
 __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     constexpr int NT = F2::NT, TY = F2::TY, PLANE = F2::PLANE, PF = F2::PF;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -106,7 +116,8 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     for (int i = t; i < p.nmat + 1; i += NT) {
         const int id = i < p.nmat ? i : kZeroMat;
         const MatConst &m = c_mat[id];
-        S.mw[id] = MatW{m.L0, m.M0, m.M0x2, m.L1, m.M1, m.M1x3, m.C2, 0.0};
+        if (VF) S.mw[id].v = MatV{{m.vl[0], m.vl[1], m.vl[2]}, {m.vm[0], m.vm[1], m.vm[2]}, {0.0, 0.0}};
+        else S.mw[id].w = MatW{m.L0, m.M0, m.M0x2, m.L1, m.M1, m.M1x3, m.C2, 0.0};
     }
     const int Lfirst = max(Z0 - 1, 0);
     // synchronous first three planes (the loop prefetches two planes ahead); the fourth ring
@@ -188,7 +199,8 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         if (layer_ok) {
             double ue[24], fe[24];
             gather<F2::PY>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
-            element_force_wht(ue, S.mw[mcur], fe);     // zero material outside the domain
+            if constexpr (VF) element_force_vfem_wht(ue, S.mw[mcur].v, fe);   // zero material outside
+            else element_force_wht(ue, S.mw[mcur].w, fe);                    // the domain -> fe = 0
             // x-sums at this element's -x node column: own -x corners + lane lx-1's +x corners
             // local nodes: (-x,-y)=0,4  (+x,-y)=1,5  (+x,+y)=2,6  (-x,+y)=3,7   (bottom, top)
             double xs[12];   // [dy][dz][c]

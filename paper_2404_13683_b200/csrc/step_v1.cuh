@@ -173,9 +173,10 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
                              dj >= 0 && dj < p.dbg_ne;
             double ue[24];
             gather<C::PY>(ue, plo, phi, lx, ly);
-            if constexpr (PATH == OVX_FP64) {
+            if constexpr (PATH == OVX_FP64 || PATH == OVX_VFEM) {
                 double fe[24];
-                element_force_wht(ue, c_mat[m], fe);   // zero material -> fe = 0 exactly
+                if constexpr (PATH == OVX_VFEM) element_force_vfem_wht(ue, c_mat[m], fe);
+                else element_force_wht(ue, c_mat[m], fe);   // zero material -> fe = 0 exactly
 #pragma unroll
                 for (int r = 0; r < 24; ++r) {
                     S.fe[r][el] = fe[r];

@@ -15,7 +15,7 @@ import numpy as np
 from . import build as _build
 
 OVX_OK, OVX_EINVAL, OVX_EUNSTABLE, OVX_ESTATE, OVX_ECUDA, OVX_ENCCL, OVX_ENOMEM = 0, 2, 3, 6, 7, 8, 9
-OVX_INT8, OVX_FP64, OVX_FP64_DENSE, OVX_VFEM = 0, 1, 2, 3   # OVX_VFEM: NEXT-3, the conventional element
+OVX_INT8, OVX_FP64, OVX_FP64_DENSE, OVX_VFEM, OVX_VFEM_DENSE = 0, 1, 2, 3, 4   # VFEM: NEXT-3
 
 _c = ctypes
 _vp = _c.c_void_p

@@ -20,7 +20,7 @@ def _model():
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("path", [0, 1, 3])
 def test_slabs_on_one_gpu_equal_monolithic(world, path):
     import torch
     if not torch.cuda.is_available():
@@ -42,7 +42,7 @@ def test_slabs_on_one_gpu_equal_monolithic(world, path):
     mu, mup, _ = s.get_state()
     if path == 0:   # INT8: same kernel and summation order -> bit-identical
         assert np.array_equal(u, mu) and np.array_equal(up, mup)
-    else:           # factored FP64: monolithic runs use step_f64 (different summation order)
+    else:           # factored FP64 / VFEM: monolithic runs use step_f64 (rounding may differ)
         assert np.linalg.norm(u - mu) <= 1e-12 * np.linalg.norm(mu)
     if path == 0:
         ru, rup, _, _ = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=oracle.PATH_INT8)

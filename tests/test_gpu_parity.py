@@ -33,9 +33,9 @@ def _solver(ovxmod, m, path):
     return s
 
 
-PATHS = [("int8", 0), ("fp64", 1), ("fp64_dense", 2), ("vfem", 3)]
-EXACT = {0: True, 1: False, 2: True, 3: True}  # factored FP64 differs from the dense order by rounding
-ORACLE_PATH = {0: oracle.PATH_INT8, 1: oracle.PATH_FP64, 2: oracle.PATH_FP64, 3: oracle.PATH_VFEM}
+PATHS = [("int8", 0), ("fp64", 1), ("fp64_dense", 2), ("vfem", 3), ("vfem_dense", 4)]
+EXACT = {0: True, 1: False, 2: True, 3: False, 4: True}   # factored forms differ from the dense order by rounding
+ORACLE_PATH = {0: oracle.PATH_INT8, 1: oracle.PATH_FP64, 2: oracle.PATH_FP64, 3: oracle.PATH_VFEM, 4: oracle.PATH_VFEM}
 
 
 def _close(a, ref, path, rel=1e-13):
@@ -166,7 +166,7 @@ def _node_force_oracle(m, u, ix, iy, iz, path):
         ue = np.concatenate([u[3 * n:3 * n + 3] for n in nodes])
         mm = m.mat[e]
         fe = (oracle.element_int8(ue, m.kappa[mm], m.G[mm], m.ds)["fe"] if path == 0
-              else oracle.element_vfem(ue, m.kappa[mm], m.G[mm], m.ds) if path == 3
+              else oracle.element_vfem(ue, m.kappa[mm], m.G[mm], m.ds) if path in (3, 4)
               else oracle.element_fp64(ue, m.kappa[mm], m.G[mm], m.ds))
         a = corner[(dy, dx)] + 4 * top
         return fe[3 * a:3 * a + 3]
