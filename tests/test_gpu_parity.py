@@ -334,3 +334,28 @@ def test_damping_rejected_on_slabs(ovxmod):
     s.set_damping(1.0, 1e-9)
     with pytest.raises(ovxmod.OvxError):
         s.set_slab(1, np.zeros(m.nx * m.ny, np.uint8))
+
+
+def test_e1_rebar_reduced_bit_exact(ovxmod):
+    """NEXT-2: the paper's rebar model (E1) at ds = 8 mm (steel / concrete, Table 1 source and
+    receivers, Rayleigh damping over 100-125 kHz), 30 steps: INT8 and dense-FP64 states and
+    receiver traces equal the oracle's bit for bit."""
+    m = wl.e1_rebar(8.0, steps=30)
+    m.amp = (1e3 * wl.bandlimited_impulse(12 * m.dt, 100e3, 125e3, m.dt, 30)).reshape(1, -1)   # early pulse
+    z = np.zeros(3 * m.n_nodes)
+    for path in (0, 2):
+        s = _solver(ovxmod, m, path)
+        s.set_receivers(m.receivers, 30)
+        s.set_state(z, z, 0)
+        s.step(30)
+        u, up, _ = s.get_state()
+        tr = s.get_traces()
+        ru, rup, ref = z.copy(), z.copy(), np.zeros((len(m.receivers), 3, 30))
+        for it in range(30):
+            ru, rup, _, st = oracle.run(m.as_dict(), ru, rup, it, 1, path=ORACLE_PATH[path])
+            assert st == 0
+            for k, n in enumerate(m.receivers):
+                ref[k, :, it] = ru[3 * n:3 * n + 3]
+        assert np.array_equal(u, ru) and np.array_equal(up, rup), path
+        assert np.array_equal(tr, ref), path
+        assert np.abs(tr).max() > 0
