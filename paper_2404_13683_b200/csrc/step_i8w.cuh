@@ -34,10 +34,10 @@ struct I8W {
     static constexpr int NT = 2 * NE;                  // threads
     static constexpr int MT = NE / 128;                // M=128 MMA tiles per layer
     static constexpr int TY = EY - 1;
+    static constexpr int PY = EY + 1;
     static constexpr int NOWN = TX * TY;
-    static constexpr int PYT = EY / MT + 1;            // node rows of one M-tile's plane copy (5)
-    static constexpr int NODEST = PX * PYT;            // nodes of one M-tile plane (165)
-    static constexpr int PLANET = NODEST * 3;
+    static constexpr int NODES = PX * PY;              // nodes of one u plane held in smem
+    static constexpr int PLANE = NODES * 3;
     static constexpr int TMEM_COLS = MT * 256;
 };
 
@@ -45,13 +45,12 @@ struct SmemI8W {
     uint8_t A[I8W::MT][4][A1_BYTES];      // [M-tile][half-word array], K-major canonical layout
     alignas(128) uint8_t B[6 * B1_PITCH];
     alignas(128) uint8_t BI[2][6 * BI_PITCH];
-    double up[I8W::MT][4][I8W::PLANET];             // per M-tile ring: L-1 (update), L, L+1, L+2
-    unsigned long long nmax[I8W::MT][4][I8W::NODEST];   // max_c |u_c| of each node (bit patterns)
-    double ysum[3][2][I8W::EY][EX][3];              // [layer slot][face] x-pair P of the +y corners
+    double up[5][I8W::PLANE];                       // ring: L-2, L-1 (updates), L, L+1 (gather), L+2
+    unsigned long long nmax[5][I8W::NODES];         // max_c |u_c| of each node (bit patterns)
+    double ysum[3][2][I8W::EY][EX][3];              // [layer mod 3][face] x-pair P of the +y corners
     double tf[2][I8W::NE][3];                       // [layer parity][tile node] top-face sums T
     double2 mc[kMaxMat];                            // (cG, c1) per material, staged from c_mat
-    uint64_t mbar[I8W::MT];                         // MMA completion, per M-tile
-    uint64_t r3full[3], r3empty[3];                 // element row 3 (tile 0) -> node row 4 (tile 1)
+    uint64_t mbar[I8W::MT];
     uint32_t tmem;
 };
 
@@ -135,28 +134,31 @@ __device__ __forceinline__ void i8w_convert(const StepParams &p, const double (&
         i8w_chunks<MODE, M, HF, false>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj);
 }
 
-// Decoupled M-tiles.  Each M-tile (8 warps: elements of rows 4mt .. 4mt+3) runs the layer loop on
-// its own: a private copy of its 5 node rows of every u plane (ring of 4), its own named barriers
-// (MMA hand-off, end of layer), its own TMEM columns and MMA mbarrier.  The two tiles meet in one
-// place only — node row 4 (tile 1) needs the x-pairs of element row 3 (tile 0) — handled as a
-// producer / consumer pair of mbarriers per face-sum slot, so the tiles drift freely (one's
-// conversion overlapping the other's epilogue) instead of meeting at a CTA barrier every layer.
-// Per layer L and tile:  prefetch plane L+2 → convert L → MMA → post-phase L-1 → epilogue L →
-// park plane L+2 → tile barrier.
+__device__ __forceinline__ int ring5(int x) { return (x + 10) % 5; }   // x >= -10
+__device__ __forceinline__ int ring3(int x) { return (x + 9) % 3; }    // x >= -9
+
+// Skewed M-tiles: iteration L = half-iterations 2L, 2L+1 (one CTA barrier at its end)
+//   M-tile 0: [convert(L) -> MMA(L)] | [post-phase(L-1), epilogue(L)]
+//   M-tile 1: [post-phase(L-2), epilogue(L-1)] | [convert(L) -> MMA(L)]   (its MMAs run across the barrier)
+// so one M-tile's conversion (F2I / FP64 heavy) overlaps the other's epilogue (integer heavy) and the
+// tensor core work of the two M-tiles is spread over the iteration.  Node row 4 (M-tile 1) reads the
+// x-pairs of element row 3 (M-tile 0) one iteration after they were written.
+// DAMP (MODE_STEP only): Rayleigh damping, reading R1 — the smem planes hold the EBE input
+// ũ = u + cb·(u − u_prev) (node maxima of ũ), the update reads u and u_prev from global memory and
+// writes u^{it+1} to p.un.
 template <int MODE, int M, bool DAMP>
 __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     using C = I8W;
     constexpr int NB = (7 * M + 1 + 7) / 8;
     constexpr int NA = (NB + 1) / 2;
     constexpr double ISCALE = 1.0 / (double)(1ull << (7 * M));    // exact power of two
-    constexpr int NODEST = C::NODEST;
+    constexpr int NT = C::NT, NODES = C::NODES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     SmemI8W &S = *reinterpret_cast<SmemI8W *>(smem_raw);
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     const int wu = __shfl_sync(0xffffffffu, warp, 0);   // the warp index as a uniform value
-    const int mt = wu >> 3, hf = (wu >> 2) & 1, qd = wu & 3;   // warp-uniform roles
-    const int tl = t - 256 * mt;                         // thread index within the M-tile
+    const int mt = wu >> 3, hf = (wu >> 2) & 1, qd = wu & 3;   // warp-uniform roles (uniform registers)
     const int row = 32 * qd + lane;                      // MMA row = TMEM lane
 
     int bid = blockIdx.x;
@@ -174,18 +176,19 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     const int Lend = min(nz, Z1);                       // layers [Lfirst, Lend) are computed
     auto layer_ok = [&](int x) { return x >= Lfirst && x < Lend; };
 
-    // element (lx, ly) of the tile; its (-x,-y) corner is tile node (lx, ly); local row lyl = qd
-    const int lx = lane, ly = 4 * mt + qd, lyl = qd;
+    // element (lx, ly) of the tile; its (-x,-y) corner is tile node (lx, ly)
+    const int lx = lane, ly = 4 * mt + qd;
     const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
     const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
     const uint8_t *matp = p.mat + (ein ? ex + p.nx * ey : 0);
     const int64_t mstride = p.nx * p.ny;
+    // node (lx, ly): owned by this tile (lx, ly >= 1) if inside the grid; half 0 updates it
     const bool tnode = lx >= 1 && ly >= 1;
     const bool own = tnode && ex < NX1 && ey < NY1;
     const int64_t ucol = own ? ex + NX1 * ey : 0;
     const bool upd_role = own && hf == 0;
 
-    // u (undamped) or ũ = u + cb·(u − u_prev) (damped) at global offset o
+    // u (undamped) or ũ = u + cb·(u − u_prev) (damped) of one node component (global offset o)
     auto load_in = [&](int64_t o) {
         const double uu = __ldg(p.u + o);
         if constexpr (DAMP) {
@@ -195,14 +198,12 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             return uu;
         }
     };
-    // plane loader role: node li of this M-tile's plane copy (node rows 4mt .. 4mt+4), taken by
-    // the last NODEST threads of the tile
-    const int li = tl - (256 - NODEST);
+    // plane loader role: node li of the smem plane, taken by the last NODES threads
+    const int li = t - (NT - NODES);
     const bool lrole = li >= 0;
     const int lpx = lrole ? li % PX : 0, lpy = lrole ? li / PX : 0;
-    const int64_t lgx = X0 - 1 + lpx, lgy = Y0 - 1 + 4 * mt + lpy;
-    const bool ldn = lrole && lgx >= 0 && lgx < NX1 && lgy >= 0 && lgy < NY1;
-    const int64_t ldoff = ldn ? 3 * (lgx + NX1 * lgy) : 0;
+    const bool ldn = lrole && X0 - 1 + lpx >= 0 && X0 - 1 + lpx < NX1 && Y0 - 1 + lpy >= 0 && Y0 - 1 + lpy < NY1;
+    const int64_t ldoff = ldn ? 3 * ((X0 - 1 + lpx) + NX1 * (Y0 - 1 + lpy)) : 0;
 
     bool has_src = false, has_rec = false;
     if (MODE == MODE_STEP && hf == 0) {
@@ -220,33 +221,28 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     }
 
     // ---- one-time setup: B operands, zero K-padding chunks, TMEM, mbarriers ----
-    for (int idx = t; idx < 48 * 96; idx += C::NT) {
+    for (int idx = t; idx < 48 * 96; idx += NT) {
         const int n = idx / 96, kb = idx - n * 96;
         const int off = (n >> 3) * B1_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
         S.B[off] = ((kb & 1) == (n & 1)) ? (uint8_t)(-(int)c_K8[(n >> 1) * 48 + (kb >> 1)]) : (uint8_t)0;
     }
-    for (int idx = t; idx < 2 * 48 * 32; idx += C::NT) {
+    for (int idx = t; idx < 2 * 48 * 32; idx += NT) {
         const int s2 = idx / (48 * 32), r2 = idx - s2 * 48 * 32;
         const int n = r2 / 32, kb = r2 - n * 32;
         const int off = (n >> 3) * BI_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
         const int k = 16 * s2 + (kb >> 1);
         S.BI[s2][off] = ((kb & 1) == (n & 1) && k == (n >> 1)) ? (uint8_t)0x80 : (uint8_t)0;
     }
-    for (int idx = t; idx < C::MT * 4 * 128; idx += C::NT) {
+    for (int idx = t; idx < C::MT * 4 * 128; idx += NT) {
         const int a = idx >> 7, r = idx & 127;
         *reinterpret_cast<uint4 *>(&S.A[a >> 2][a & 3][(r >> 3) * A1_PITCH + 6 * 128 + (r & 7) * 16]) =
             make_uint4(0, 0, 0, 0);
     }
     if (warp == 0) ptx::tmem_alloc<C::TMEM_COLS>(&S.tmem);
-    if (t == 0) {
+    if (t == 0)
         for (int mm = 0; mm < C::MT; ++mm) ptx::mbar_init(&S.mbar[mm], 1);
-        for (int k = 0; k < 3; ++k) {
-            ptx::mbar_init(&S.r3full[k], 2);    // the two tile-0 warps of element row 3
-            ptx::mbar_init(&S.r3empty[k], 2);   // the two tile-1 warps of node row 4
-        }
-    }
-    for (int i = t; i < 2 * C::NE * 3; i += C::NT) (&S.tf[0][0][0])[i] = 0.0;
-    for (int i = t; i < p.nmat + 1; i += C::NT) {      // a per-lane indexed constant-bank load serialises
+    for (int i = t; i < 2 * C::NE * 3; i += NT) (&S.tf[0][0][0])[i] = 0.0;
+    for (int i = t; i < p.nmat + 1; i += NT) {      // a per-lane indexed constant-bank load serialises
         const int id = i < p.nmat ? i : kZeroMat;
         S.mc[id] = make_double2(c_mat[id].cG, c_mat[id].c1);
     }
@@ -260,11 +256,11 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             unsigned long long m = 0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                S.up[mt][iz & 3][3 * li + c] = v3[c];
+                S.up[ring5(iz)][3 * li + c] = v3[c];
                 const unsigned long long b = abs_bits(v3[c]);
                 m = b > m ? b : m;
             }
-            S.nmax[mt][iz & 3][li] = m;
+            S.nmax[ring5(iz)][li] = m;
         }
     }
     ptx::fence_proxy_async_smem();
@@ -272,270 +268,285 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     __syncthreads();
     ptx::tc_fence_after();
 
-    // face-sum slot and phase of layer x (relative to the first loop layer, so that each slot's
-    // first use sees a fresh mbarrier)
-    auto fslot = [&](int x) { return (x - (Z0 - 1)) % 3; };
-    auto fpar = [&](int x) { return (uint32_t)(((x - (Z0 - 1)) / 3) & 1); };
-
     uint32_t phase = 0;
     int mcur = (ein && Lfirst < nz) ? (int)__ldg(matp + mstride * Lfirst) : kZeroMat;
     int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matp + mstride * (Lfirst + 1)) : kZeroMat;
-    double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;   // update operands of the post-phase plane (L-1)
+    double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;   // update operands of this M-tile's post-phase plane
     double uv[3] = {0.0, 0.0, 0.0};              // DAMP: u of the owned node (the plane holds ũ)
     uint8_t dm = 0;
-    double plo[3] = {0.0, 0.0, 0.0};             // x-pair P(iy) of this thread's face, layer L-1
-    int64_t ro_plane = 3 * PSTRIDE * (int64_t)(Z0 + 1);               // plane L+2 of u
-    const uint8_t *ro_mat = matp + mstride * (int64_t)(Z0 + 1);        // material of layer L+2
-    int64_t ro_node = ucol + PSTRIDE * (int64_t)(Z0 - 1);             // owned node of plane L
-    const bool r3prod = mt == 0 && qd == 3;      // warps writing element row 3 (tile 0)
-    const bool r3cons = mt == 1 && qd == 0;      // warps reading it for node row 4 (tile 1)
+    double plo[3] = {0.0, 0.0, 0.0};             // x-pair P(iy) of this thread's face, last epilogue layer
+    // conversion -> epilogue hand-over (the same iteration for M-tile 0, the next one for M-tile 1)
+    double es = 0.0;
+    bool edeg = false, edbg = false;
+    int em = kZeroMat;
+    int64_t edj = -1;
 
-    for (int L = Z0 - 1; L <= Z1; ++L, ro_plane += 3 * PSTRIDE, ro_mat += mstride, ro_node += PSTRIDE) {
-        // ---- 1. prefetch: plane L+2, material of layer L+2, update operands of plane L ----
-        const int pz = L + 2;
-        const bool pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < nz);
-        double pfv[3] = {0.0, 0.0, 0.0};
-        if (pf && ldn) {
+    // ---- post-phase of layer / plane Lp: face sums, f_n = T + B, update ----
+    auto post_phase = [&](int Lp, int s3, int s5) {   // s3, s5: ring slots of Lp
+        if (!tnode) return;
+        const bool plane_done = (Lp >= Z0 && Lp <= nz && Lp < Z1);
+        const bool bot_iface = (p.slab_flags & 1) && Lp == 0;
+        const bool top_iface = (p.slab_flags & 2) && Lp == nz;
+        double face[3] = {0.0, 0.0, 0.0};
+        if (layer_ok(Lp)) {
+            const double(*ys)[EX][3] = S.ysum[s3][hf];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) pfv[c] = load_in(ro_plane + ldoff + c);
+            for (int c = 0; c < 3; ++c) face[c] = __dadd_rn(plo[c], ys[ly - 1][lx][c]);   // P(iy) + P(iy-1)
         }
-        const int mfar = (ein && L + 2 < nz && L >= Lfirst) ? (int)__ldg(ro_mat) : kZeroMat;
-        double upv_n[3] = {0.0, 0.0, 0.0}, wn_n = 0.0, uv_n[3] = {0.0, 0.0, 0.0};
-        uint8_t dm_n = 0;
-        if (MODE == MODE_STEP && upd_role && L >= Z0 && L <= nz && L < Z1) {
-            const int64_t un_next = ro_node;
-            upv_n[0] = p.uo[3 * un_next];
-            upv_n[1] = p.uo[3 * un_next + 1];
-            upv_n[2] = p.uo[3 * un_next + 2];
-            if constexpr (DAMP) {
+        if (hf == 1) {        // top face of layer Lp: T of plane Lp+1
 #pragma unroll
-                for (int c = 0; c < 3; ++c) uv_n[c] = __ldg(p.u + 3 * un_next + c);
-            }
-            wn_n = __ldg(p.w + un_next);
-            dm_n = p.dmask ? __ldg(p.dmask + un_next) : (uint8_t)0;
-        }
-        const int sL = L & 3, sL1 = (L + 1) & 3, sLm1 = (L + 3) & 3;   // ring slots of L, L+1, L-1
-
-        // ---- 2. conversion of layer L (this thread's three chunks), MMA hand-off ----
-        double es = 0.0;
-        bool edeg = false, edbg = false;
-        int64_t edj = -1;
-        if (layer_ok(L)) {
-            const int64_t eid = ex + p.nx * (ey + p.ny * (int64_t)L);
-            const int64_t dj = eid - p.dbg_e0;
-            const bool dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < C::TY && (L + 1 >= Z0) &&
-                             (L + 1 < Z1) && dj >= 0 && dj < p.dbg_ne;
-            const unsigned long long *m0 = S.nmax[mt][sL], *m1 = S.nmax[mt][sL1];
-            const int n0 = lyl * PX + lx;
-            unsigned long long ab = m0[n0];
-            ab = max(ab, m0[n0 + 1]);
-            ab = max(ab, m0[n0 + PX]);
-            ab = max(ab, m0[n0 + PX + 1]);
-            ab = max(ab, m1[n0]);
-            ab = max(ab, m1[n0 + 1]);
-            ab = max(ab, m1[n0 + PX]);
-            ab = max(ab, m1[n0 + PX + 1]);
-            const double amax = __longlong_as_double((long long)ab);
-            const double cG = S.mc[mcur].x;
-            const double s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
-            const bool deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
-            const bool vzero = !ein || !(s >= 0x1p-1022);
-            const bool fast = (s <= 0x1.fffffffffffffp1023) && (vzero || s >= 0x1p-960);
-            uint8_t *Ab = &S.A[mt][0][0];
-            const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
-            double ue[16];
-            if (hf == 0) {
-                gather16<0>(ue, S.up[mt][sL], S.up[mt][sL1], lx, lyl);
-                i8w_convert<MODE, M, 0>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
-                if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
+            for (int c = 0; c < 3; ++c) S.tf[Lp & 1][lx + EX * ly][c] = face[c];
+        } else if (own && plane_done) {
+            const int64_t un_id = ucol + PSTRIDE * Lp;
+            if (bot_iface) {  // interface plane: B waits for T from the rank below
+#pragma unroll
+                for (int c = 0; c < 3; ++c) p.iface_bot_b[3 * ucol + c] = face[c];
             } else {
-                gather16<1>(ue, S.up[mt][sL], S.up[mt][sL1], lx, lyl);
-                i8w_convert<MODE, M, 1>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
-            }
-            es = s;
-            edeg = deg;
-            edbg = dbg;
-            edj = dj;
-            ptx::fence_proxy_async_smem();
-            asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
-            if ((wu & 7) == 0) {     // first warp of the M-tile; one elected lane issues
-                const int mtu = wu >> 3;
-                if (ptx::elect_one()) {
-                    ptx::tc_fence_after();
-                    const uint32_t b0 = ptx::smem_u32(&S.B[0]);
-                    const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
-                    const uint32_t a0 = ptx::smem_u32(&S.A[mtu][0][0]);
+                double f[3];
 #pragma unroll
-                    for (int pa = 0; pa < NA; ++pa) {
-                        const uint32_t abase = a0 + pa * A1_BYTES;
-                        const uint32_t d = S.tmem + mtu * 256 + pa * 64;
+                for (int c = 0; c < 3; ++c) f[c] = __dadd_rn(S.tf[(Lp - 1) & 1][lx + EX * ly][c], face[c]);
+                if (top_iface) {
 #pragma unroll
-                        for (int ks = 0; ks < 3; ++ks)
-                            ptx::mma_i8(d, ptx::smem_desc(abase + ks * 256, 128, A1_PITCH),
-                                        ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC, ks > 0 ? 1u : 0u);
-                        ptx::mma_i8(d, ptx::smem_desc(abase + 3 * 128, 128, A1_PITCH),
-                                    ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
-                        ptx::mma_i8(d, ptx::smem_desc(abase + 5 * 128, 128, A1_PITCH),
-                                    ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
+                    for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = f[c];
+                } else if (MODE == MODE_STEP) {
+                    const double *up = &S.up[s5][(ly * PX + lx) * 3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const int64_t dof = 3 * un_id + c;
+                        double F = 0.0;
+                        if (has_src)
+                            for (int k = 0; k < p.nsrc; ++k)
+                                if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
+                        const double uc = DAMP ? uv[c] : up[c];
+                        double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
+                        if constexpr (DAMP) b = __dsub_rn(b, __dmul_rn(p.ca, __dsub_rn(uc, upv[c])));
+                        double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
+                        if ((dm >> c) & 1) un = 0.0;
+                        (DAMP ? p.un : p.uo)[dof] = un;
+                        if (has_rec)
+                            for (int k = 0; k < p.nrec; ++k)
+                                if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
                     }
-                    ptx::mma_commit(&S.mbar[mtu]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) p.fout[3 * un_id + c] = f[c];
                 }
-                __syncwarp();
             }
         }
+    };
 
-        // ---- 3. (overlaps the MMAs) post-phase of layer / plane Lp = L-1 ----
-        {
-            const int Lp = L - 1;
-            // node row 4 reads element row 3 of tile 0: wait until it is written (layer Lp)
-            if (r3cons && Lp >= Z0 - 1) ptx::mbar_wait(&S.r3full[fslot(Lp)], fpar(Lp));
-            if (tnode) {
-                const bool plane_done = (Lp >= Z0 && Lp <= nz && Lp < Z1);
-                const bool bot_iface = (p.slab_flags & 1) && Lp == 0;
-                const bool top_iface = (p.slab_flags & 2) && Lp == nz;
-                double face[3] = {0.0, 0.0, 0.0};
-                if (layer_ok(Lp)) {
-                    const double(*ys)[EX][3] = S.ysum[fslot(Lp)][hf];
+    // ---- epilogue of layer Le: the 4 corner nodes of this thread's face ----
+    auto epilogue = [&](int Le, int s3) {              // s3: ysum slot of Le
+        ptx::mbar_wait(&S.mbar[mt], phase);
+        phase ^= 1;
+        ptx::tc_fence_after();
+        // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
+        const double alpha = edeg ? 0.0 : -__dmul_rn(S.mc[em].y, __dmul_rn(es, ISCALE));
+        const uint32_t tb = S.tmem + ((uint32_t)(qd * 32) << 16) + mt * 256 + 24 * hf;
+        double fc[12];                               // [corner][c] of the face
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) face[c] = __dadd_rn(plo[c], ys[ly - 1][lx][c]);   // P(iy) + P(iy-1)
+        for (int rr = 0; rr < 3; ++rr) {             // 4 outputs per round (8 columns per array)
+            uint32_t R0[8], R1[8], R2[8] = {}, R3[8] = {};
+            ptx::tmem_ld8(tb + 0 + rr * 8, R0);
+            ptx::tmem_ld8(tb + 64 + rr * 8, R1);
+            if (NA > 2) ptx::tmem_ld8(tb + 128 + rr * 8, R2);
+            if (NA > 3) ptx::tmem_ld8(tb + 192 + rr * 8, R3);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = 4 * rr + q;
+                const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
+                const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
+                const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
+                const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
+                // D holds −C_j, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^46
+                const double dlo = limb_exact(c0, c1_, c2_, c3);
+                const double dhi = NA > 2 ? limb_exact(c4, c5, c6, c7) : 0.0;
+                const double Y = NA > 2 ? __fma_rn(dhi, 0x1p32, dlo) : dlo;    // RN(−y)
+                const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
+                if (MODE == MODE_DEBUG && edbg) {
+                    const int i = 12 * hf + j;
+                    const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};
+                    __int128 y = 0;
+#pragma unroll
+                    for (int jj = 7; jj >= 0; --jj) y = y * 256 - (__int128)Cj[jj];
+                    if (p.dbg_C)
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) p.dbg_C[edj * 192 + jj * 24 + i] = -Cj[jj];
+                    if (p.dbg_yhi) p.dbg_yhi[edj * 24 + i] = (long long)(y >> 64);
+                    if (p.dbg_ylo) p.dbg_ylo[edj * 24 + i] = (long long)(unsigned long long)y;
+                    if (p.dbg_fe) p.dbg_fe[edj * 24 + i] = f;
                 }
-                if (hf == 1) {        // top face of layer Lp: T of plane Lp+1
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) S.tf[Lp & 1][lx + EX * ly][c] = face[c];
-                } else if (own && plane_done) {
-                    const int64_t un_id = ucol + PSTRIDE * Lp;
-                    if (bot_iface) {  // interface plane: B waits for T from the rank below
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) p.iface_bot_b[3 * ucol + c] = face[c];
-                    } else {
-                        double f[3];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) f[c] = __dadd_rn(S.tf[(Lp - 1) & 1][lx + EX * ly][c], face[c]);
-                        if (top_iface) {
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = f[c];
-                        } else if (MODE == MODE_STEP) {
-                            const double *up = &S.up[mt][sLm1][(lyl * PX + lx) * 3];
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) {
-                                const int64_t dof = 3 * un_id + c;
-                                double F = 0.0;
-                                if (has_src)
-                                    for (int k = 0; k < p.nsrc; ++k)
-                                        if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
-                                const double uc = DAMP ? uv[c] : up[c];
-                                double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
-                                if constexpr (DAMP) b = __dsub_rn(b, __dmul_rn(p.ca, __dsub_rn(uc, upv[c])));
-                                double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
-                                if ((dm >> c) & 1) un = 0.0;
-                                (DAMP ? p.un : p.uo)[dof] = un;
-                                if (has_rec)
-                                    for (int k = 0; k < p.nrec; ++k)
-                                        if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
-                            }
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) p.fout[3 * un_id + c] = f[c];
-                        }
-                    }
-                }
-            }
-            if (r3cons && Lp >= Z0 - 1) {        // row 3 of layer Lp consumed: release its slot
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&S.r3empty[fslot(Lp)]);
+                fc[j] = f;
             }
         }
+        ptx::tc_fence_before();
+        // x-pairs: P(iy) of node (lx, ly) = own (-x,-y) corner + lane lx-1's (+x,-y) corner;
+        // the +y corners give P(iy-1) of node (lx, ly+1), exchanged through smem
+        double(*ys)[EX][3] = S.ysum[s3][hf];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double pm = __shfl_up_sync(0xffffffffu, fc[3 * 1 + c], 1);   // (+x,-y) of lx-1
+            const double pp = __shfl_up_sync(0xffffffffu, fc[3 * 2 + c], 1);   // (+x,+y) of lx-1
+            plo[c] = __dadd_rn(fc[3 * 0 + c], pm);
+            ys[ly][lx][c] = __dadd_rn(fc[3 * 3 + c], pp);
+        }
+    };
 
-        // ---- 4. epilogue of layer L: the 4 corner nodes of this thread's face ----
-        // (tile 0's row-3 warps first wait until tile 1 has consumed this slot's previous use)
-        if (r3prod && L <= Z1 - 1) ptx::mbar_wait(&S.r3empty[fslot(L)], fpar(L) ^ 1u);
-        if (layer_ok(L)) {
-            ptx::mbar_wait(&S.mbar[mt], phase);
-            phase ^= 1;
-            ptx::tc_fence_after();
-            // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
-            const double alpha = edeg ? 0.0 : -__dmul_rn(S.mc[mcur].y, __dmul_rn(es, ISCALE));
-            const uint32_t tb = S.tmem + ((uint32_t)(qd * 32) << 16) + mt * 256 + 24 * hf;
-            double fc[12];                               // [corner][c] of the face
-#pragma unroll
-            for (int rr = 0; rr < 3; ++rr) {             // 4 outputs per round (8 columns per array)
-                uint32_t R0[8], R1[8], R2[8] = {}, R3[8] = {};
-                ptx::tmem_ld8(tb + 0 + rr * 8, R0);
-                ptx::tmem_ld8(tb + 64 + rr * 8, R1);
-                if (NA > 2) ptx::tmem_ld8(tb + 128 + rr * 8, R2);
-                if (NA > 3) ptx::tmem_ld8(tb + 192 + rr * 8, R3);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int j = 4 * rr + q;
-                    const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
-                    const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
-                    const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
-                    const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
-                    // D holds −C_j, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^46
-                    const double dlo = limb_exact(c0, c1_, c2_, c3);
-                    const double dhi = NA > 2 ? limb_exact(c4, c5, c6, c7) : 0.0;
-                    const double Y = NA > 2 ? __fma_rn(dhi, 0x1p32, dlo) : dlo;    // RN(−y)
-                    const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
-                    if (MODE == MODE_DEBUG && edbg) {
-                        const int i = 12 * hf + j;
-                        const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};
-                        __int128 y = 0;
-#pragma unroll
-                        for (int jj = 7; jj >= 0; --jj) y = y * 256 - (__int128)Cj[jj];
-                        if (p.dbg_C)
-#pragma unroll
-                            for (int jj = 0; jj < 8; ++jj) p.dbg_C[edj * 192 + jj * 24 + i] = -Cj[jj];
-                        if (p.dbg_yhi) p.dbg_yhi[edj * 24 + i] = (long long)(y >> 64);
-                        if (p.dbg_ylo) p.dbg_ylo[edj * 24 + i] = (long long)(unsigned long long)y;
-                        if (p.dbg_fe) p.dbg_fe[edj * 24 + i] = f;
-                    }
-                    fc[j] = f;
-                }
-            }
-            ptx::tc_fence_before();
-            // x-pairs: P(iy) of node (lx, ly) = own (-x,-y) corner + lane lx-1's (+x,-y) corner;
-            // the +y corners give P(iy-1) of node (lx, ly+1), exchanged through smem
-            double(*ys)[EX][3] = S.ysum[fslot(L)][hf];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const double pm = __shfl_up_sync(0xffffffffu, fc[3 * 1 + c], 1);   // (+x,-y) of lx-1
-                const double pp = __shfl_up_sync(0xffffffffu, fc[3 * 2 + c], 1);   // (+x,+y) of lx-1
-                plo[c] = __dadd_rn(fc[3 * 0 + c], pm);
-                ys[ly][lx][c] = __dadd_rn(fc[3 * 3 + c], pp);
-            }
+    // ---- conversion of layer L (this thread's three chunks) and the MMA hand-off ----
+    auto convert = [&](int L, int sL, int sL1) {       // ring slots of planes L, L+1
+        const int64_t eid = ex + p.nx * (ey + p.ny * (int64_t)L);
+        const int64_t dj = eid - p.dbg_e0;
+        const bool dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < C::TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
+                         dj >= 0 && dj < p.dbg_ne;
+        // s_e from the per-node maxima of the two planes
+        const unsigned long long *m0 = S.nmax[sL], *m1 = S.nmax[sL1];
+        const int n0 = ly * PX + lx;
+        unsigned long long ab = m0[n0];
+        ab = max(ab, m0[n0 + 1]);
+        ab = max(ab, m0[n0 + PX]);
+        ab = max(ab, m0[n0 + PX + 1]);
+        ab = max(ab, m1[n0]);
+        ab = max(ab, m1[n0 + 1]);
+        ab = max(ab, m1[n0 + PX]);
+        ab = max(ab, m1[n0 + PX + 1]);
+        const double amax = __longlong_as_double((long long)ab);
+        const double cG = S.mc[mcur].x;
+        const double s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
+        const bool deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
+        const bool vzero = !ein || !(s >= 0x1p-1022);
+        const bool fast = (s <= 0x1.fffffffffffffp1023) && (vzero || s >= 0x1p-960);
+        uint8_t *Ab = &S.A[mt][0][0];
+        const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
+        double ue[16];
+        if (hf == 0) {
+            gather16<0>(ue, S.up[sL], S.up[sL1], lx, ly);
+            i8w_convert<MODE, M, 0>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
+            if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
+        } else {
+            gather16<1>(ue, S.up[sL], S.up[sL1], lx, ly);
+            i8w_convert<MODE, M, 1>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
         }
-        if (r3prod && L <= Z1 - 1) {             // element row 3 of layer L is in place
+        es = s;
+        edeg = deg;
+        em = mcur;
+        edbg = dbg;
+        edj = dj;
+        ptx::fence_proxy_async_smem();
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
+        if ((wu & 7) == 0) {     // first warp of the M-tile; one elected lane issues
+            const int mtu = wu >> 3;
+            if (ptx::elect_one()) {
+                ptx::tc_fence_after();
+                const uint32_t b0 = ptx::smem_u32(&S.B[0]);
+                const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
+                const uint32_t a0 = ptx::smem_u32(&S.A[mtu][0][0]);
+#pragma unroll
+                for (int pa = 0; pa < NA; ++pa) {
+                    const uint32_t abase = a0 + pa * A1_BYTES;
+                    const uint32_t d = S.tmem + mtu * 256 + pa * 64;
+#pragma unroll
+                    for (int ks = 0; ks < 3; ++ks)
+                        ptx::mma_i8(d, ptx::smem_desc(abase + ks * 256, 128, A1_PITCH),
+                                    ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC, ks > 0 ? 1u : 0u);
+                    ptx::mma_i8(d, ptx::smem_desc(abase + 3 * 128, 128, A1_PITCH),
+                                ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
+                    ptx::mma_i8(d, ptx::smem_desc(abase + 5 * 128, 128, A1_PITCH),
+                                ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
+                }
+                ptx::mma_commit(&S.mbar[mtu]);
+            }
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&S.r3full[fslot(L)]);
         }
-        // ---- 5. park plane L+2 (slot of plane L-2, no longer read) with its node maxima ----
-        if (pf && lrole) {
-            unsigned long long m = 0;
+    };
+
+    // ring slots of planes / layers L-2 .. L+2 (q5_k = (L-2+k) mod 5) and L-2 .. L (q3_k = (L-2+k) mod 3)
+    int q5_0 = ring5(Z0 - 3), q5_1 = ring5(Z0 - 2), q5_2 = ring5(Z0 - 1), q5_3 = ring5(Z0), q5_4 = ring5(Z0 + 1);
+    int q3_0 = ring3(Z0 - 3), q3_1 = ring3(Z0 - 2), q3_2 = ring3(Z0 - 1);
+    // running offsets of the prefetch (advanced once per iteration): plane L+2 of u, the material of
+    // layer L+2, the owned node of plane L - mt
+    int64_t ro_plane = 3 * PSTRIDE * (int64_t)(Z0 + 1);
+    const uint8_t *ro_mat = matp + mstride * (int64_t)(Z0 + 1);
+    int64_t ro_node = ucol + PSTRIDE * (int64_t)(Z0 - 1 - mt);
+    // half-iterations: h = 2L (even) and 2L+1 (odd); one copy of each phase body, selected per M-tile
+    double pfv[3] = {0.0, 0.0, 0.0};
+    bool pf = false;
+    int mfar = kZeroMat;
+    double upv_n[3] = {0.0, 0.0, 0.0}, wn_n = 0.0, uv_n[3] = {0.0, 0.0, 0.0};
+    uint8_t dm_n = 0;
+    for (int h = 2 * (Z0 - 1); h <= 2 * (Z1 + 1) + 1; ++h) {
+        const int L = h >> 1;
+        const bool odd = h & 1;
+        if (!odd) {
+            // ---- prefetch: plane L+2, material of layer L+2, update operands of the next post plane ----
+            const int pz = L + 2;
+            pf = (pz > Lfirst + 1) && (L + 1 < Z1) && (L + 1 < nz);
+            if (pf && ldn) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                S.up[mt][pz & 3][3 * li + c] = pfv[c];
-                const unsigned long long b = abs_bits(pfv[c]);
-                m = b > m ? b : m;
+                for (int c = 0; c < 3; ++c) pfv[c] = load_in(ro_plane + ldoff + c);
             }
-            S.nmax[mt][pz & 3][li] = m;
+            mfar = (ein && L + 2 < nz && L >= Lfirst) ? (int)__ldg(ro_mat) : kZeroMat;
+            const int Pn = L - mt;                    // plane this thread updates in the next iteration
+            if (MODE == MODE_STEP && upd_role && Pn >= Z0 && Pn <= nz && Pn < Z1) {
+                const int64_t un_next = ro_node;
+                upv_n[0] = p.uo[3 * un_next];
+                upv_n[1] = p.uo[3 * un_next + 1];
+                upv_n[2] = p.uo[3 * un_next + 2];
+                if constexpr (DAMP) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) uv_n[c] = __ldg(p.u + 3 * un_next + c);
+                }
+                wn_n = __ldg(p.w + un_next);
+                dm_n = p.dmask ? __ldg(p.dmask + un_next) : (uint8_t)0;
+            }
         }
-        if (L >= Lfirst) {
-            mcur = mnxt;
-            mnxt = mfar;
+        // M-tile 0: convert at even h, post-phase + epilogue at odd h; M-tile 1 the other way round
+        if (odd == (mt == 1)) {
+            if (layer_ok(L)) convert(L, q5_2, q5_3);
+        } else {
+            post_phase(L - 1 - mt, mt ? q3_0 : q3_1, mt ? q5_0 : q5_1);
+            if (layer_ok(L - mt)) epilogue(L - mt, mt ? q3_1 : q3_2);
         }
-        upv[0] = upv_n[0];
-        upv[1] = upv_n[1];
-        upv[2] = upv_n[2];
-        uv[0] = uv_n[0];
-        uv[1] = uv_n[1];
-        uv[2] = uv_n[2];
-        wn = wn_n;
-        dm = dm_n;
-        asm volatile("bar.sync %0, 256;" ::"r"(3 + mt) : "memory");   // end of layer, this M-tile
+        if (odd) {
+            // ---- park plane L+2 (slot of plane L-3, no longer read) with its node maxima ----
+            const int pz = L + 2;
+            if (pf && lrole) {
+                unsigned long long m = 0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    S.up[q5_4][3 * li + c] = pfv[c];
+                    const unsigned long long b = abs_bits(pfv[c]);
+                    m = b > m ? b : m;
+                }
+                S.nmax[q5_4][li] = m;
+            }
+            if (L >= Lfirst) {
+                mcur = mnxt;
+                mnxt = mfar;
+            }
+            upv[0] = upv_n[0];
+            upv[1] = upv_n[1];
+            upv[2] = upv_n[2];
+            uv[0] = uv_n[0];
+            uv[1] = uv_n[1];
+            uv[2] = uv_n[2];
+            wn = wn_n;
+            dm = dm_n;
+            upv_n[0] = upv_n[1] = upv_n[2] = 0.0;
+            ro_plane += 3 * PSTRIDE;
+            ro_mat += mstride;
+            ro_node += PSTRIDE;
+            {   // advance the ring slots to L+1 (rotation instead of a modulo per use)
+                const int t5 = q5_0;
+                q5_0 = q5_1; q5_1 = q5_2; q5_2 = q5_3; q5_3 = q5_4; q5_4 = t5;
+                const int t3 = q3_0;
+                q3_0 = q3_1; q3_1 = q3_2; q3_2 = t3;
+            }
+            wn_n = 0.0;
+            dm_n = 0;
+            __syncthreads();
+        }
     }
-    ptx::tc_fence_before();
-    __syncthreads();
     ptx::tc_fence_after();
     if (warp == 0) ptx::tmem_dealloc<C::TMEM_COLS>(S.tmem);
 }
