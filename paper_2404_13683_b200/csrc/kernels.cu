@@ -217,17 +217,6 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 #include "step_f64.cuh"
 
 #include "step_i8w.cuh"
-#include "step_i8c.cuh"
-
-// INT8 kernel: step_i8w (two threads per element, default) or step_i8c (three threads per element,
-// one per component); OVX_I8_KERNEL=c selects the latter.
-bool i8_three() {
-    static bool c = [] {
-        const char *e = getenv("OVX_I8_KERNEL");
-        return e && e[0] == 'c';
-    }();
-    return c;
-}
 
 template <int MODE, int M, bool DAMP>
 cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
@@ -242,27 +231,8 @@ cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int MODE, int M, bool DAMP>
-cudaError_t launch_i8c(const StepParams &p, int64_t ctas, cudaStream_t st) {
-    static bool attr = false;
-    const int smem = (int)sizeof(SmemI8C);
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_i8c<MODE, M, DAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    step_i8c<MODE, M, DAMP><<<(unsigned)ctas, I8C::NT, smem, st>>>(p);
-    return cudaGetLastError();
-}
-
 template <int M>
 cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
-    if (i8_three()) {
-        if (mode == MODE_STEP)
-            return p.damped ? launch_i8c<MODE_STEP, M, true>(p, ctas, st) : launch_i8c<MODE_STEP, M, false>(p, ctas, st);
-        if (mode == MODE_APPLY) return launch_i8c<MODE_APPLY, M, false>(p, ctas, st);
-        return launch_i8c<MODE_DEBUG, M, false>(p, ctas, st);
-    }
     if (mode == MODE_STEP)
         return p.damped ? launch_i8w<MODE_STEP, M, true>(p, ctas, st) : launch_i8w<MODE_STEP, M, false>(p, ctas, st);
     if (mode == MODE_APPLY) return launch_i8w<MODE_APPLY, M, false>(p, ctas, st);
@@ -399,8 +369,8 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
         const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + tyy - 1) / tyy;
         const int zc = choose_zchunk(nz + 1, tx * ty, 1);
         li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
-        li.threads = i8_three() ? I8C::NT : I8W::NT;
-        li.smem = i8_three() ? (int)sizeof(SmemI8C) : (int)sizeof(SmemI8W);
+        li.threads = I8W::NT;
+        li.smem = (int)sizeof(SmemI8W);
         return li;
     }
     if (path == OVX_FP64) return info_t<OVX_FP64>(nx, ny, nz);
