@@ -208,18 +208,24 @@ class Sharded:
         self.s = self.c.ovx
         self.nn = (n + 1) * (n + 1) * (self.slab.nzl + 1)
         self.ne = n * n * self.slab.nzl
-        self.launches_per_step = 1 + (1 if self.slab.flags & 1 else 0)
+        self.run = D.SlabRun.__new__(D.SlabRun)       # the overlapped schedule of dist.SlabRun
+        self.run.slab, self.run.compute, self.run.transport = self.slab, self.c, self.t
+        self.run._comm = None
+        self.launches_per_step = None                    # counted on the first step
 
     def set_state(self, u, up):
         self.c.set_state(u, up, 0)
 
     def step(self, k):
-        for _ in range(k):
-            self.c.begin()
-            self.t.exchange_up(self.slab, self.c.a_send, self.c.a_recv)
-            self.c.iface()
-            self.t.exchange_down(self.slab, self.c.u_send, self.c.u_recv)
-            self.c.end()
+        """Edge z-chunks first, then the NCCL exchange and the interface update on a second stream
+        while the interior chunks compute (dist.SlabRun.step(overlap=True))."""
+        if self.launches_per_step is None and k > 0:
+            _, n0 = self.s.get_timers()
+            self.run.step(1, overlap=True)
+            _, n1 = self.s.get_timers()
+            self.launches_per_step = n1 - n0
+            k -= 1
+        self.run.step(k, overlap=True)
 
     def get_state(self):
         return self.c.get_state()

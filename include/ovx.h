@@ -158,6 +158,16 @@ ovx_status ovx_set_iface_buffers(ovx_ctx *ctx, double *a_send, double *a_recv, d
 ovx_status ovx_step_begin(ovx_ctx *ctx);
 ovx_status ovx_step_iface(ovx_ctx *ctx);
 ovx_status ovx_step_end(ovx_ctx *ctx);
+/* Overlapped form (exchange overlapped with interior compute): ovx_step_begin is
+ * ovx_step_begin_part(0) (the first and last z-chunk of the slab — the CTAs that produce a_send and
+ * the plane-0 partial) followed by ovx_step_begin_part(1) (the interior chunks), both on the context
+ * stream.  Once part 0 has completed (an event recorded after it), the caller may exchange and call
+ * ovx_step_iface_stream on another stream while part 1 runs: the interior chunks neither read nor
+ * write plane 0, the top plane or the interface buffers.  ovx_step_end must be ordered after both
+ * (the context stream waits for the other stream).  stream: a cudaStream_t, NULL = default stream,
+ * OVX_LIBRARY_STREAM = the context stream.  Results are identical to the serial form. */
+ovx_status ovx_step_begin_part(ovx_ctx *ctx, int part);
+ovx_status ovx_step_iface_stream(ovx_ctx *ctx, void *stream);
 
 /* ---- parity hooks -------------------------------------------------------- */
 /* f = K u for one EBE product (same kernel as ovx_step, update disabled).

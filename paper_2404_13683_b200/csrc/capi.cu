@@ -569,7 +569,7 @@ static StepParams step_params(ovx_ctx *ctx) {
     return p;
 }
 
-ovx_status ovx_step_begin(ovx_ctx *ctx) {
+static ovx_status step_begin_impl(ovx_ctx *ctx, int part) {
     ovx_status s = need_ready(ctx);
     if (s) return s;
     if (!(ctx->dt > 0)) return fail(ctx, OVX_ESTATE, "set dt first");
@@ -578,18 +578,34 @@ ovx_status ovx_step_begin(ovx_ctx *ctx) {
     cudaSetDevice(ctx->device);
     s = ensure_constants(ctx);
     if (s) return s;
-    CK(launch_step(ctx->path, MODE_STEP, step_params(ctx), ctx->stream));
-    ctx->launches += 1;
+    int nl = 0;
+    CK(launch_step(ctx->path, MODE_STEP, step_params(ctx), ctx->stream, part, &nl));
+    ctx->launches += nl;
     return OVX_OK;
 }
 
-ovx_status ovx_step_iface(ovx_ctx *ctx) {
+ovx_status ovx_step_begin(ovx_ctx *ctx) { return step_begin_impl(ctx, -1); }
+
+ovx_status ovx_step_begin_part(ovx_ctx *ctx, int part) {
+    if (part != 0 && part != 1) return fail(ctx, OVX_EINVAL, "part must be 0 (edge chunks) or 1 (interior)");
+    return step_begin_impl(ctx, part);
+}
+
+static ovx_status step_iface_impl(ovx_ctx *ctx, cudaStream_t st) {
     ovx_status s = need_ready(ctx);
     if (s) return s;
     if (!(ctx->slab_flags & 1)) return OVX_OK;
     cudaSetDevice(ctx->device);
-    CK(launch_iface_update(step_params(ctx), ctx->a_recv, ctx->u_send, ctx->stream));
+    CK(launch_iface_update(step_params(ctx), ctx->a_recv, ctx->u_send, st));
+    ctx->launches += 1;
     return OVX_OK;
+}
+
+ovx_status ovx_step_iface(ovx_ctx *ctx) { return step_iface_impl(ctx, ctx ? ctx->stream : nullptr); }
+
+ovx_status ovx_step_iface_stream(ovx_ctx *ctx, void *stream) {
+    if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
+    return step_iface_impl(ctx, stream == OVX_LIBRARY_STREAM ? ctx->stream : (cudaStream_t)stream);
 }
 
 ovx_status ovx_step_end(ovx_ctx *ctx) {

@@ -378,13 +378,10 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
     return info_t<OVX_FP64_DENSE>(nx, ny, nz);
 }
 
-cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
-    const int ty = path == OVX_INT8 ? 8 - 1 : V1<OVX_FP64>::TY;
-    p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
-    p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
-    p.zchunk = choose_zchunk(p.nz + 1, (int64_t)p.tiles_x * p.tiles_y, path == OVX_INT8 ? 1 : 2);
-    const int64_t tz = (p.nz + 1 + p.zchunk - 1) / p.zchunk;
-    const int64_t ctas = (int64_t)p.tiles_x * p.tiles_y * tz;
+static cudaError_t launch_chunks(int path, int mode, StepParams p, cudaStream_t st, int c0, int c1) {
+    if (c1 <= c0) return cudaSuccess;
+    p.tz0 = c0;
+    const int64_t ctas = (int64_t)p.tiles_x * p.tiles_y * (c1 - c0);
     if (path == OVX_INT8) {
         if (p.stages == 4) return launch_i8_mode<4>(mode, p, ctas, st);
         if (p.stages == 6) return launch_i8_mode<6>(mode, p, ctas, st);
@@ -393,6 +390,32 @@ cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st) {
     if (path == OVX_FP64) return launch_mode<OVX_FP64>(mode, p, ctas, st);
     if (path == OVX_VFEM) return launch_mode<OVX_VFEM>(mode, p, ctas, st);
     return launch_mode<OVX_FP64_DENSE>(mode, p, ctas, st);   // OVX_FP64_DENSE and OVX_VFEM_DENSE (its matrices)
+}
+
+cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st, int part, int *nlaunch) {
+    const int ty = path == OVX_INT8 ? 8 - 1 : V1<OVX_FP64>::TY;
+    p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
+    p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
+    p.zchunk = choose_zchunk(p.nz + 1, (int64_t)p.tiles_x * p.tiles_y, path == OVX_INT8 ? 1 : 2);
+    const int n = (int)((p.nz + 1 + p.zchunk - 1) / p.zchunk);
+    int cnt = 0;
+    cudaError_t e = cudaSuccess;
+    auto go = [&](int c0, int c1) {
+        if (e == cudaSuccess && c1 > c0) {
+            e = launch_chunks(path, mode, p, st, c0, c1);
+            ++cnt;
+        }
+    };
+    if (part < 0) {
+        go(0, n);
+    } else if (part == 0) {
+        go(0, 1);
+        if (n > 1) go(n - 1, n);
+    } else {
+        go(1, n - 1);
+    }
+    if (nlaunch) *nlaunch = cnt;
+    return e;
 }
 
 cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, const uint8_t *mat_below,

@@ -56,6 +56,7 @@ struct StepParams {
     double *iface_bot_b;   // [NX1*NY1][3] the layer-0 bottom-face sum B of plane 0 (bit 0)
     // tiling
     int tiles_x, tiles_y, zchunk;
+    int tz0;               // first z-chunk of this launch (z-slab overlap: edge chunks, then the interior)
     // MODE_DEBUG outputs for elements [dbg_e0, dbg_e0 + dbg_ne)
     int64_t dbg_e0, dbg_ne;
     double *dbg_s;
@@ -76,7 +77,9 @@ struct LaunchInfo {
 cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, const double *kk,
                              const double *kg, cudaStream_t st);
 LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz);
-cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st);
+// part: -1 all z-chunks; 0 the first and the last chunk (the ones holding interface planes);
+// 1 the others.  Launching part 0 then part 1 computes the same step as part -1.
+cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st, int part = -1, int *nlaunch = nullptr);
 cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, const uint8_t *mat_below,
                           double dt, double *w, cudaStream_t st);
 cudaError_t launch_iface_update(const StepParams &p, const double *a_recv, double *u_send, cudaStream_t st);

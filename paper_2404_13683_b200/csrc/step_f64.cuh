@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     const int tx = bid % p.tiles_x;
     bid /= p.tiles_x;
     const int ty = bid % p.tiles_y;
-    const int tz = bid / p.tiles_y;
+    const int tz = p.tz0 + bid / p.tiles_y;            // z-chunk (a launch may cover a subrange)
     const int64_t X0 = (int64_t)tx * TX, Y0 = (int64_t)ty * TY;
     const int Z0 = tz * p.zchunk;
     const int Z1 = (int)min((int64_t)Z0 + p.zchunk, p.nz + 1);

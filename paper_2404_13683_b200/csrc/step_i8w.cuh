@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     const int tx = bid % p.tiles_x;
     bid /= p.tiles_x;
     const int ty = bid % p.tiles_y;
-    const int tz = bid / p.tiles_y;
+    const int tz = p.tz0 + bid / p.tiles_y;            // z-chunk (a launch may cover a subrange)
     const int64_t X0 = (int64_t)tx * TX, Y0 = (int64_t)ty * C::TY;
     const int Z0 = tz * p.zchunk;
     const int Z1 = (int)min((int64_t)Z0 + p.zchunk, p.nz + 1);

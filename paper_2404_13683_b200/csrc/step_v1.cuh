@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
     const int tx = bid % p.tiles_x;
     bid /= p.tiles_x;
     const int ty = bid % p.tiles_y;
-    const int tz = bid / p.tiles_y;
+    const int tz = p.tz0 + bid / p.tiles_y;            // z-chunk (a launch may cover a subrange)
     const int64_t X0 = (int64_t)tx * TX, Y0 = (int64_t)ty * TY;
     const int64_t Z0 = (int64_t)tz * p.zchunk;
     const int64_t Z1 = min(Z0 + (int64_t)p.zchunk, p.nz + 1);

@@ -7,6 +7,8 @@ single-GPU run: per step
             interface's top-face force sum T is left in a_send, plane 0's bottom-face sum B
             (layer 0) is kept on the device
     xchg A: a_send(r) -> a_recv(r+1)                                 (NCCL P2P over NVLink)
+    (overlap=True: the edge z-chunks run first, then the exchanges and the interface update run on
+     a second stream while the interior chunks compute)
     iface : owner forms f = T + B (the single-GPU order, reading U2), updates plane 0
     xchg u: u_send(r) -> u_recv(r-1)
     end   : the rank below installs the updated plane, swaps u / u_prev
@@ -145,8 +147,18 @@ class OvxCompute:
     def begin(self):
         self.ovx.step_begin()
 
+    def begin_edges(self):
+        """The first and last z-chunk: they produce a_send and the plane-0 partial."""
+        self.ovx.step_begin_part(0)
+
+    def begin_interior(self):
+        self.ovx.step_begin_part(1)
+
     def iface(self):
         self.ovx.step_iface()
+
+    def iface_on(self, stream):
+        self.ovx.step_iface_stream(stream)
 
     def end(self):
         self.ovx.step_end()
@@ -179,8 +191,29 @@ class SlabRun:
     def set_state(self, u_global, up_global, it: int = 0):
         self.compute.set_state(self._planes(u_global), self._planes(up_global), it)
 
-    def step(self, n: int = 1):
+    def step(self, n: int = 1, overlap: bool = False):
+        """overlap (CUDA compute only): the edge z-chunks run first; the exchange and the interface
+        update then run on a second stream while the interior chunks compute."""
         s, t, c = self.slab, self.transport, self.compute
+        if overlap and hasattr(c, "begin_edges"):
+            import torch
+            comp = torch.cuda.current_stream()
+            if getattr(self, "_comm", None) is None:
+                self._comm = torch.cuda.Stream()
+            comm = self._comm
+            for _ in range(n):
+                c.begin_edges()
+                ev = torch.cuda.Event()
+                ev.record(comp)
+                c.begin_interior()
+                with torch.cuda.stream(comm):
+                    comm.wait_event(ev)
+                    t.exchange_up(s, c.a_send, c.a_recv)
+                    c.iface_on(comm)
+                    t.exchange_down(s, c.u_send, c.u_recv)
+                comp.wait_stream(comm)
+                c.end()
+            return
         for _ in range(n):
             c.begin()
             t.exchange_up(s, c.a_send, c.a_recv)
@@ -208,7 +241,30 @@ class SlabGroup:
         for r in self.runs:
             r.set_state(u, up, it)
 
-    def step(self, n=1):
+    def step(self, n=1, overlap: bool = False):
+        if overlap:                    # the overlapped schedule of SlabRun.step, all ranks in lock step
+            import torch
+            comp = torch.cuda.current_stream()
+            if getattr(self, "_comm", None) is None:
+                self._comm = torch.cuda.Stream()
+            comm = self._comm
+            for _ in range(n):
+                for r in self.runs:
+                    r.compute.begin_edges()
+                ev = torch.cuda.Event()
+                ev.record(comp)
+                for r in self.runs:
+                    r.compute.begin_interior()
+                with torch.cuda.stream(comm):
+                    comm.wait_event(ev)
+                    self.lb.exchange_all_up(self.runs)
+                    for r in self.runs:
+                        r.compute.iface_on(comm)
+                    self.lb.exchange_all_down(self.runs)
+                comp.wait_stream(comm)
+                for r in self.runs:
+                    r.compute.end()
+            return
         for _ in range(n):
             for r in self.runs:
                 r.compute.begin()

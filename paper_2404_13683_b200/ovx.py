@@ -61,6 +61,8 @@ _SIGS = {
     "ovx_set_iface_buffers": [_vp, _vp, _vp, _vp, _vp],
     "ovx_step_begin": [_vp],
     "ovx_step_iface": [_vp],
+    "ovx_step_begin_part": [_vp, _int],
+    "ovx_step_iface_stream": [_vp, _vp],
     "ovx_step_end": [_vp],
     "ovx_set_receivers": [_vp, _int, _vp, _i64],
     "ovx_get_traces": [_vp, _vp],
@@ -301,6 +303,15 @@ class Ovx:
 
     def step_iface(self) -> None:
         self._call("ovx_step_iface")
+
+    def step_begin_part(self, part: int) -> None:
+        """0: the edge z-chunks (interface producers), 1: the interior chunks (ovx_step_begin_part)."""
+        self._call("ovx_step_begin_part", int(part))
+
+    def step_iface_stream(self, stream) -> None:
+        """Interface update on another stream (torch.cuda.Stream or raw handle; 0 = default)."""
+        raw = int(getattr(stream, "cuda_stream", stream))
+        self._call("ovx_step_iface_stream", _vp(raw) if raw else None)
 
     def step_end(self) -> None:
         self._call("ovx_step_end")
