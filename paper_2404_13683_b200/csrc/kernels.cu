@@ -207,6 +207,20 @@ __device__ __forceinline__ double limb_exact(int32_t c0, int32_t c1, int32_t c2,
     asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(acc) : "r"(p1), "r"(c_two16));
     return __longlong_as_double(acc) - 0x1.8p52;
 }
+// Biased stage products (INT8 kernel): the A operand's K-padding bytes are 255 and the matching B
+// entries 127 (16 bytes per row), so every accumulator D_j = −C_j + I8_BIAS with I8_BIAS =
+// 16·255·127 = 518160 > max|C_j| = 255·1258 = 320790 (max absolute row sum of K_D): all D_j > 0.
+// The limb p0 + 2^16 p1 (p0 = D0 + 256 D1, p1 = D2 + 256 D3, both in [0, 2^28)) then needs no sign
+// extension, and the bias comes out exactly with the magic: 1.5·2^52 + I8_BIAS·(1 + 2^8 + 2^16 + 2^24)
+// is an integer below 2^53.
+constexpr int32_t I8_BIAS = 16 * 255 * 127;
+constexpr double I8_LIMB_MAGIC = 0x1.8p52 + (double)I8_BIAS * 16843009.0;
+__device__ __forceinline__ double limb_biased(int32_t d0, int32_t d1, int32_t d2, int32_t d3) {
+    const uint32_t p0 = (uint32_t)(d0 + 256 * d1), p1 = (uint32_t)(d2 + 256 * d3);
+    unsigned long long acc = 0x4338000000000000ull + p0;
+    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(p1), "r"(c_two16));
+    return __longlong_as_double((long long)acc) - I8_LIMB_MAGIC;
+}
 // max_i |x_i| of finite / infinite doubles as the integer max of their magnitude bit patterns
 // (monotone for non-NaN values; a NaN sorts above +inf and makes the element degenerate)
 __device__ __forceinline__ unsigned long long abs_bits(double x) {

@@ -231,12 +231,14 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         const int n = r2 / 32, kb = r2 - n * 32;
         const int off = (n >> 3) * BI_PITCH + (kb >> 4) * 128 + (n & 7) * 16 + (kb & 15);
         const int k = 16 * s2 + (kb >> 1);
-        S.BI[s2][off] = ((kb & 1) == (n & 1) && k == (n >> 1)) ? (uint8_t)0x80 : (uint8_t)0;
+        // identity fold (−128 on the G bytes) and, against the A padding chunk, the accumulator bias
+        S.BI[s2][off] = (s2 == 1 && kb >= 16) ? (uint8_t)127
+                        : ((kb & 1) == (n & 1) && k == (n >> 1)) ? (uint8_t)0x80 : (uint8_t)0;
     }
-    for (int idx = t; idx < C::MT * 4 * 128; idx += NT) {
+    for (int idx = t; idx < C::MT * 4 * 128; idx += NT) {   // K-padding bytes: 255 (bias source)
         const int a = idx >> 7, r = idx & 127;
         *reinterpret_cast<uint4 *>(&S.A[a >> 2][a & 3][(r >> 3) * A1_PITCH + 6 * 128 + (r & 7) * 16]) =
-            make_uint4(0, 0, 0, 0);
+            make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
     }
     if (warp == 0) ptx::tmem_alloc<C::TMEM_COLS>(&S.tmem);
     if (t == 0)
@@ -358,15 +360,16 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
                 const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
                 const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
                 const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
-                const int32_t c6 = (int32_t)R3[2 * q], c7 = (int32_t)R3[2 * q + 1];
-                // D holds −C_j, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^46
-                const double dlo = limb_exact(c0, c1_, c2_, c3);
-                const double dhi = NA > 2 ? limb_exact(c4, c5, c6, c7) : 0.0;
+                const int32_t c6 = NA > 3 ? (int32_t)R3[2 * q] : I8_BIAS, c7 = NA > 3 ? (int32_t)R3[2 * q + 1] : I8_BIAS;
+                // D_j = −C_j + I8_BIAS, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^46
+                const double dlo = limb_biased(c0, c1_, c2_, c3);
+                const double dhi = NA > 2 ? limb_biased(c4, c5, c6, c7) : 0.0;
                 const double Y = NA > 2 ? __fma_rn(dhi, 0x1p32, dlo) : dlo;    // RN(−y)
                 const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
                 if (MODE == MODE_DEBUG && edbg) {
                     const int i = 12 * hf + j;
-                    const int32_t Cj[8] = {c0, c1_, c2_, c3, c4, c5, c6, c7};
+                    const int32_t Cj[8] = {c0 - I8_BIAS, c1_ - I8_BIAS, c2_ - I8_BIAS, c3 - I8_BIAS,
+                                           c4 - I8_BIAS, c5 - I8_BIAS, c6 - I8_BIAS, c7 - I8_BIAS};
                     __int128 y = 0;
 #pragma unroll
                     for (int jj = 7; jj >= 0; --jj) y = y * 256 - (__int128)Cj[jj];
