@@ -359,7 +359,8 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
                 const int j = 4 * rr + q;
                 const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
                 const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
-                const int32_t c4 = (int32_t)R2[2 * q], c5 = (int32_t)R2[2 * q + 1];
+                // stages beyond NA arrays are absent: give them the bias value (C_j = 0 after removal)
+                const int32_t c4 = NA > 2 ? (int32_t)R2[2 * q] : I8_BIAS, c5 = NA > 2 ? (int32_t)R2[2 * q + 1] : I8_BIAS;
                 const int32_t c6 = NA > 3 ? (int32_t)R3[2 * q] : I8_BIAS, c7 = NA > 3 ? (int32_t)R3[2 * q + 1] : I8_BIAS;
                 // D_j = −C_j + I8_BIAS, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^46
                 const double dlo = limb_biased(c0, c1_, c2_, c3);
