@@ -46,7 +46,7 @@ struct SmemI8W {
     alignas(128) uint8_t B[6 * B1_PITCH];
     alignas(128) uint8_t BI[2][6 * BI_PITCH];
     double up[5][I8W::PLANE];                       // ring: L-2, L-1 (updates), L, L+1 (gather), L+2
-    unsigned long long nmax[5][I8W::NODES];         // [slot of plane P] max |u_c| of each node over planes P, P+1
+    unsigned long long nmax[5][I8W::NODES];         // max_c |u_c| of each node (bit patterns)
     double ysum[3][2][I8W::EY][EX][3];              // [layer mod 3][face] x-pair P of the +y corners
     double tf[2][I8W::NE][3];                       // [layer parity][tile node] top-face sums T
     double2 mc[kMaxMat];                            // (cG, c1) per material, staged from c_mat
@@ -248,9 +248,6 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         const int id = i < p.nmat ? i : kZeroMat;
         S.mc[id] = make_double2(c_mat[id].cG, c_mat[id].c1);
     }
-    // node maxima: the loader of node li keeps the max of the last parked plane in mlast and writes
-    // the pair maximum over planes (P, P+1) when plane P+1 arrives
-    unsigned long long mlast = 0;
     for (int j = 0; j < 2; ++j) {
         const int iz = Lfirst + j;
         if (lrole) {
@@ -265,8 +262,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
                 const unsigned long long b = abs_bits(v3[c]);
                 m = b > m ? b : m;
             }
-            if (j == 1) S.nmax[ring5(Lfirst)][li] = m > mlast ? m : mlast;
-            mlast = m;
+            S.nmax[ring5(iz)][li] = m;
         }
     }
     ptx::fence_proxy_async_smem();
@@ -407,13 +403,17 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         const int64_t dj = eid - p.dbg_e0;
         const bool dbg = (MODE == MODE_DEBUG) && ein && lx < TX && ly < C::TY && (L + 1 >= Z0) && (L + 1 < Z1) &&
                          dj >= 0 && dj < p.dbg_ne;
-        // s_e from the node maxima over the two planes of the layer (pair maxima, 4 corners)
-        const unsigned long long *m0 = S.nmax[sL];
+        // s_e from the per-node maxima of the two planes
+        const unsigned long long *m0 = S.nmax[sL], *m1 = S.nmax[sL1];
         const int n0 = ly * PX + lx;
         unsigned long long ab = m0[n0];
         ab = max(ab, m0[n0 + 1]);
         ab = max(ab, m0[n0 + PX]);
         ab = max(ab, m0[n0 + PX + 1]);
+        ab = max(ab, m1[n0]);
+        ab = max(ab, m1[n0 + 1]);
+        ab = max(ab, m1[n0 + PX]);
+        ab = max(ab, m1[n0 + PX + 1]);
         const double amax = __longlong_as_double((long long)ab);
         const double cG = S.mc[mcur].x;
         const double s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
@@ -522,8 +522,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
                     const unsigned long long b = abs_bits(pfv[c]);
                     m = b > m ? b : m;
                 }
-                S.nmax[q5_3][li] = m > mlast ? m : mlast;   // planes L+1, L+2: layer L+1
-                mlast = m;
+                S.nmax[q5_4][li] = m;
             }
             if (L >= Lfirst) {
                 mcur = mnxt;
