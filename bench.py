@@ -39,8 +39,9 @@ def _peaks() -> dict:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "src": "measured (MEASURED_PEAKS.json)"}
-    return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "bf16_tflops": d.get("bf16_tflops", 1590.0),
+                "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
 
 
 class ClockSampler:
@@ -312,7 +313,7 @@ def main() -> None:
     e0.record(stream)
     R.set_state(uh, uh)
     R.step(args.steps)
-    _ = R.get_state()
+    u_final = R.get_state()[0]
     e1.record(stream)
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
@@ -325,6 +326,13 @@ def main() -> None:
         torch.cuda.empty_cache()
         R64, ms64, _ = timed_run(OVX_FP64, args.steps, args.warmup, False)
         fp64 = {"value": E_total * args.steps / (ms64 / 1e3), "ms_per_step": ms64 / args.steps}
+        if world == 1:   # BASELINE "L2 err vs FP64": the same K steps from the same field on both paths
+            R64.set_state(uh, uh)
+            R64.step(args.steps)
+            u64 = R64.get_state()[0]
+            fp64["l2_err_int8_vs_fp64"] = float(np.linalg.norm(u_final - u64) / np.linalg.norm(u64))
+            fp64["l2_err_steps"] = args.steps
+            del u64
         del R64
 
     if rank != 0:
@@ -360,6 +368,11 @@ def main() -> None:
         "dof_steps_per_s": 3 * nodes_total * args.steps / (ms / 1e3),
         "roofline": roof,
         "int8_tops_useful": (18432 * R_ne / (kernel_ms / 1e3) / 1e12) if (path == OVX_INT8 and kernel_ms) else None,
+        # BASELINE "INT8 tensor-pipe % peak": useful INT8 MACs×2 per second over the INT8 dense peak
+        # (2 × the measured bf16 TF/s, the guide's nominal int8:bf16 ratio); ncu pipe activity in
+        # profiles/r1_int8_v*.md (sm__pipe_tensor_cycles_active)
+        "int8_tensor_pct_of_peak": (100.0 * 18432 * R_ne / (kernel_ms / 1e3) / 1e12 / (2.0 * pk["bf16_tflops"]))
+                                   if (path == OVX_INT8 and kernel_ms) else None,
         "fp64_path": fp64,
         "clocks": clocks,
         "gpu_launches": R_lps * args.steps,
