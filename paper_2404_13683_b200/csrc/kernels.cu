@@ -1,22 +1,23 @@
 // kernels.cu — sm_100a kernels of the OVFEM / TCOVFEM explicit time step.
 //
-// One fused kernel per time step (DESIGN.md §Kernels):
-//   CTA  = a tile of TX×TY owned node columns marching in z over a chunk of node planes.
-//   Per element layer L it computes the 128 = (TX+1)(TY+1) elements touching its owned
-//   nodes (one halo element ring recomputed by the neighbour tile, so no cross-CTA
-//   reduction is needed), accumulates their forces into two shared-memory node planes
-//   in the node-local pairwise order of reading U2 (bit-identical to the oracle), and applies
-//   the central-difference update (Eq. 3, L263-L266 with the sign of Eq. 3)
-//   to each completed plane.
+// One fused kernel per time step (DESIGN.md §6):
+//   CTA  = a tile of 32 × 8 elements per layer (owned node columns 31 × 7; one halo element ring
+//   recomputed by the neighbour tiles, so no cross-CTA reduction), marching in z over a chunk of
+//   node planes (chunk count from a wave model).  Per element layer it computes the element
+//   forces, sums them into node forces in the pairwise order of reading U2 (bit-identical to the
+//   oracle) and applies the central-difference update (Eq. 3, L263-L266 with the sign
+//   of Eq. 3; Rayleigh damping, reading R1, optional) to each completed plane.
 //
-// Element force, two paths:
-//   OVX_FP64: f_e = (κ ds/256)·(K^κ u_e) + (G ds/384)·((K̄^G+128I) u_e), integer matrices
-//             applied first with sequential FP64 sums (DESIGN.md oracle (i) step 3).
-//   OVX_INT8: PAPER.md Eq. 9 via Eqs. 10-17: s_e = max|ū_e|, v = trunc(2^56 ū_e/s_e),
-//             byte slices of v + 2^56 (variant B) as the u8 A operand of
-//             tcgen05.mma.kind::i8 (M=128 elements, N=48, K=96, 4 half-word arrays),
-//             K_e^INT8 ⊗ I_2 as the resident s8 B operand, s32 accumulators in TMEM,
-//             exact two-limb recombination y = K_e^INT8 v and f_e = c1·(RN(y)·s_e 2^-56 + c2 u_e).
+// Kernels (paths of include/ovx.h):
+//   step_i8w  OVX_INT8: PAPER.md Eq. 9 via Eqs. 10-17 — s_e = max|ū_e|, v = trunc(2^{7M} ū_e/s_e),
+//             byte slices of v + 2^{7M} (variant B) as the u8 A operand of tcgen05.mma.kind::i8
+//             (M=128 elements, N=48, 4 half-word arrays), −K_e^INT8 ⊗ I_2 and the folded Eq. 9
+//             diagonal (variant D) as the resident s8 B operand, s32 accumulators in TMEM, exact
+//             two-limb recombination, f_e = RN(c1 s_e 2^{-7M})·RN(y).
+//   step_f64  OVX_FP64 / OVX_VFEM: factored FP64 element forces (Walsh-Hadamard modes of the
+//             corner values; OVFEM or trilinear VFEM weights), shuffle / SMEM node sums.
+//   step_v1   OVX_FP64_DENSE / OVX_VFEM_DENSE (and the FP64 z-slab / debug variants): the literal
+//             dense form with sequential _rn sums, a bit-exact mirror of the oracle.
 #include <algorithm>
 #include <cstdlib>
 
@@ -196,17 +197,8 @@ __device__ __forceinline__ void element_force_vfem_wht(const double (&ue)[24], c
     }
 }
 
-// Exact double of the limb c0 + 2^8 c1 + 2^16 c2 + 2^24 c3 of the stage products (|c_j| < 2^21,
-// so the pairs p0, p1 fit 32 bits and the limb |.| < 2^46): p0 + 2^16 p1 is formed in the low
-// bits of the double 1.5·2^52 (one IMAD.WIDE; the multiplier is read from constant memory so
-// ptxas keeps it a single wide multiply-add), then the magic is subtracted exactly.
+// multiplier of the limb's high pair, read from constant memory so ptxas keeps one wide multiply-add
 __constant__ int32_t c_two16 = 65536;
-__device__ __forceinline__ double limb_exact(int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
-    const int32_t p0 = c0 + 256 * c1, p1 = c2 + 256 * c3;
-    long long acc = 0x4338000000000000ll + (long long)p0;
-    asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(acc) : "r"(p1), "r"(c_two16));
-    return __longlong_as_double(acc) - 0x1.8p52;
-}
 // Biased stage products (INT8 kernel): the A operand's K-padding bytes are 255 and the matching B
 // entries 127 (16 bytes per row), so every accumulator D_j = −C_j + I8_BIAS with I8_BIAS =
 // 16·255·127 = 518160 > max|C_j| = 255·1258 = 320790 (max absolute row sum of K_D): all D_j > 0.

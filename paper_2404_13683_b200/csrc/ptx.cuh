@@ -23,22 +23,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-// Blocking wait with a suspend-time hint: the warp sleeps in hardware instead of spinning.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAITS_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-        "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(1000000u)
-        : "memory");
-}
-// 64-bit multiply-add of a signed 32-bit value: acc + (int64)a * b   (one IMAD.WIDE)
-__device__ __forceinline__ long long mad_wide(int32_t a, int32_t b, long long acc) {
-    long long r;
-    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(acc));
-    return r;
-}
 
 // One lane of a converged warp (elect.sync): keeps the tcgen05 issue code warp-uniform.
 __device__ __forceinline__ bool elect_one() {
@@ -88,15 +72,7 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
                  : "memory");
 }
 
-// ---- TMEM -> registers: 32 lanes x 16 columns of 32 bit (warp-collective) ----
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
+// ---- TMEM -> registers (warp-collective) ----
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
