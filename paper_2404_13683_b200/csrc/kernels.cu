@@ -17,7 +17,7 @@
 //   step_f64  OVX_FP64 / OVX_VFEM: factored FP64 element forces (Walsh-Hadamard modes of the
 //             corner values; OVFEM or trilinear VFEM weights), shuffle / SMEM node sums.
 //   step_v1   OVX_FP64_DENSE / OVX_VFEM_DENSE (and the FP64 z-slab / debug variants): the literal
-//             dense form with sequential _rn sums, a bit-exact mirror of the oracle.
+//             dense form with sequential _rn sums, a bit-exact mirror of the test oracle's definition.
 #include <algorithm>
 #include <cstdlib>
 
