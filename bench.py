@@ -194,8 +194,9 @@ class Single:
     def step(self, k):
         self.s.step(k)
 
-    def get_state(self):
-        return self.s.get_state()
+    def get_state(self, out_u=None):
+        """The step's result: the final displacement field u^{K} (into out_u, e.g. pinned)."""
+        return self.s.get_state(out_u=out_u, with_prev=False)[0]
 
 
 class Sharded:
@@ -228,8 +229,8 @@ class Sharded:
             k -= 1
         self.run.step(k, overlap=True)
 
-    def get_state(self):
-        return self.c.get_state()
+    def get_state(self, out_u=None):
+        return self.s.get_state(out_u=out_u, with_prev=False)[0]
 
 
 def main() -> None:
@@ -308,12 +309,13 @@ def main() -> None:
 
     # end to end through the public API with pinned host buffers (upload state, K steps, download)
     uh = torch.from_numpy(R.u0).pin_memory().numpy()
+    uout = torch.empty(R.u0.size, dtype=torch.float64).pin_memory().numpy()   # pinned result buffer
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     R.set_state(uh, uh)
     R.step(args.steps)
-    u_final = R.get_state()[0]
+    u_final = R.get_state(out_u=uout)
     e1.record(stream)
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
@@ -329,7 +331,7 @@ def main() -> None:
         if world == 1:   # BASELINE "L2 err vs FP64": the same K steps from the same field on both paths
             R64.set_state(uh, uh)
             R64.step(args.steps)
-            u64 = R64.get_state()[0]
+            u64 = R64.get_state()
             fp64["l2_err_int8_vs_fp64"] = float(np.linalg.norm(u_final - u64) / np.linalg.norm(u64))
             fp64["l2_err_steps"] = args.steps
             del u64
@@ -378,8 +380,9 @@ def main() -> None:
         "gpu_launches": R_lps * args.steps,
         "e2e": {"value": E_total * args.steps / (ms_e2e / 1e3), "unit": METRIC,
                 "h2d_bytes_per_step": 2 * 24 * R_nn / args.steps,
-                "d2h_bytes_per_step": 2 * 24 * R_nn / args.steps,
-                "note": f"per GPU: set_state(host pinned) + {args.steps} steps + get_state(host)"},
+                "d2h_bytes_per_step": 24 * R_nn / args.steps,
+                "note": f"per GPU: set_state(u, u_prev from pinned host) + {args.steps} steps + the result u^K "
+                        f"into a pinned host buffer (get_state)"},
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_oracle_sample(args.path, steps=8)   # ~10 s of oracle work

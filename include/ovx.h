@@ -122,6 +122,10 @@ ovx_status ovx_set_receivers(ovx_ctx *ctx, int n, const int64_t *node, int64_t n
 ovx_status ovx_get_traces(ovx_ctx *ctx, double *out);
 
 /* ---- state (u^{it}, u^{it-1}, it) is the complete state: also checkpoint/resume -- */
+/* Host arrays of 3*Nn doubles (node-major xyz), caller-owned; pinned memory makes the copies DMA.
+ * set: both arrays required; the uploaded state is checked on the device and a NaN/Inf anywhere
+ * gives OVX_EINVAL (the state is then unset).  get: u and/or u_prev may be NULL (skipped); it may
+ * be NULL.  Both synchronise the context stream. */
 ovx_status ovx_set_state(ovx_ctx *ctx, const double *u, const double *u_prev, int64_t it);
 ovx_status ovx_get_state(ovx_ctx *ctx, double *u, double *u_prev, int64_t *it);
 ovx_status ovx_set_state_device(ovx_ctx *ctx, const double *u, const double *u_prev, int64_t it);

@@ -407,11 +407,23 @@ static ovx_status set_state_impl(ovx_ctx *ctx, const double *u, const double *up
     if (!ctx->have_grid) return fail(ctx, OVX_ESTATE, "set grid first");
     if (!u || !up) return fail(ctx, OVX_EINVAL, "null state arrays");
     const int64_t n3 = 3 * ctx->nn();
-    if (kind == cudaMemcpyHostToDevice && (!finite_all(u, n3) || !finite_all(up, n3)))
-        return fail(ctx, OVX_EINVAL, "non-finite state");
     cudaSetDevice(ctx->device);
     CK(cudaMemcpyAsync(ctx->d_u, u, 8 * n3, kind, ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_up, up, 8 * n3, kind, ctx->stream));
+    if (kind == cudaMemcpyHostToDevice) {   // finiteness checked on the device (the host scan was serial)
+        int *d_flag = nullptr, h = 0;
+        CK(cudaMalloc(&d_flag, sizeof(int)));
+        CK(cudaMemsetAsync(d_flag, 0, sizeof(int), ctx->stream));
+        CK(launch_finite_check(ctx->d_u, n3, d_flag, ctx->stream));
+        CK(launch_finite_check(ctx->d_up, n3, d_flag, ctx->stream));
+        CK(cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(d_flag);
+        if (h) {
+            ctx->have_state = false;
+            return fail(ctx, OVX_EINVAL, "non-finite state");
+        }
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->it = it;
     ctx->have_state = true;

@@ -206,11 +206,17 @@ class Ovx:
             raise OvxError(OVX_EINVAL, "state size mismatch")
         self._call("ovx_set_state", _np_ptr(u), _np_ptr(up), it)
 
-    def get_state(self):
-        u = np.zeros(3 * self.n_nodes)
-        up = np.zeros(3 * self.n_nodes)
+    def get_state(self, out_u=None, out_up=None, with_prev: bool = True):
+        """(u, u_prev, it) on the host.  out_u / out_up: optional preallocated float64 arrays (e.g.
+        pinned); with_prev=False skips u_prev (returned as None)."""
+        n = 3 * self.n_nodes
+        u = np.empty(n) if out_u is None else out_u
+        up = (np.empty(n) if out_up is None else out_up) if with_prev else None
+        for a in (u, up):
+            if a is not None and (a.dtype != np.float64 or a.size != n or not a.flags.c_contiguous):
+                raise OvxError(OVX_EINVAL, "output arrays must be contiguous float64 of 3*n_nodes")
         it = np.zeros(1, dtype=np.int64)
-        self._call("ovx_get_state", _np_ptr(u), _np_ptr(up), _np_ptr(it))
+        self._call("ovx_get_state", _np_ptr(u), _np_ptr(up) if up is not None else None, _np_ptr(it))
         return u, up, int(it[0])
 
     def set_state_device(self, u, u_prev, it: int = 0) -> None:

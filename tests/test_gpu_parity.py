@@ -359,3 +359,23 @@ def test_e1_rebar_reduced_bit_exact(ovxmod):
         assert np.array_equal(u, ru) and np.array_equal(up, rup), path
         assert np.array_equal(tr, ref), path
         assert np.abs(tr).max() > 0
+
+
+def test_state_roundtrip_and_nonfinite_rejected(ovxmod):
+    """set_state checks finiteness on the device (OVX_EINVAL for a NaN/Inf anywhere); get_state
+    writes into caller-provided arrays and can skip u_prev."""
+    m = wl.small_random(6, 5, 4, ds=0.01)
+    s = _solver(ovxmod, m, 0)
+    u = wl.random_field(m)
+    up = wl.random_field(m, seed=3)
+    s.set_state(u, up, 7)
+    out = np.empty_like(u)
+    r, rp, it = s.get_state(out_u=out, with_prev=False)
+    assert r is out and rp is None and it == 7 and np.array_equal(out, u)
+    r, rp, _ = s.get_state()
+    assert np.array_equal(r, u) and np.array_equal(rp, up)
+    for bad in (np.nan, np.inf):
+        v = up.copy()
+        v[123] = bad
+        with pytest.raises(ovxmod.OvxError):
+            s.set_state(u, v, 0)
