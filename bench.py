@@ -312,13 +312,17 @@ def main() -> None:
     uout = torch.empty(R.u0.size, dtype=torch.float64).pin_memory().numpy()   # pinned result buffer
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    th0 = time.perf_counter()
     e0.record(stream)
     R.set_state(uh, uh)
+    th1 = time.perf_counter()
     R.step(args.steps)
     u_final = R.get_state(out_u=uout)
     e1.record(stream)
     barrier()
+    th2 = time.perf_counter()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    e2e_host_ms = {"set_state": 1e3 * (th1 - th0), "total": 1e3 * (th2 - th0)}
 
     # FP64 CUDA-core path measured beside the INT8 path (same workload, same clock record)
     R_nn, R_ne, R_lps = R.nn, R.ne, R.launches_per_step
@@ -382,7 +386,7 @@ def main() -> None:
                 "h2d_bytes_per_step": 2 * 24 * R_nn / args.steps,
                 "d2h_bytes_per_step": 24 * R_nn / args.steps,
                 "note": f"per GPU: set_state(u, u_prev from pinned host) + {args.steps} steps + the result u^K "
-                        f"into a pinned host buffer (get_state)"},
+                        f"into a pinned host buffer (get_state)", "host_ms": e2e_host_ms},
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_oracle_sample(args.path, steps=8)   # ~10 s of oracle work
