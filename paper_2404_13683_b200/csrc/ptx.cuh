@@ -22,7 +22,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-
+// Same, with a suspend-time hint: the warp sleeps in hardware until the phase completes (or the
+// hint expires) instead of spinning through issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
 
 // One lane of a converged warp (elect.sync): keeps the tcgen05 issue code warp-uniform.
 __device__ __forceinline__ bool elect_one() {

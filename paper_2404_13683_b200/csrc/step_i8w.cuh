@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
 
     // ---- epilogue of layer Le: the 4 corner nodes of this thread's face ----
     auto epilogue = [&](int Le, int s3) {              // s3: ysum slot of Le
-        ptx::mbar_wait(&S.mbar[mt], phase);
+        ptx::mbar_wait_sleep(&S.mbar[mt], phase);
         phase ^= 1;
         ptx::tc_fence_after();
         // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
