@@ -379,3 +379,29 @@ def test_state_roundtrip_and_nonfinite_rejected(ovxmod):
         v[123] = bad
         with pytest.raises(ovxmod.OvxError):
             s.set_state(u, v, 0)
+
+
+@pytest.mark.parametrize("name,path", [("int8", 0), ("fp64", 1)])
+def test_full_size_1000_steps_closed_form(ovxmod, name, path):
+    """BASELINE bar at the bench size: C2 (256³, the bench launch), 1000 steps from the standing P
+    wave (an exact lattice eigenmode of the roller box) against the closed-form amplitude
+    u^n = a_n u^0 (1-D lattice dispersion, PAPER.md Eq. 3 recurrence) — relative L2 ≤ 1e-10;
+    the INT8 path also within 1e-10 of the FP64 path."""
+    from oracle import physics
+    m = wl.c2_block(256)
+    u0 = wl.standing_wave(m, mvec=(16, 0, 0), U=(1.0, 0.0, 0.0))
+    k = math.pi * 16 / (m.nx * m.ds)
+    V = math.sqrt((m.kappa[0] + 4 * m.G[0] / 3) / m.rho[0])
+    lam = physics.lattice_lambda_axis(V, k, m.ds)
+    s = _solver(ovxmod, m, path)
+    s.set_state(u0, u0, 0)
+    s.step(1000)
+    u, _, _ = s.get_state(with_prev=False)
+    ref = physics.mode_amplitude(lam, m.dt, 1000) * u0
+    assert np.linalg.norm(u - ref) <= 1e-10 * np.linalg.norm(ref)
+    if path == 0:
+        s64 = _solver(ovxmod, m, 1)
+        s64.set_state(u0, u0, 0)
+        s64.step(1000)
+        u64, _, _ = s64.get_state(with_prev=False)
+        assert np.linalg.norm(u - u64) <= 1e-10 * np.linalg.norm(u64)
