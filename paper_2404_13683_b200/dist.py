@@ -7,8 +7,8 @@ single-GPU run: per step
             interface's top-face force sum T is left in a_send, plane 0's bottom-face sum B
             (layer 0) is kept on the device
     xchg A: a_send(r) -> a_recv(r+1)                                 (NCCL P2P over NVLink)
-    (overlap=True: the edge z-chunks run first, then the exchanges and the interface update run on
-     a second stream while the interior chunks compute)
+    (overlap=True: the edge z-chunks run on a second, high-priority stream concurrently with the
+     interior chunks; the exchanges and the interface update follow them on that stream)
     iface : owner forms f = T + B (the single-GPU order, reading U2), updates plane 0
     xchg u: u_send(r) -> u_recv(r-1)
     end   : the rank below installs the updated plane, swaps u / u_prev
@@ -122,7 +122,8 @@ class OvxCompute:
         self.ovx = Ovx(device)
         # the interface exchange (torch copies / NCCL P2P) is ordered against torch's current
         # stream, so the slab's kernels must run on that same stream
-        self.ovx.set_stream(stream if stream is not None else torch.cuda.current_stream(device))
+        self._stream = stream if stream is not None else torch.cuda.current_stream(device)
+        self.ovx.set_stream(self._stream)
         o = self.ovx
         o.set_grid(lm.nx, lm.ny, lm.nz, lm.ds)
         o.set_materials(lm.rho, lm.kappa, lm.G)
@@ -147,9 +148,18 @@ class OvxCompute:
     def begin(self):
         self.ovx.step_begin()
 
-    def begin_edges(self):
-        """The first and last z-chunk: they produce a_send and the plane-0 partial."""
-        self.ovx.step_begin_part(0)
+    def begin_edges(self, stream=None):
+        """The first and last z-chunk: they produce a_send and the plane-0 partial.  stream: launch
+        them on another stream (so they share the SMs with the interior launch instead of adding a
+        wave tail in front of it); the context stream is restored afterwards."""
+        if stream is None:
+            self.ovx.step_begin_part(0)
+            return
+        self.ovx.set_stream(stream)
+        try:
+            self.ovx.step_begin_part(0)
+        finally:
+            self.ovx.set_stream(self._stream)
 
     def begin_interior(self):
         self.ovx.step_begin_part(1)
@@ -199,15 +209,13 @@ class SlabRun:
             import torch
             comp = torch.cuda.current_stream()
             if getattr(self, "_comm", None) is None:
-                self._comm = torch.cuda.Stream()
+                self._comm = torch.cuda.Stream(priority=-1)   # edge chunks first when SMs free up
             comm = self._comm
             for _ in range(n):
-                c.begin_edges()
-                ev = torch.cuda.Event()
-                ev.record(comp)
-                c.begin_interior()
-                with torch.cuda.stream(comm):
-                    comm.wait_event(ev)
+                comm.wait_stream(comp)                # after the previous step's end
+                c.begin_edges(comm)                   # edge chunks on the high-priority stream
+                c.begin_interior()                    # interior chunks, concurrently, on comp
+                with torch.cuda.stream(comm):         # ordered after the edge chunks only
                     t.exchange_up(s, c.a_send, c.a_recv)
                     c.iface_on(comm)
                     t.exchange_down(s, c.u_send, c.u_recv)
@@ -246,17 +254,15 @@ class SlabGroup:
             import torch
             comp = torch.cuda.current_stream()
             if getattr(self, "_comm", None) is None:
-                self._comm = torch.cuda.Stream()
+                self._comm = torch.cuda.Stream(priority=-1)
             comm = self._comm
             for _ in range(n):
+                comm.wait_stream(comp)
                 for r in self.runs:
-                    r.compute.begin_edges()
-                ev = torch.cuda.Event()
-                ev.record(comp)
+                    r.compute.begin_edges(comm)
                 for r in self.runs:
                     r.compute.begin_interior()
                 with torch.cuda.stream(comm):
-                    comm.wait_event(ev)
                     self.lb.exchange_all_up(self.runs)
                     for r in self.runs:
                         r.compute.iface_on(comm)
