@@ -219,15 +219,16 @@ class Sharded:
         self.c.set_state(u, up, 0)
 
     def step(self, k):
-        """Edge z-chunks first, then the NCCL exchange and the interface update on a second stream
-        while the interior chunks compute (dist.SlabRun.step(overlap=True))."""
+        """Serial schedule (one launch over the slab, then the ~20-50 µs NCCL exchange and the
+        interface update): measured faster than the overlapped schedule, whose second launch costs
+        more in wave balance than the exchange it hides."""
         if self.launches_per_step is None and k > 0:
             _, n0 = self.s.get_timers()
-            self.run.step(1, overlap=True)
+            self.run.step(1, overlap=False)
             _, n1 = self.s.get_timers()
             self.launches_per_step = n1 - n0
             k -= 1
-        self.run.step(k, overlap=True)
+        self.run.step(k, overlap=False)
 
     def get_state(self, out_u=None):
         return self.s.get_state(out_u=out_u, with_prev=False)[0]
