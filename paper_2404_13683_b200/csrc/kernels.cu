@@ -224,25 +224,46 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 
 #include "step_i8w.cuh"
 
-template <int MODE, int M, bool DAMP>
+static_assert(2 * (sizeof(SmemI8<I8S>) + 1024) <= 233472, "two 16x8 INT8 CTAs must fit one SM");
+
+template <int MODE, int M, bool DAMP, class G>
 cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
-    const int smem = (int)sizeof(SmemI8W);
+    const int smem = (int)sizeof(SmemI8<G>);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        // all of the unified L1/shared array as shared memory, so G::CPS CTAs fit one SM
+        e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_i8w<MODE, M, DAMP><<<(unsigned)ctas, I8W::NT, smem, st>>>(p);
+    step_i8w<MODE, M, DAMP, G><<<(unsigned)ctas, G::NT, smem, st>>>(p);
     return cudaGetLastError();
+}
+
+// INT8 tile geometry: 32 × 8 elements, one CTA per SM with skewed M-tiles (default), or 16 × 8,
+// two CTAs per SM (OVX_I8_TILE=16; measured 2.34 vs 2.27 ms per C2 step: fewer barrier stalls,
+// but more pipe throttling and load latency — DESIGN.md §6.1).
+bool i8_wide() {
+    static const bool w = [] {
+        const char *e = std::getenv("OVX_I8_TILE");
+        return !(e && std::atoi(e) == 16);
+    }();
+    return w;
+}
+
+template <int M, class G>
+cudaError_t launch_i8_mode_g(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
+    if (mode == MODE_STEP)
+        return p.damped ? launch_i8w<MODE_STEP, M, true, G>(p, ctas, st) : launch_i8w<MODE_STEP, M, false, G>(p, ctas, st);
+    if (mode == MODE_APPLY) return launch_i8w<MODE_APPLY, M, false, G>(p, ctas, st);
+    return launch_i8w<MODE_DEBUG, M, false, G>(p, ctas, st);
 }
 
 template <int M>
 cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
-    if (mode == MODE_STEP)
-        return p.damped ? launch_i8w<MODE_STEP, M, true>(p, ctas, st) : launch_i8w<MODE_STEP, M, false>(p, ctas, st);
-    if (mode == MODE_APPLY) return launch_i8w<MODE_APPLY, M, false>(p, ctas, st);
-    return launch_i8w<MODE_DEBUG, M, false>(p, ctas, st);
+    return i8_wide() ? launch_i8_mode_g<M, I8W>(mode, p, ctas, st) : launch_i8_mode_g<M, I8S>(mode, p, ctas, st);
 }
 
 template <int PATH, int MODE, bool DAMP = false>
@@ -371,12 +392,12 @@ cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, c
 LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
     if (path == OVX_INT8) {
         LaunchInfo li;
-        const int tyy = 8 - 1;
-        const int64_t tx = (nx + 1 + TX - 1) / TX, ty = (ny + 1 + tyy - 1) / tyy;
-        const int zc = choose_zchunk(nz + 1, tx * ty, 1);
+        const int tx_ = i8_wide() ? I8W::TX : I8S::TX, tyy = I8W::TY, cps = i8_wide() ? I8W::CPS : I8S::CPS;
+        const int64_t tx = (nx + 1 + tx_ - 1) / tx_, ty = (ny + 1 + tyy - 1) / tyy;
+        const int zc = choose_zchunk(nz + 1, tx * ty, cps);
         li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
-        li.threads = I8W::NT;
-        li.smem = (int)sizeof(SmemI8W);
+        li.threads = i8_wide() ? I8W::NT : I8S::NT;
+        li.smem = i8_wide() ? (int)sizeof(SmemI8<I8W>) : (int)sizeof(SmemI8<I8S>);
         return li;
     }
     if (path == OVX_FP64) return info_t<OVX_FP64>(nx, ny, nz);
@@ -399,10 +420,12 @@ static cudaError_t launch_chunks(int path, int mode, StepParams p, cudaStream_t 
 }
 
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st, int part, int *nlaunch) {
-    const int ty = path == OVX_INT8 ? 8 - 1 : V1<OVX_FP64>::TY;
-    p.tiles_x = (int)((p.nx + 1 + TX - 1) / TX);
+    const int ty = path == OVX_INT8 ? I8W::TY : V1<OVX_FP64>::TY;
+    const int tx = path == OVX_INT8 ? (i8_wide() ? I8W::TX : I8S::TX) : TX;
+    const int cps = path == OVX_INT8 ? (i8_wide() ? I8W::CPS : I8S::CPS) : 2;
+    p.tiles_x = (int)((p.nx + 1 + tx - 1) / tx);
     p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
-    p.zchunk = choose_zchunk(p.nz + 1, (int64_t)p.tiles_x * p.tiles_y, path == OVX_INT8 ? 1 : 2);
+    p.zchunk = choose_zchunk(p.nz + 1, (int64_t)p.tiles_x * p.tiles_y, cps);
     const int n = (int)((p.nz + 1 + p.zchunk - 1) / p.zchunk);
     int cnt = 0;
     cudaError_t e = cudaSuccess;

@@ -28,7 +28,16 @@ constexpr int A1_BYTES = 16 * A1_PITCH;          // one half-word array of 128 r
 constexpr int B1_PITCH = 6 * 128;                // main B: 48 rows × 96 K-bytes
 constexpr int BI_PITCH = 2 * 128;                // identity blocks: 48 rows × 32 K-bytes
 
-struct I8W {
+// Tile geometry: EXv element columns × 8 rows per layer, MTv = EXv·8/128 M-tiles per CTA.
+//   I8G<32, 2>: 512 threads, one CTA per SM (≈215 KB smem, all 512 TMEM columns), the two M-tiles
+//               skewed by half an iteration inside the CTA;
+//   I8G<16, 1>: 256 threads, two CTAs per SM (≈113 KB smem, 256 TMEM columns each): no skew inside
+//               the CTA — the two resident CTAs overlap each other's barriers and phases.
+template <int EXv>
+struct I8G {
+    static constexpr int EX = EXv;                     // element columns per layer (x)
+    static constexpr int TX = EX - 1;                  // owned node columns (x)
+    static constexpr int PX = TX + 2;                  // node columns of a u plane held in smem
     static constexpr int EY = 8;
     static constexpr int NE = EX * EY;                 // elements per layer
     static constexpr int NT = 2 * NE;                  // threads
@@ -39,23 +48,28 @@ struct I8W {
     static constexpr int NODES = PX * PY;              // nodes of one u plane held in smem
     static constexpr int PLANE = NODES * 3;
     static constexpr int TMEM_COLS = MT * 256;
+    static constexpr int NS3 = MT == 2 ? 3 : 2;        // face-sum slots (the skew needs a third)
+    static constexpr int CPS = MT == 2 ? 1 : 2;        // resident CTAs per SM
 };
+using I8W = I8G<32>;
+using I8S = I8G<16>;
 
-struct SmemI8W {
-    uint8_t A[I8W::MT][4][A1_BYTES];      // [M-tile][half-word array], K-major canonical layout
+template <class G>
+struct SmemI8 {
+    uint8_t A[G::MT][4][A1_BYTES];        // [M-tile][half-word array], K-major canonical layout
     alignas(128) uint8_t B[6 * B1_PITCH];
     alignas(128) uint8_t BI[2][6 * BI_PITCH];
-    double up[5][I8W::PLANE];                       // ring: L-2, L-1 (updates), L, L+1 (gather), L+2
-    unsigned long long nmax[5][I8W::NODES];         // max_c |u_c| of each node (bit patterns)
-    double ysum[3][2][I8W::EY][EX][3];              // [layer mod 3][face] x-pair P of the +y corners
-    double tf[2][I8W::NE][3];                       // [layer parity][tile node] top-face sums T
+    double up[5][G::PLANE];                         // ring: L-2, L-1 (updates), L, L+1 (gather), L+2
+    unsigned long long nmax[5][G::NODES];           // max_c |u_c| of each node (bit patterns)
+    double ysum[G::NS3][2][G::EY][G::EX][3];        // [layer slot][face] x-pair P of the +y corners
+    double tf[2][G::NE][3];                         // [layer parity][tile node] top-face sums T
     double2 mc[kMaxMat];                            // (cG, c1) per material, staged from c_mat
-    uint64_t mbar[I8W::MT];
+    uint64_t mbar[G::MT];
     uint32_t tmem;
 };
 
 // ū values 8hf .. 8hf+15 of tile element (lx, ly) (local node order of reading Q1)
-template <int HF>
+template <int HF, int PX>
 __device__ __forceinline__ void gather16(double (&ue)[16], const double *lo, const double *hi, int lx, int ly) {
     const int cx[4] = {0, 1, 1, 0}, cy[4] = {0, 0, 1, 1};
 #pragma unroll
@@ -135,7 +149,8 @@ __device__ __forceinline__ void i8w_convert(const StepParams &p, const double (&
 }
 
 __device__ __forceinline__ int ring5(int x) { return (x + 10) % 5; }   // x >= -10
-__device__ __forceinline__ int ring3(int x) { return (x + 9) % 3; }    // x >= -9
+template <int NS3>
+__device__ __forceinline__ int ring3(int x) { return (x + 12) % NS3; }  // x >= -12
 
 // Skewed M-tiles: iteration L = half-iterations 2L, 2L+1 (one CTA barrier at its end)
 //   M-tile 0: [convert(L) -> MMA(L)] | [post-phase(L-1), epilogue(L)]
@@ -146,15 +161,16 @@ __device__ __forceinline__ int ring3(int x) { return (x + 9) % 3; }    // x >= -
 // DAMP (MODE_STEP only): Rayleigh damping, reading R1 — the smem planes hold the EBE input
 // ũ = u + cb·(u − u_prev) (node maxima of ũ), the update reads u and u_prev from global memory and
 // writes u^{it+1} to p.un.
-template <int MODE, int M, bool DAMP>
-__global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
-    using C = I8W;
+template <int MODE, int M, bool DAMP, class G>
+__global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
+    using C = G;
+    constexpr int EX = C::EX, TX = C::TX, PX = C::PX;
     constexpr int NB = (7 * M + 1 + 7) / 8;
     constexpr int NA = (NB + 1) / 2;
     constexpr double ISCALE = 1.0 / (double)(1ull << (7 * M));    // exact power of two
     constexpr int NT = C::NT, NODES = C::NODES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    SmemI8W &S = *reinterpret_cast<SmemI8W *>(smem_raw);
+    SmemI8<C> &S = *reinterpret_cast<SmemI8<C> *>(smem_raw);
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     const int wu = __shfl_sync(0xffffffffu, warp, 0);   // the warp index as a uniform value
@@ -177,7 +193,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
     auto layer_ok = [&](int x) { return x >= Lfirst && x < Lend; };
 
     // element (lx, ly) of the tile; its (-x,-y) corner is tile node (lx, ly)
-    const int lx = lane, ly = 4 * mt + qd;
+    const int lx = (128 * mt + row) % EX, ly = (128 * mt + row) / EX;
     const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
     const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
     const uint8_t *matp = p.mat + (ein ? ex + p.nx * ey : 0);
@@ -390,8 +406,8 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         double(*ys)[EX][3] = S.ysum[s3][hf];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const double pm = __shfl_up_sync(0xffffffffu, fc[3 * 1 + c], 1);   // (+x,-y) of lx-1
-            const double pp = __shfl_up_sync(0xffffffffu, fc[3 * 2 + c], 1);   // (+x,+y) of lx-1
+            const double pm = __shfl_up_sync(0xffffffffu, fc[3 * 1 + c], 1, EX);   // (+x,-y) of lx-1
+            const double pp = __shfl_up_sync(0xffffffffu, fc[3 * 2 + c], 1, EX);   // (+x,+y) of lx-1
             plo[c] = __dadd_rn(fc[3 * 0 + c], pm);
             ys[ly][lx][c] = __dadd_rn(fc[3 * 3 + c], pp);
         }
@@ -424,11 +440,11 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
         const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
         double ue[16];
         if (hf == 0) {
-            gather16<0>(ue, S.up[sL], S.up[sL1], lx, ly);
+            gather16<0, PX>(ue, S.up[sL], S.up[sL1], lx, ly);
             i8w_convert<MODE, M, 0>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
             if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
         } else {
-            gather16<1>(ue, S.up[sL], S.up[sL1], lx, ly);
+            gather16<1, PX>(ue, S.up[sL], S.up[sL1], lx, ly);
             i8w_convert<MODE, M, 1>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
         }
         es = s;
@@ -466,7 +482,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
 
     // ring slots of planes / layers L-2 .. L+2 (q5_k = (L-2+k) mod 5) and L-2 .. L (q3_k = (L-2+k) mod 3)
     int q5_0 = ring5(Z0 - 3), q5_1 = ring5(Z0 - 2), q5_2 = ring5(Z0 - 1), q5_3 = ring5(Z0), q5_4 = ring5(Z0 + 1);
-    int q3_0 = ring3(Z0 - 3), q3_1 = ring3(Z0 - 2), q3_2 = ring3(Z0 - 1);
+    int q3_0 = ring3<C::NS3>(Z0 - 3), q3_1 = ring3<C::NS3>(Z0 - 2), q3_2 = ring3<C::NS3>(Z0 - 1);
     // running offsets of the prefetch (advanced once per iteration): plane L+2 of u, the material of
     // layer L+2, the owned node of plane L - mt
     int64_t ro_plane = 3 * PSTRIDE * (int64_t)(Z0 + 1);
@@ -543,7 +559,7 @@ __global__ void __launch_bounds__(I8W::NT, 1) step_i8w(const StepParams p) {
             {   // advance the ring slots to L+1 (rotation instead of a modulo per use)
                 const int t5 = q5_0;
                 q5_0 = q5_1; q5_1 = q5_2; q5_2 = q5_3; q5_3 = q5_4; q5_4 = t5;
-                const int t3 = q3_0;
+                const int t3 = C::NS3 == 3 ? q3_0 : q3_1;   // two slots: (a, b, a) -> (b, a, b)
                 q3_0 = q3_1; q3_1 = q3_2; q3_2 = t3;
             }
             wn_n = 0.0;
