@@ -206,7 +206,7 @@ class Sharded:
         from paper_2404_13683_b200 import dist as D
         self.lm, self.slab, self.u0 = _slab_workload(n, world, rank)
         self.c = D.OvxCompute(self.lm, self.slab, local, path, stream=stream)
-        self.t = D.TorchTransport()
+        self.t = D.TorchTransport() if os.environ.get("OVX_BENCH_BACKEND", "nccl") == "nccl" else D.HostStagedTransport()
         self.s = self.c.ovx
         self.nn = (n + 1) * (n + 1) * (self.slab.nzl + 1)
         self.ne = n * n * self.slab.nzl
@@ -257,9 +257,17 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("OVX_BENCH_DEVICE") is not None:   # test hook: all ranks on one device
+        local = int(os.environ["OVX_BENCH_DEVICE"])
     torch.cuda.set_device(local)
+    # OVX_BENCH_BACKEND=gloo (test hook, with OVX_BENCH_DEVICE): several ranks on one GPU, the
+    # interface messages staged through host memory; the benchmark itself uses NCCL
+    backend = os.environ.get("OVX_BENCH_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     paths = {"int8": OVX_INT8, "fp64": OVX_FP64, "fp64_dense": OVX_FP64_DENSE, "vfem": OVX_VFEM,
              "vfem_dense": OVX_VFEM_DENSE}
     path = paths[args.path]
@@ -274,7 +282,7 @@ def main() -> None:
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device="cuda")
+        t = torch.tensor([x], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -327,6 +335,10 @@ def main() -> None:
 
     # FP64 CUDA-core path measured beside the INT8 path (same workload, same clock record)
     R_nn, R_ne, R_lps = R.nn, R.ne, R.launches_per_step
+    if world > 1:   # the job's launches: step kernels of every rank + the interface updates
+        t = torch.tensor([float(R_lps)], device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        R_lps = int(t.item())
     fp64 = None
     if path == OVX_INT8 and not args.no_fp64_companion:
         del R
@@ -370,7 +382,9 @@ def main() -> None:
                                 f"C5: {args.n}x{args.n}x{args.n * world} homogeneous block, {args.n}^3 z-slab per GPU"),
                    "material": "kappa=5/3, G=1, rho=1, ds=1, rollers", "path": args.path,
                    "elements": E_total, "nodes": nodes_total,
-                   "parallelism": "single GPU" if world == 1 else f"z-slabs x{world}, NCCL P2P interface exchange",
+                   "parallelism": "single GPU" if world == 1 else
+                   (f"z-slabs x{world}, NCCL P2P interface exchange" if backend == "nccl" else
+                    f"z-slabs x{world} on one device, {backend} host-staged interface exchange (test hook)"),
                    "l2": "inputs larger than L2 (%.2f GB touched per step per GPU)" % (_algorithmic_bytes(R_nn, R_ne) / 1e9)},
         "dof_steps_per_s": 3 * nodes_total * args.steps / (ms / 1e3),
         "roofline": roof,

@@ -100,6 +100,26 @@ class TorchTransport:
         self._run(ops)
 
 
+class HostStagedTransport(TorchTransport):
+    """TorchTransport for a CPU-only backend (gloo) with device buffers: each message is staged
+    through host memory.  A test hook (several ranks sharing one GPU, which NCCL refuses); the
+    NCCL transport moves device buffers directly."""
+
+    def _run(self, ops):
+        if not ops:
+            return
+        staged = []
+        for op in ops:
+            h = op.tensor.detach().to("cpu")
+            staged.append((op, h))
+        reqs = self.dist.batch_isend_irecv([self.dist.P2POp(op.op, h, op.peer, op.group) for op, h in staged])
+        for req in reqs:
+            req.wait()
+        for op, h in staged:
+            if op.op is self.dist.irecv:
+                op.tensor.copy_(h)
+
+
 class LoopbackTransport:
     """All ranks in one process (tests on one device): exchanges are plain tensor copies.
     Use with SlabGroup, which runs the per-rank phases in lock step."""
