@@ -20,6 +20,7 @@
 //             dense form with sequential _rn sums, a bit-exact mirror of the test oracle's definition.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "ovx_internal.h"
 #include "ptx.cuh"
@@ -224,46 +225,54 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 
 #include "step_i8w.cuh"
 
-static_assert(2 * (sizeof(SmemI8<I8S>) + 1024) <= 233472, "two 16x8 INT8 CTAs must fit one SM");
+static_assert(2 * (sizeof(SmemI8<I8S, false>) + 1024) <= 233472, "two 16x8 INT8 CTAs must fit one SM");
 
-template <int MODE, int M, bool DAMP, class G>
+template <int MODE, int M, bool DAMP, class G, bool TA>
 cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
-    const int smem = (int)sizeof(SmemI8<G>);
+    const int smem = (int)sizeof(SmemI8<G, TA>);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         // all of the unified L1/shared array as shared memory, so G::CPS CTAs fit one SM
-        e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G, TA>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    step_i8w<MODE, M, DAMP, G><<<(unsigned)ctas, G::NT, smem, st>>>(p);
+    step_i8w<MODE, M, DAMP, G, TA><<<(unsigned)ctas, G::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-// INT8 tile geometry: 32 × 8 elements, one CTA per SM with skewed M-tiles (default), or 16 × 8,
-// two CTAs per SM (OVX_I8_TILE=16; measured 2.34 vs 2.27 ms per C2 step: fewer barrier stalls,
-// but more pipe throttling and load latency — DESIGN.md §6.1).
-bool i8_wide() {
-    static const bool w = [] {
-        const char *e = std::getenv("OVX_I8_TILE");
-        return !(e && std::atoi(e) == 16);
+// INT8 kernel variant (OVX_I8_KERNEL): "tmem" (default) 32 × 8 tiles, skewed M-tiles, the A operand
+// in TMEM (the MMAs read only B from shared memory); "smem" the same with A in shared memory;
+// "smem16" 16 × 8 tiles, two CTAs per SM, A in shared memory.  DESIGN.md §6.1 has the measurements.
+int i8_variant() {
+    static const int v = [] {
+        const char *e = std::getenv("OVX_I8_KERNEL");
+        if (e && std::strcmp(e, "smem") == 0) return 1;
+        if (e && std::strcmp(e, "smem16") == 0) return 2;
+        return 0;
     }();
-    return w;
+    return v;
 }
+bool i8_wide() { return i8_variant() != 2; }
 
-template <int M, class G>
+template <int M, class G, bool TA>
 cudaError_t launch_i8_mode_g(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
     if (mode == MODE_STEP)
-        return p.damped ? launch_i8w<MODE_STEP, M, true, G>(p, ctas, st) : launch_i8w<MODE_STEP, M, false, G>(p, ctas, st);
-    if (mode == MODE_APPLY) return launch_i8w<MODE_APPLY, M, false, G>(p, ctas, st);
-    return launch_i8w<MODE_DEBUG, M, false, G>(p, ctas, st);
+        return p.damped ? launch_i8w<MODE_STEP, M, true, G, TA>(p, ctas, st)
+                        : launch_i8w<MODE_STEP, M, false, G, TA>(p, ctas, st);
+    if (mode == MODE_APPLY) return launch_i8w<MODE_APPLY, M, false, G, TA>(p, ctas, st);
+    return launch_i8w<MODE_DEBUG, M, false, G, TA>(p, ctas, st);
 }
 
 template <int M>
 cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
-    return i8_wide() ? launch_i8_mode_g<M, I8W>(mode, p, ctas, st) : launch_i8_mode_g<M, I8S>(mode, p, ctas, st);
+    switch (i8_variant()) {
+    case 1: return launch_i8_mode_g<M, I8W, false>(mode, p, ctas, st);
+    case 2: return launch_i8_mode_g<M, I8S, false>(mode, p, ctas, st);
+    default: return launch_i8_mode_g<M, I8W, true>(mode, p, ctas, st);
+    }
 }
 
 template <int PATH, int MODE, bool DAMP = false>
@@ -397,7 +406,8 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
         const int zc = choose_zchunk(nz + 1, tx * ty, cps);
         li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
         li.threads = i8_wide() ? I8W::NT : I8S::NT;
-        li.smem = i8_wide() ? (int)sizeof(SmemI8<I8W>) : (int)sizeof(SmemI8<I8S>);
+        li.smem = i8_variant() == 0 ? (int)sizeof(SmemI8<I8W, true>)
+                  : i8_variant() == 1 ? (int)sizeof(SmemI8<I8W, false>) : (int)sizeof(SmemI8<I8S, false>);
         return li;
     }
     if (path == OVX_FP64) return info_t<OVX_FP64>(nx, ny, nz);

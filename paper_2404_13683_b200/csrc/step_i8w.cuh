@@ -54,9 +54,9 @@ struct I8G {
 using I8W = I8G<32>;
 using I8S = I8G<16>;
 
-template <class G>
+template <class G, bool TA>
 struct SmemI8 {
-    uint8_t A[G::MT][4][A1_BYTES];        // [M-tile][half-word array], K-major canonical layout
+    uint8_t A[G::MT][4][TA ? 16 : A1_BYTES];   // [M-tile][half-word array], K-major canonical layout (TA: in TMEM)
     alignas(128) uint8_t B[6 * B1_PITCH];
     alignas(128) uint8_t BI[2][6 * BI_PITCH];
     double up[5][G::PLANE];                         // ring: L-2, L-1 (updates), L, L+1 (gather), L+2
@@ -80,9 +80,14 @@ __device__ __forceinline__ void gather16(double (&ue)[16], const double *lo, con
     }
 }
 
-template <int MODE, int M, int HF, bool FAST>
+// TMEM layout of the TA (A operand in TMEM) kernel, 512 columns: D of M-tile mt, array pa at
+// mt·192 + pa·48 (48 columns = N); A (shared by the two skewed M-tiles) at 384 + pa·28 + 4·chunk.
+constexpr uint32_t TA_D_TILE = 192, TA_D_ARR = 48, TA_A0 = 384, TA_A_ARR = 28;
+
+template <int MODE, int M, int HF, bool FAST, bool TA>
 __device__ __forceinline__ void i8w_chunks(const StepParams &p, const double (&ue)[16], double cG, double r, double R,
-                                           bool deg, uint8_t *Ab, uint32_t rowoff, bool dbg, int64_t dj) {
+                                           bool deg, uint8_t *Ab, uint32_t rowoff, bool dbg, int64_t dj,
+                                           uint32_t ta, uint64_t *xbar, uint32_t xpar) {
     constexpr int NB = (7 * M + 1 + 7) / 8;
     constexpr int NA = (NB + 1) / 2;
     constexpr double SCALE = (double)(1ull << (7 * M));
@@ -121,6 +126,10 @@ __device__ __forceinline__ void i8w_chunks(const StepParams &p, const double (&u
             }
         }
         const uint32_t off = rowoff + (uint32_t)ch * 128;
+        if (TA && cc == 0) {   // the shared TMEM A: the other M-tile's MMAs must have read it
+            ptx::mbar_wait(xbar, xpar);
+            ptx::tc_fence_after();
+        }
 #pragma unroll
         for (int pa = 0; pa < NA; ++pa) {
             const uint32_t *src = pa < 2 ? lo : hi;
@@ -130,22 +139,25 @@ __device__ __forceinline__ void i8w_chunks(const StepParams &p, const double (&u
             wv.y = __byte_perm(src[2], src[3], sel);
             wv.z = __byte_perm(src[4], src[5], sel);
             wv.w = __byte_perm(src[6], src[7], sel);
-            *reinterpret_cast<uint4 *>(Ab + pa * A1_BYTES + off) = wv;
+            if constexpr (TA)
+                ptx::tmem_st4(ta + pa * TA_A_ARR + 4 * ch, wv.x, wv.y, wv.z, wv.w);
+            else
+                *reinterpret_cast<uint4 *>(Ab + pa * A1_BYTES + off) = wv;
         }
     }
 }
 
-template <int MODE, int M, int HF>
+template <int MODE, int M, int HF, bool TA>
 __device__ __forceinline__ void i8w_convert(const StepParams &p, const double (&ue)[16], double cG, double s,
                                             bool deg, bool vzero, bool fast, uint8_t *Ab, uint32_t rowoff,
-                                            bool dbg, int64_t dj) {
+                                            bool dbg, int64_t dj, uint32_t ta, uint64_t *xbar, uint32_t xpar) {
     constexpr double SCALE = (double)(1ull << (7 * M));
     const double r = 1.0 / s;                                  // RN(1/s_e), reading Q7
     const double R = vzero ? 0.0 : __dmul_rn(r, SCALE);        // exact power-of-two scaling
     if (__all_sync(0xffffffffu, fast))
-        i8w_chunks<MODE, M, HF, true>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj);
+        i8w_chunks<MODE, M, HF, true, TA>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj, ta, xbar, xpar);
     else
-        i8w_chunks<MODE, M, HF, false>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj);
+        i8w_chunks<MODE, M, HF, false, TA>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj, ta, xbar, xpar);
 }
 
 __device__ __forceinline__ int ring5(int x) { return (x + 10) % 5; }   // x >= -10
@@ -161,8 +173,9 @@ __device__ __forceinline__ int ring3(int x) { return (x + 12) % NS3; }  // x >= 
 // DAMP (MODE_STEP only): Rayleigh damping, reading R1 — the smem planes hold the EBE input
 // ũ = u + cb·(u − u_prev) (node maxima of ũ), the update reads u and u_prev from global memory and
 // writes u^{it+1} to p.un.
-template <int MODE, int M, bool DAMP, class G>
+template <int MODE, int M, bool DAMP, class G, bool TA>
 __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
+    static_assert(!TA || G::MT == 2, "the TMEM A operand is shared by two skewed M-tiles");
     using C = G;
     constexpr int EX = C::EX, TX = C::TX, PX = C::PX;
     constexpr int NB = (7 * M + 1 + 7) / 8;
@@ -170,7 +183,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     constexpr double ISCALE = 1.0 / (double)(1ull << (7 * M));    // exact power of two
     constexpr int NT = C::NT, NODES = C::NODES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    SmemI8<C> &S = *reinterpret_cast<SmemI8<C> *>(smem_raw);
+    SmemI8<C, TA> &S = *reinterpret_cast<SmemI8<C, TA> *>(smem_raw);
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     const int wu = __shfl_sync(0xffffffffu, warp, 0);   // the warp index as a uniform value
@@ -251,6 +264,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         S.BI[s2][off] = (s2 == 1 && kb >= 16) ? (uint8_t)127
                         : ((kb & 1) == (n & 1) && k == (n >> 1)) ? (uint8_t)0x80 : (uint8_t)0;
     }
+    if (!TA)
     for (int idx = t; idx < C::MT * 4 * 128; idx += NT) {   // K-padding bytes: 255 (bias source)
         const int a = idx >> 7, r = idx & 127;
         *reinterpret_cast<uint4 *>(&S.A[a >> 2][a & 3][(r >> 3) * A1_PITCH + 6 * 128 + (r & 7) * 16]) =
@@ -285,8 +299,16 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    if (TA && wu < 4) {   // K-padding chunk 6 of the TMEM A arrays: 255 bytes (bias source), written once
+#pragma unroll
+        for (int pa = 0; pa < 4; ++pa)
+            ptx::tmem_st4(S.tmem + ((uint32_t)(qd * 32) << 16) + TA_A0 + pa * TA_A_ARR + 24, ~0u, ~0u, ~0u, ~0u);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();   // ordered before the first MMA by the M-tile barrier of convert()
+    }
 
     uint32_t phase = 0;
+    uint32_t xpar = mt == 0 ? 1u : 0u;   // TA: parity of the other M-tile's MMA completion to wait for
     int mcur = (ein && Lfirst < nz) ? (int)__ldg(matp + mstride * Lfirst) : kZeroMat;
     int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matp + mstride * (Lfirst + 1)) : kZeroMat;
     double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;   // update operands of this M-tile's post-phase plane
@@ -360,15 +382,16 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         ptx::tc_fence_after();
         // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
         const double alpha = edeg ? 0.0 : -__dmul_rn(S.mc[em].y, __dmul_rn(es, ISCALE));
-        const uint32_t tb = S.tmem + ((uint32_t)(qd * 32) << 16) + mt * 256 + 24 * hf;
+        constexpr uint32_t DARR = TA ? TA_D_ARR : 64;
+        const uint32_t tb = S.tmem + ((uint32_t)(qd * 32) << 16) + mt * (TA ? TA_D_TILE : 256) + 24 * hf;
         double fc[12];                               // [corner][c] of the face
 #pragma unroll
         for (int rr = 0; rr < 3; ++rr) {             // 4 outputs per round (8 columns per array)
             uint32_t R0[8], R1[8], R2[8] = {}, R3[8] = {};
             ptx::tmem_ld8(tb + 0 + rr * 8, R0);
-            ptx::tmem_ld8(tb + 64 + rr * 8, R1);
-            if (NA > 2) ptx::tmem_ld8(tb + 128 + rr * 8, R2);
-            if (NA > 3) ptx::tmem_ld8(tb + 192 + rr * 8, R3);
+            ptx::tmem_ld8(tb + DARR + rr * 8, R1);
+            if (NA > 2) ptx::tmem_ld8(tb + 2 * DARR + rr * 8, R2);
+            if (NA > 3) ptx::tmem_ld8(tb + 3 * DARR + rr * 8, R3);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -439,13 +462,20 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         uint8_t *Ab = &S.A[mt][0][0];
         const uint32_t rowoff = (uint32_t)((row >> 3) * A1_PITCH + (row & 7) * 16);
         double ue[16];
+        const uint32_t ta = S.tmem + ((uint32_t)(qd * 32) << 16) + TA_A0;
+        uint64_t *xbar = &S.mbar[C::MT - 1 - mt];
         if (hf == 0) {
             gather16<0, PX>(ue, S.up[sL], S.up[sL1], lx, ly);
-            i8w_convert<MODE, M, 0>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
+            i8w_convert<MODE, M, 0, TA>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj, ta, xbar, xpar);
             if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
         } else {
             gather16<1, PX>(ue, S.up[sL], S.up[sL1], lx, ly);
-            i8w_convert<MODE, M, 1>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj);
+            i8w_convert<MODE, M, 1, TA>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj, ta, xbar, xpar);
+        }
+        xpar ^= 1u;
+        if (TA) {
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
         }
         es = s;
         edeg = deg;
@@ -463,6 +493,16 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
                 const uint32_t a0 = ptx::smem_u32(&S.A[mtu][0][0]);
 #pragma unroll
                 for (int pa = 0; pa < NA; ++pa) {
+                    if constexpr (TA) {   // A from TMEM: column 8·ks = chunks 2ks, 2ks+1; identity: chunks 3-4, 5-6
+                        const uint32_t at = S.tmem + TA_A0 + pa * TA_A_ARR;
+                        const uint32_t d = S.tmem + mtu * TA_D_TILE + pa * TA_D_ARR;
+#pragma unroll
+                        for (int ks = 0; ks < 3; ++ks)
+                            ptx::mma_i8_ts(d, at + 8 * ks, ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC,
+                                           ks > 0 ? 1u : 0u);
+                        ptx::mma_i8_ts(d, at + 12, ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
+                        ptx::mma_i8_ts(d, at + 20, ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
+                    } else {
                     const uint32_t abase = a0 + pa * A1_BYTES;
                     const uint32_t d = S.tmem + mtu * 256 + pa * 64;
 #pragma unroll
@@ -473,6 +513,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
                                 ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
                     ptx::mma_i8(d, ptx::smem_desc(abase + 5 * 128, 128, A1_PITCH),
                                 ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
+                    }
                 }
                 ptx::mma_commit(&S.mbar[mtu]);
             }
