@@ -499,3 +499,9 @@ cudaError_t launch_finite_check(const double *u, int64_t n, int *flag, cudaStrea
 }
 
 }  // namespace ovx
+
+#ifdef OVX_TRACE
+extern "C" int ovx_trace_read(unsigned long long *host) {
+    return (int)cudaMemcpyFromSymbol(host, ovx::g_tr, sizeof(unsigned long long) * TRH * 16 * TRN);
+}
+#endif

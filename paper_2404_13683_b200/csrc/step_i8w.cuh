@@ -20,6 +20,18 @@
 //     with the sign of Eq. 3).  This post-phase of layer L-1 runs while the MMAs of layer L are
 //     in flight.  Results are bit-identical to the test oracle's.
 
+// Per-warp phase timeline (profiling builds only: -DOVX_TRACE, tools/trace_i8.py): clock64 stamps
+// of one CTA (block OVX_TRACE) over TRH half-iterations, TRN points each.
+#ifdef OVX_TRACE
+#define TRN 12
+#define TRH 16
+__device__ unsigned long long g_tr[TRH * 16 * TRN];
+#define TR(pt) do { if (blockIdx.x == OVX_TRACE && lane == 1 && trh >= 0 && trh < TRH) \
+                        g_tr[(trh * 16 + warp) * TRN + (pt)] = clock64(); } while (0)
+#else
+#define TR(pt) do { } while (0)
+#endif
+
 // A operand row (one element, one half-word array): 7 chunks of 16 B — chunks 0-2 the u bytes,
 // 3-5 the G bytes, 6 zero (K padding of the identity block's second K-step).
 constexpr int A1_CHUNKS = 7;
@@ -64,6 +76,7 @@ struct SmemI8 {
     double ysum[G::NS3][2][G::EY][G::EX][3];        // [layer slot][face] x-pair P of the +y corners
     double tf[2][G::NE][3];                         // [layer parity][tile node] top-face sums T
     double2 mc[kMaxMat];                            // (cG, c1) per material, staged from c_mat
+    uint8_t mid[5][G::NE];                          // material id of each tile element, ring like up
     uint64_t mbar[G::MT];
     uint32_t tmem;
 };
@@ -190,6 +203,8 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     const int mt = wu >> 3, hf = (wu >> 2) & 1, qd = wu & 3;   // warp-uniform roles (uniform registers)
     const int row = 32 * qd + lane;                      // MMA row = TMEM lane
 
+    int trh = -1000;   // trace: half-iteration index (OVX_TRACE builds)
+    (void)trh;
     int bid = blockIdx.x;
     const int tx = bid % p.tiles_x;
     bid /= p.tiles_x;
@@ -209,6 +224,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     const int lx = (128 * mt + row) % EX, ly = (128 * mt + row) / EX;
     const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
     const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
+    const int elem = lx + EX * ly;                   // tile element of this thread
     const uint8_t *matp = p.mat + (ein ? ex + p.nx * ey : 0);
     const int64_t mstride = p.nx * p.ny;
     // node (lx, ly): owned by this tile (lx, ly >= 1) if inside the grid; half 0 updates it
@@ -278,6 +294,11 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         const int id = i < p.nmat ? i : kZeroMat;
         S.mc[id] = make_double2(c_mat[id].cG, c_mat[id].c1);
     }
+    if (hf == 0)
+        for (int j = 0; j < 2; ++j) {   // material ids of layers Lfirst, Lfirst + 1
+            const int iz = Lfirst + j;
+            S.mid[ring5(iz)][elem] = (uint8_t)((ein && iz < nz) ? (int)__ldg(matp + mstride * iz) : kZeroMat);
+        }
     for (int j = 0; j < 2; ++j) {
         const int iz = Lfirst + j;
         if (lrole) {
@@ -309,8 +330,6 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
 
     uint32_t phase = 0;
     uint32_t xpar = mt == 0 ? 1u : 0u;   // TA: parity of the other M-tile's MMA completion to wait for
-    int mcur = (ein && Lfirst < nz) ? (int)__ldg(matp + mstride * Lfirst) : kZeroMat;
-    int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matp + mstride * (Lfirst + 1)) : kZeroMat;
     double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;   // update operands of this M-tile's post-phase plane
     double uv[3] = {0.0, 0.0, 0.0};              // DAMP: u of the owned node (the plane holds ũ)
     uint8_t dm = 0;
@@ -327,12 +346,26 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         const bool plane_done = (Lp >= Z0 && Lp <= nz && Lp < Z1);
         const bool bot_iface = (p.slab_flags & 1) && Lp == 0;
         const bool top_iface = (p.slab_flags & 2) && Lp == nz;
+        // all shared-memory operands first (one round trip instead of three dependent ones): the
+        // y-pair P(iy-1), T of plane Lp (half 0) and u of the node (indices in range for every thread)
+        double ysv[3], tfv[3], ucv[3];
+        {
+            const double(*ys)[EX][3] = S.ysum[s3][hf];
+            const double *tp = &S.tf[(Lp - 1) & 1][lx + EX * ly][0];
+            const double *up = &S.up[s5][(ly * PX + lx) * 3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                ysv[c] = ys[ly - 1][lx][c];
+                tfv[c] = tp[c];
+                ucv[c] = up[c];
+            }
+        }
         double face[3] = {0.0, 0.0, 0.0};
         if (layer_ok(Lp)) {
-            const double(*ys)[EX][3] = S.ysum[s3][hf];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) face[c] = __dadd_rn(plo[c], ys[ly - 1][lx][c]);   // P(iy) + P(iy-1)
+            for (int c = 0; c < 3; ++c) face[c] = __dadd_rn(plo[c], ysv[c]);   // P(iy) + P(iy-1)
         }
+        TR(9);
         if (hf == 1) {        // top face of layer Lp: T of plane Lp+1
 #pragma unroll
             for (int c = 0; c < 3; ++c) S.tf[Lp & 1][lx + EX * ly][c] = face[c];
@@ -344,12 +377,11 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
             } else {
                 double f[3];
 #pragma unroll
-                for (int c = 0; c < 3; ++c) f[c] = __dadd_rn(S.tf[(Lp - 1) & 1][lx + EX * ly][c], face[c]);
+                for (int c = 0; c < 3; ++c) f[c] = __dadd_rn(tfv[c], face[c]);
                 if (top_iface) {
 #pragma unroll
                     for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = f[c];
                 } else if (MODE == MODE_STEP) {
-                    const double *up = &S.up[s5][(ly * PX + lx) * 3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         const int64_t dof = 3 * un_id + c;
@@ -357,12 +389,14 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
                         if (has_src)
                             for (int k = 0; k < p.nsrc; ++k)
                                 if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
-                        const double uc = DAMP ? uv[c] : up[c];
+                        if (c == 0) TR(10);
+                        const double uc = DAMP ? uv[c] : ucv[c];
                         double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
                         if constexpr (DAMP) b = __dsub_rn(b, __dmul_rn(p.ca, __dsub_rn(uc, upv[c])));
                         double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
                         if ((dm >> c) & 1) un = 0.0;
                         (DAMP ? p.un : p.uo)[dof] = un;
+                        if (c == 2) TR(11);
                         if (has_rec)
                             for (int k = 0; k < p.nrec; ++k)
                                 if (p.rec_node[k] == un_id) p.traces[(3 * k + c) * p.rec_nt + p.it] = un;
@@ -378,6 +412,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     // ---- epilogue of layer Le: the 4 corner nodes of this thread's face ----
     auto epilogue = [&](int Le, int s3) {              // s3: ysum slot of Le
         ptx::mbar_wait_sleep(&S.mbar[mt], phase);
+        TR(5);
         phase ^= 1;
         ptx::tc_fence_after();
         // −RN(c1·s·2^{-7M}); a degenerate element contributes 0 (oracle: fe = 0)
@@ -454,6 +489,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         ab = max(ab, m1[n0 + PX]);
         ab = max(ab, m1[n0 + PX + 1]);
         const double amax = __longlong_as_double((long long)ab);
+        const int mcur = S.mid[sL][elem];
         const double cG = S.mc[mcur].x;
         const double s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
         const bool deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
@@ -483,7 +519,9 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         edbg = dbg;
         edj = dj;
         ptx::fence_proxy_async_smem();
+        TR(1);
         asm volatile("bar.sync %0, 256;" ::"r"(1 + mt) : "memory");   // the 8 warps of this M-tile
+        TR(2);
         if ((wu & 7) == 0) {     // first warp of the M-tile; one elected lane issues
             const int mtu = wu >> 3;
             if (ptx::elect_one()) {
@@ -519,6 +557,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
             }
             __syncwarp();
         }
+        TR(3);
     };
 
     // ring slots of planes / layers L-2 .. L+2 (q5_k = (L-2+k) mod 5) and L-2 .. L (q3_k = (L-2+k) mod 3)
@@ -538,6 +577,10 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     for (int h = 2 * (Z0 - 1); h <= 2 * (Z1 + 1) + 1; ++h) {
         const int L = h >> 1;
         const bool odd = h & 1;
+#ifdef OVX_TRACE
+        trh = h - 2 * (Z0 - 1) - 20;
+#endif
+        TR(0);
         if (!odd) {
             // ---- prefetch: plane L+2, material of layer L+2, update operands of the next post plane ----
             const int pz = L + 2;
@@ -566,7 +609,9 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
             if (layer_ok(L)) convert(L, q5_2, q5_3);
         } else {
             post_phase(L - 1 - mt, mt ? q3_0 : q3_1, mt ? q5_0 : q5_1);
+            TR(4);
             if (layer_ok(L - mt)) epilogue(L - mt, mt ? q3_1 : q3_2);
+            TR(6);
         }
         if (odd) {
             // ---- park plane L+2 (slot of plane L-3, no longer read) with its node maxima ----
@@ -581,10 +626,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
                 }
                 S.nmax[q5_4][li] = m;
             }
-            if (L >= Lfirst) {
-                mcur = mnxt;
-                mnxt = mfar;
-            }
+            if (hf == 0 && pf) S.mid[q5_4][elem] = (uint8_t)mfar;   // material of layer L+2
             upv[0] = upv_n[0];
             upv[1] = upv_n[1];
             upv[2] = upv_n[2];
@@ -605,7 +647,9 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
             }
             wn_n = 0.0;
             dm_n = 0;
+            TR(7);
             __syncthreads();
+            TR(8);
         }
     }
     ptx::tc_fence_after();
