@@ -225,8 +225,6 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 
 #include "step_i8w.cuh"
 
-static_assert(2 * (sizeof(SmemI8<I8S, false>) + 1024) <= 233472, "two 16x8 INT8 CTAs must fit one SM");
-
 template <int MODE, int M, bool DAMP, class G, bool TA>
 cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static bool attr = false;
@@ -243,19 +241,15 @@ cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// INT8 kernel variant (OVX_I8_KERNEL): "tmem" (default) 32 × 8 tiles, skewed M-tiles, the A operand
-// in TMEM (the MMAs read only B from shared memory); "smem" the same with A in shared memory;
-// "smem16" 16 × 8 tiles, two CTAs per SM, A in shared memory.  DESIGN.md §6.1 has the measurements.
+// INT8 kernel variant (OVX_I8_KERNEL): "tmem" (default) the A operand in TMEM (the MMAs read only B
+// from shared memory); "smem" A in shared memory.  DESIGN.md §6.1 has the measurements.
 int i8_variant() {
     static const int v = [] {
         const char *e = std::getenv("OVX_I8_KERNEL");
-        if (e && std::strcmp(e, "smem") == 0) return 1;
-        if (e && std::strcmp(e, "smem16") == 0) return 2;
-        return 0;
+        return (e && std::strcmp(e, "smem") == 0) ? 1 : 0;
     }();
     return v;
 }
-bool i8_wide() { return i8_variant() != 2; }
 
 template <int M, class G, bool TA>
 cudaError_t launch_i8_mode_g(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
@@ -268,11 +262,8 @@ cudaError_t launch_i8_mode_g(int mode, const StepParams &p, int64_t ctas, cudaSt
 
 template <int M>
 cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
-    switch (i8_variant()) {
-    case 1: return launch_i8_mode_g<M, I8W, false>(mode, p, ctas, st);
-    case 2: return launch_i8_mode_g<M, I8S, false>(mode, p, ctas, st);
-    default: return launch_i8_mode_g<M, I8W, true>(mode, p, ctas, st);
-    }
+    return i8_variant() == 1 ? launch_i8_mode_g<M, I8W, false>(mode, p, ctas, st)
+                             : launch_i8_mode_g<M, I8W, true>(mode, p, ctas, st);
 }
 
 template <int PATH, int MODE, bool DAMP = false>
@@ -401,13 +392,12 @@ cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, c
 LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
     if (path == OVX_INT8) {
         LaunchInfo li;
-        const int tx_ = i8_wide() ? I8W::TX : I8S::TX, tyy = I8W::TY, cps = i8_wide() ? I8W::CPS : I8S::CPS;
+        const int tx_ = I8W::TX, tyy = I8W::TY, cps = I8W::CPS;
         const int64_t tx = (nx + 1 + tx_ - 1) / tx_, ty = (ny + 1 + tyy - 1) / tyy;
         const int zc = choose_zchunk(nz + 1, tx * ty, cps);
         li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
-        li.threads = i8_wide() ? I8W::NT : I8S::NT;
-        li.smem = i8_variant() == 0 ? (int)sizeof(SmemI8<I8W, true>)
-                  : i8_variant() == 1 ? (int)sizeof(SmemI8<I8W, false>) : (int)sizeof(SmemI8<I8S, false>);
+        li.threads = I8W::NT;
+        li.smem = i8_variant() == 0 ? (int)sizeof(SmemI8<I8W, true>) : (int)sizeof(SmemI8<I8W, false>);
         return li;
     }
     if (path == OVX_FP64) return info_t<OVX_FP64>(nx, ny, nz);
@@ -431,8 +421,8 @@ static cudaError_t launch_chunks(int path, int mode, StepParams p, cudaStream_t 
 
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st, int part, int *nlaunch) {
     const int ty = path == OVX_INT8 ? I8W::TY : V1<OVX_FP64>::TY;
-    const int tx = path == OVX_INT8 ? (i8_wide() ? I8W::TX : I8S::TX) : TX;
-    const int cps = path == OVX_INT8 ? (i8_wide() ? I8W::CPS : I8S::CPS) : 2;
+    const int tx = path == OVX_INT8 ? I8W::TX : TX;
+    const int cps = path == OVX_INT8 ? I8W::CPS : 2;
     p.tiles_x = (int)((p.nx + 1 + tx - 1) / tx);
     p.tiles_y = (int)((p.ny + 1 + ty - 1) / ty);
     p.zchunk = choose_zchunk(p.nz + 1, (int64_t)p.tiles_x * p.tiles_y, cps);

@@ -40,11 +40,10 @@ constexpr int A1_BYTES = 16 * A1_PITCH;          // one half-word array of 128 r
 constexpr int B1_PITCH = 6 * 128;                // main B: 48 rows × 96 K-bytes
 constexpr int BI_PITCH = 2 * 128;                // identity blocks: 48 rows × 32 K-bytes
 
-// Tile geometry: EXv element columns × 8 rows per layer, MTv = EXv·8/128 M-tiles per CTA.
-//   I8G<32, 2>: 512 threads, one CTA per SM (≈215 KB smem, all 512 TMEM columns), the two M-tiles
-//               skewed by half an iteration inside the CTA;
-//   I8G<16, 1>: 256 threads, two CTAs per SM (≈113 KB smem, 256 TMEM columns each): no skew inside
-//               the CTA — the two resident CTAs overlap each other's barriers and phases.
+// Tile geometry: EXv element columns × 8 rows per layer, MTv = EXv·8/128 M-tiles per CTA; the kernel
+// runs I8G<32>: 512 threads, one CTA per SM, the two M-tiles skewed by half an iteration.  (A 16 × 8
+// tile, two CTAs per SM with the A operand in shared memory, measured 2.34 vs 2.27 ms per C2 step:
+// profiles/r1_int8_v24_tile16.md.)
 template <int EXv>
 struct I8G {
     static constexpr int EX = EXv;                     // element columns per layer (x)
@@ -64,7 +63,6 @@ struct I8G {
     static constexpr int CPS = MT == 2 ? 1 : 2;        // resident CTAs per SM
 };
 using I8W = I8G<32>;
-using I8S = I8G<16>;
 
 template <class G, bool TA>
 struct SmemI8 {
