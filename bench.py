@@ -319,19 +319,24 @@ def main() -> None:
     # end to end through the public API with pinned host buffers (upload state, K steps, download)
     uh = torch.from_numpy(R.u0).pin_memory().numpy()
     uout = torch.empty(R.u0.size, dtype=torch.float64).pin_memory().numpy()   # pinned result buffer
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    th0 = time.perf_counter()
-    e0.record(stream)
-    R.set_state(uh, uh)
-    th1 = time.perf_counter()
-    R.step(args.steps)
-    u_final = R.get_state(out_u=uout)
-    e1.record(stream)
-    barrier()
-    th2 = time.perf_counter()
-    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
-    e2e_host_ms = {"set_state": 1e3 * (th1 - th0), "total": 1e3 * (th2 - th0)}
+    def e2e_once():
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        th0 = time.perf_counter()
+        e0.record(stream)
+        R.set_state(uh, uh)
+        th1 = time.perf_counter()
+        R.step(args.steps)
+        u_fin = R.get_state(out_u=uout)
+        e1.record(stream)
+        barrier()
+        th2 = time.perf_counter()
+        return u_fin, max_over_ranks(e0.elapsed_time(e1)), {"set_state": 1e3 * (th1 - th0), "total": 1e3 * (th2 - th0)}
+
+    # two passes over the same region: the first touches the freshly pinned pages (the first upload
+    # from a new pinned buffer measured 15-420 ms on different boxes); the second is reported
+    e2e_once()
+    u_final, ms_e2e, e2e_host_ms = e2e_once()
 
     # FP64 CUDA-core path measured beside the INT8 path (same workload, same clock record)
     R_nn, R_ne, R_lps = R.nn, R.ne, R.launches_per_step

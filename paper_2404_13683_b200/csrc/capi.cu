@@ -27,6 +27,7 @@ struct ovx_ctx {
     double dt = 0;
     int path = OVX_INT8, stages = 8;
     uint8_t *d_mat = nullptr, *d_mask = nullptr;
+    int *d_flag = nullptr;   // finiteness flag (allocated once: no cudaMalloc / cudaFree per state upload)
     double *d_u = nullptr, *d_up = nullptr, *d_w = nullptr;
     double alpha = 0, beta = 0;       // Rayleigh damping (reading R1)
     double *d_un = nullptr;           // third state buffer of damped steps
@@ -411,14 +412,13 @@ static ovx_status set_state_impl(ovx_ctx *ctx, const double *u, const double *up
     CK(cudaMemcpyAsync(ctx->d_u, u, 8 * n3, kind, ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_up, up, 8 * n3, kind, ctx->stream));
     if (kind == cudaMemcpyHostToDevice) {   // finiteness checked on the device (the host scan was serial)
-        int *d_flag = nullptr, h = 0;
-        CK(cudaMalloc(&d_flag, sizeof(int)));
-        CK(cudaMemsetAsync(d_flag, 0, sizeof(int), ctx->stream));
-        CK(launch_finite_check(ctx->d_u, n3, d_flag, ctx->stream));
-        CK(launch_finite_check(ctx->d_up, n3, d_flag, ctx->stream));
-        CK(cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        int h = 0;
+        if (!ctx->d_flag) CK(cudaMalloc(&ctx->d_flag, sizeof(int)));
+        CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
+        CK(launch_finite_check(ctx->d_u, n3, ctx->d_flag, ctx->stream));
+        CK(launch_finite_check(ctx->d_up, n3, ctx->d_flag, ctx->stream));
+        CK(cudaMemcpyAsync(&h, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(d_flag);
         if (h) {
             ctx->have_state = false;
             return fail(ctx, OVX_EINVAL, "non-finite state");
@@ -676,13 +676,12 @@ ovx_status ovx_check_finite(ovx_ctx *ctx) {
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
     if (!ctx->have_grid) return fail(ctx, OVX_ESTATE, "set grid first");
     cudaSetDevice(ctx->device);
-    int *d_flag = nullptr, h = 0;
-    CK(cudaMalloc(&d_flag, sizeof(int)));
-    CK(cudaMemsetAsync(d_flag, 0, sizeof(int), ctx->stream));
-    CK(launch_finite_check(ctx->d_u, 3 * ctx->nn(), d_flag, ctx->stream));
-    CK(cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    int h = 0;
+    if (!ctx->d_flag) CK(cudaMalloc(&ctx->d_flag, sizeof(int)));
+    CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
+    CK(launch_finite_check(ctx->d_u, 3 * ctx->nn(), ctx->d_flag, ctx->stream));
+    CK(cudaMemcpyAsync(&h, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_flag);
     if (h) return fail(ctx, OVX_EUNSTABLE, "non-finite displacement at step " + std::to_string(ctx->it));
     return OVX_OK;
 }
