@@ -405,3 +405,52 @@ def test_full_size_1000_steps_closed_form(ovxmod, name, path):
         s64.step(1000)
         u64, _, _ = s64.get_state(with_prev=False)
         assert np.linalg.norm(u - u64) <= 1e-10 * np.linalg.norm(u64)
+
+
+def _sampled_apply_check(ovxmod, m, path, u, pts, nsample=40):
+    """apply_K at full size in the bench's launch configuration; sampled node forces vs the oracle
+    (bit-exact for the exact paths, 1e-13 relative for the factored FP64 form)."""
+    import torch
+    s = _solver(ovxmod, m, path)
+    ut = torch.from_numpy(u).cuda()
+    ft = torch.empty_like(ut)
+    s.apply_K_device(ut, ft)
+    s.sync()
+    rng = np.random.default_rng(13683 + path)
+    pts = list(pts) + [(int(rng.integers(0, m.nx + 1)), int(rng.integers(0, m.ny + 1)), int(rng.integers(0, m.nz + 1)))
+                       for _ in range(nsample)]
+    nx1, ny1 = m.nx + 1, m.ny + 1
+    idx = torch.tensor([3 * (ix + nx1 * (iy + ny1 * iz)) + c for (ix, iy, iz) in pts for c in range(3)],
+                       device="cuda")
+    f = ft[idx].cpu().numpy().reshape(-1, 3)
+    del ut, ft
+    for k, (ix, iy, iz) in enumerate(pts):
+        ref = _node_force_oracle(m, u, ix, iy, iz, path)
+        if EXACT[path]:
+            assert np.array_equal(f[k], ref), (ix, iy, iz)
+        else:
+            assert np.abs(f[k] - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max()), (ix, iy, iz)
+
+
+@pytest.mark.parametrize("name,path", [("int8", 0), ("fp64", 1)])
+def test_full_size_c3_sampled(ovxmod, name, path):
+    """BASELINE config 3 at full size (512³ two-layer soil over bedrock, 1.35e8 elements):
+    sampled nodes on the boundaries, the soil/rock interface plane and at random."""
+    m = wl.c3_two_layer(512)
+    u = wl.random_field(m)
+    iface = 512 - 128
+    pts = [(0, 0, 0), (512, 512, 512), (256, 256, iface), (255, 17, iface - 1), (1, 511, iface + 1),
+           (31, 7, 64), (32, 8, 129), (511, 0, 384)]
+    _sampled_apply_check(ovxmod, m, path, u, pts)
+
+
+@pytest.mark.parametrize("name,path", [("int8", 0), ("fp64", 1)])
+def test_full_size_c4_sampled(ovxmod, name, path):
+    """BASELINE config 4 at full size (891×352×1056, 3.3e8 elements, 1.0e9 DOF, one B200):
+    sampled nodes on the layer boundaries, around the stiff cylinder and at random."""
+    m = wl.c4_ground()
+    u = wl.random_field(m)
+    cx, cz = int(160 / 324 * 891), int(100 / 384 * 1056)
+    pts = [(0, 0, 0), (891, 352, 1056), (cx, 100, cz), (cx + 41, 5, cz), (cx - 41, 351, cz), (cx, 200, cz + 41),
+           (400, 176, 1056 - 52), (10, 10, 1056 - 211), (890, 1, 1056 - 475)]
+    _sampled_apply_check(ovxmod, m, path, u, pts)
