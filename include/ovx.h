@@ -95,7 +95,8 @@ ovx_status ovx_set_dt(ovx_ctx *ctx, double dt);
  * the model, both finite and >= 0; (0, 0) (the default) is the undamped Eq. 3.  ovx_step then
  * advances u^{it+1} = fma(w, F − K ũ, (2u − u_prev) − RN(alpha·dt)·(u − u_prev)) with the EBE
  * input ũ = u + RN(beta/dt)·(u − u_prev) (backward-difference velocity, explicit).  Allocates a
- * third state buffer (24 B/node).  Not available on z-slab contexts (OVX_ESTATE).
+ * third state buffer (24 B/node).  On z-slab contexts the interface update (ovx_step_iface) applies
+ * the same damped recurrence and ovx_step_end rotates the three buffers.
  * ovx_apply_K is unaffected (it computes K u). */
 ovx_status ovx_set_damping(ovx_ctx *ctx, double alpha, double beta);
 /* Derive K_e^INT8 on the host in exact rational arithmetic,

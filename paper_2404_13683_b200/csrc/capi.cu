@@ -512,8 +512,6 @@ ovx_status ovx_set_damping(ovx_ctx *ctx, double alpha, double beta) {
     if (!ctx->have_grid) return fail(ctx, OVX_ESTATE, "set the grid first");
     if (!(alpha >= 0) || !(beta >= 0) || !std::isfinite(alpha) || !std::isfinite(beta))
         return fail(ctx, OVX_EINVAL, "Rayleigh coefficients must be finite and >= 0");
-    if (ctx->slab_flags && (alpha != 0.0 || beta != 0.0))
-        return fail(ctx, OVX_ESTATE, "damping is not supported on z-slab contexts");
     cudaSetDevice(ctx->device);
     if ((alpha != 0.0 || beta != 0.0) && !ctx->d_un) {
         if (cudaMalloc(&ctx->d_un, 24 * ctx->nn()) != cudaSuccess) {
@@ -528,8 +526,6 @@ ovx_status ovx_set_damping(ovx_ctx *ctx, double alpha, double beta) {
 
 ovx_status ovx_set_slab(ovx_ctx *ctx, int flags, const uint8_t *mat_below) {
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
-    if (flags && (ctx->alpha != 0.0 || ctx->beta != 0.0))
-        return fail(ctx, OVX_ESTATE, "damping is not supported on z-slab contexts");
     if (!ctx->have_grid || ctx->nmat == 0) return fail(ctx, OVX_ESTATE, "set grid and materials first");
     if (flags < 0 || flags > 3) return fail(ctx, OVX_EINVAL, "slab flags must be in 0..3");
     if ((flags & 1) && !mat_below) return fail(ctx, OVX_EINVAL, "a lower neighbour needs the halo materials");
@@ -577,6 +573,12 @@ static StepParams step_params(ovx_ctx *ctx) {
     p.slab_flags = ctx->slab_flags;
     p.iface_top_A = ctx->a_send;
     p.iface_bot_b = ctx->d_bot_b;
+    if (ctx->alpha != 0.0 || ctx->beta != 0.0) {   // Rayleigh damping (reading R1), as in ovx_step
+        p.damped = 1;
+        p.ca = ctx->alpha * ctx->dt;
+        p.cb = ctx->beta / ctx->dt;
+        p.un = ctx->d_un;
+    }
     fill_receivers(ctx, p);
     return p;
 }
@@ -624,10 +626,19 @@ ovx_status ovx_step_end(ovx_ctx *ctx) {
     ovx_status s = need_ready(ctx);
     if (s) return s;
     cudaSetDevice(ctx->device);
+    const bool damped = ctx->alpha != 0.0 || ctx->beta != 0.0;
+    double *next = damped ? ctx->d_un : ctx->d_up;   // the buffer holding u^{it+1}
     if (ctx->slab_flags & 2)   // the owner above sent the updated top plane
-        CK(cudaMemcpyAsync(ctx->d_up + 3 * ctx->nn2() * ctx->nz, ctx->u_recv, 24 * ctx->nn2(),
+        CK(cudaMemcpyAsync(next + 3 * ctx->nn2() * ctx->nz, ctx->u_recv, 24 * ctx->nn2(),
                            cudaMemcpyDeviceToDevice, ctx->stream));
-    std::swap(ctx->d_u, ctx->d_up);
+    if (damped) {              // (u_prev, u, u_next) <- (u, u_next, u_prev)
+        double *old_up = ctx->d_up;
+        ctx->d_up = ctx->d_u;
+        ctx->d_u = ctx->d_un;
+        ctx->d_un = old_up;
+    } else {
+        std::swap(ctx->d_u, ctx->d_up);
+    }
     ctx->it += 1;
     return OVX_OK;
 }

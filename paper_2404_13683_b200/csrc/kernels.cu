@@ -466,10 +466,12 @@ __global__ void iface_update_kernel(const StepParams p, const double *__restrict
             double F = 0.0;
             for (int k = 0; k < p.nsrc; ++k)
                 if (p.src_dof[k] == dof) F = __dadd_rn(F, p.src_val[k]);
-            const double b = __dsub_rn(__dmul_rn(2.0, p.u[dof]), p.uo[dof]);
+            const double uc = p.u[dof], upc = p.uo[dof];
+            double b = __dsub_rn(__dmul_rn(2.0, uc), upc);
+            if (p.damped) b = __dsub_rn(b, __dmul_rn(p.ca, __dsub_rn(uc, upc)));   // reading R1
             double un = __fma_rn(wn, __dsub_rn(F, f), b);
             if ((dm >> c) & 1) un = 0.0;
-            p.uo[dof] = un;
+            (p.damped ? p.un : p.uo)[dof] = un;
             u_send[dof] = un;
             if (p.it < p.rec_nt)
                 for (int k = 0; k < p.nrec; ++k)

@@ -55,7 +55,8 @@ def local_model(m, slab: Slab):
     nx, ny = m.nx, m.ny
     nn2 = (nx + 1) * (ny + 1)
     ne2 = nx * ny
-    lm = SimpleNamespace(nx=nx, ny=ny, nz=slab.nzl, ds=m.ds, rho=m.rho, kappa=m.kappa, G=m.G, dt=m.dt)
+    lm = SimpleNamespace(nx=nx, ny=ny, nz=slab.nzl, ds=m.ds, rho=m.rho, kappa=m.kappa, G=m.G, dt=m.dt,
+                         alpha=getattr(m, "alpha", 0.0), beta=getattr(m, "beta", 0.0))
     lm.mat = np.ascontiguousarray(m.mat[slab.ez0 * ne2: slab.ez1 * ne2])
     lm.mat_below = np.ascontiguousarray(m.mat[(slab.ez0 - 1) * ne2: slab.ez0 * ne2]) if slab.rank > 0 else None
     lm.dirichlet = None if m.dirichlet is None else np.ascontiguousarray(
@@ -152,6 +153,8 @@ class OvxCompute:
         o.set_slab(slab.flags, lm.mat_below)
         o.setup_elements(path, 8)
         o.set_dt(lm.dt)
+        if getattr(lm, "alpha", 0.0) or getattr(lm, "beta", 0.0):   # Rayleigh damping (reading R1)
+            o.set_damping(lm.alpha, lm.beta)
         if len(lm.src_node):
             o.set_sources(lm.src_node, lm.src_axis, lm.amp)
         n = 3 * (lm.nx + 1) * (lm.ny + 1)

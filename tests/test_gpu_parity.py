@@ -328,14 +328,6 @@ def test_damped_ragged_multichunk_bit_exact(ovxmod):
         assert np.array_equal(u, ru) and np.array_equal(up, rup), path
 
 
-def test_damping_rejected_on_slabs(ovxmod):
-    m = wl.small_random(4, 3, 4, ds=0.01)
-    s = _solver(ovxmod, m, 0)
-    s.set_damping(1.0, 1e-9)
-    with pytest.raises(ovxmod.OvxError):
-        s.set_slab(1, np.zeros(m.nx * m.ny, np.uint8))
-
-
 def test_e1_rebar_reduced_bit_exact(ovxmod):
     """NEXT-2: the paper's rebar model (E1) at ds = 8 mm (steel / concrete, Table 1 source and
     receivers, Rayleigh damping over 100-125 kHz), 30 steps: INT8 and dense-FP64 states and
