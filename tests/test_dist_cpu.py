@@ -53,7 +53,7 @@ def test_local_model_slices():
         assert tot_src == len(m.src_node)      # every source owned by exactly one rank
 
 
-def _worker(rank, world, port, path, nsteps, out):
+def _worker(rank, world, port, path, nsteps, out, staged=False):
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -62,7 +62,8 @@ def _worker(rank, world, port, path, nsteps, out):
     m = _model()
     rng = np.random.default_rng(5)
     u0 = rng.standard_normal(3 * m.n_nodes) * 1e-6
-    run = D.SlabRun(m, rank, world, lambda lm, s: OracleSlabCompute(lm, s, path), D.TorchTransport())
+    tr = D.HostStagedTransport() if staged else D.TorchTransport()
+    run = D.SlabRun(m, rank, world, lambda lm, s: OracleSlabCompute(lm, s, path), tr)
     run.set_state(u0, u0, 0)
     run.step(nsteps)
     g = D.gather_state(run)
@@ -88,5 +89,20 @@ def test_gloo_slabs_equal_monolithic_run(tmp_path, world, path):
     rng = np.random.default_rng(5)
     u0 = rng.standard_normal(3 * m.n_nodes) * 1e-6
     ru, rup, _, st = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=path)
+    assert st == 0
+    assert np.array_equal(got[0], ru) and np.array_equal(got[1], rup)
+
+
+def test_host_staged_transport_equals_monolithic(tmp_path):
+    """The bench's one-GPU test hook (dist.HostStagedTransport: messages staged through host
+    memory over gloo) carries the same protocol: world 2, INT8 emulation, bit-exact."""
+    nsteps = 20
+    out = str(tmp_path / "u.npy")
+    mp.spawn(_worker, args=(2, _free_port(), oracle.PATH_INT8, nsteps, out, True), nprocs=2, join=True)
+    got = np.load(out)
+    m = _model()
+    rng = np.random.default_rng(5)
+    u0 = rng.standard_normal(3 * m.n_nodes) * 1e-6
+    ru, rup, _, st = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=oracle.PATH_INT8)
     assert st == 0
     assert np.array_equal(got[0], ru) and np.array_equal(got[1], rup)
