@@ -1,5 +1,7 @@
 """Small cases for compute-sanitizer (racecheck / memcheck / synccheck): one INT8, FP64 and dense step
-and an apply on a ragged grid, plus a 2-slab overlapped step."""
+and an apply on a ragged grid, plus a 2-slab overlapped step and a damped 2-slab step.  The INT8
+kernel keeps its A operand in TMEM: racecheck covers the shared-memory traffic; the TMEM hand-over
+between the two M-tiles is ordered by the MMA-completion mbarriers (synccheck)."""
 import sys
 
 import numpy as np
@@ -24,6 +26,10 @@ g = D.SlabGroup(m2, 2, lambda lm, sl: D.OvxCompute(lm, sl, 0, 0))
 u2 = wl.random_field(m2) * 1e-6
 g.set_state(u2, u2, 0)
 g.step(2, overlap=True)
+m2.alpha, m2.beta = 0.02 / m2.dt, 0.03 * m2.dt      # damped z-slab step (third buffer rotation)
+g2 = D.SlabGroup(m2, 2, lambda lm, sl: D.OvxCompute(lm, sl, 0, 0))
+g2.set_state(u2, u2, 0)
+g2.step(2)
 import torch  # noqa: E402
 torch.cuda.synchronize()
 print("slabs ok", flush=True)
