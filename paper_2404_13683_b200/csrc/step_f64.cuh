@@ -123,17 +123,20 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     // synchronous first three planes (the loop prefetches two planes ahead); the fourth ring
     // slot is zeroed: the prefetch never writes the out-of-domain halo entries
     for (int idx = t; idx < PLANE; idx += NT) S.up[(Lfirst + 3) & 3][idx] = 0.0;
-    for (int j = 0; j < 3; ++j) {
-        const int iz = Lfirst + j;
-        double *dst = S.up[iz & 3];
-        for (int idx = t; idx < PLANE; idx += NT) {
-            const int py = idx / (PX * 3);
-            const int rem = idx - py * (PX * 3);
-            const int px = rem / 3, c = rem - px * 3;
-            const int64_t ix = X0 - 1 + px, iy = Y0 - 1 + py;
-            dst[idx] = (iz <= nz && ix >= 0 && ix < NX1 && iy >= 0 && iy < NY1)
-                           ? load_in(3 * (ix + NX1 * (iy + NY1 * iz)) + c) : 0.0;
+    {   // all loads of the three planes first (one DRAM round trip per CTA), then the stores
+        double v0[3][PF];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const int iz = Lfirst + j;
+#pragma unroll
+            for (int k = 0; k < PF; ++k)
+                v0[j][k] = (pfok[k] && iz <= nz) ? load_in(3 * PSTRIDE * (int64_t)iz + pfoff[k]) : 0.0;
         }
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int k = 0; k < PF; ++k)
+                if (t + k * NT < PLANE) S.up[(Lfirst + j) & 3][t + k * NT] = v0[j][k];
     }
     __syncthreads();
 
@@ -152,19 +155,22 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         }
     };
     double facc[3] = {0.0, 0.0, 0.0};   // plane L (receives layer L-1 top + layer L bottom)
-    // material ids of the current and next layer; the one after is fetched two layers ahead
+    // material ids of layers L, L+1, L+2; the one after is fetched three layers ahead
     int mcur = (ein && Lfirst < nz) ? (int)__ldg(matcol + mstride * Lfirst) : kZeroMat;
     int mnxt = (ein && Lfirst + 1 < nz) ? (int)__ldg(matcol + mstride * (Lfirst + 1)) : kZeroMat;
+    int mnx2 = (ein && Lfirst + 2 < nz) ? (int)__ldg(matcol + mstride * (Lfirst + 2)) : kZeroMat;
     double nupv[3] = {0.0, 0.0, 0.0}, nwn = 0.0, nuv[3] = {0.0, 0.0, 0.0};
     uint8_t ndm = 0;
     // running offsets (advanced once per layer instead of 64-bit products per use)
-    const uint8_t *mfar_p = matcol + mstride * (int64_t)(Z0 + 1);      // material of layer L+2
+    const uint8_t *mfar_p = matcol + mstride * (int64_t)(Z0 + 2);      // material of layer L+3
     int64_t uplane = 3 * PSTRIDE * (int64_t)(Z0 + 2);                  // plane L+3 of u
     int64_t un_id = ucol + PSTRIDE * (int64_t)(Z0 - 1);                // node of plane L
     for (int L = Z0 - 1; L < Z1; ++L, mfar_p += mstride, uplane += 3 * PSTRIDE, un_id += PSTRIDE) {
         const bool layer_ok = (L >= 0 && L < nz);
         const bool plane_done = (L >= Z0 && L <= nz);
-        const int mfar = (ein && L >= Lfirst && L + 2 < nz) ? (int)__ldg(mfar_p) : kZeroMat;
+        // material of layer L+3 (three layers ahead: the register rotation at the end of the layer
+        // waits on a load issued one layer earlier)
+        const int mfar = (ein && L >= Lfirst && L + 3 < nz) ? (int)__ldg(mfar_p) : kZeroMat;
         // ---- prefetch plane L+3 (parked next iteration) and the update operands of plane L ----
         const int pz = L + 3;
         const bool pf = (pz > Lfirst + 2) && (L + 2 < Z1) && (L + 2 < nz);
@@ -265,7 +271,8 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         }
         if (L >= Lfirst) {
             mcur = mnxt;
-            mnxt = mfar;
+            mnxt = mnx2;
+            mnx2 = mfar;
         }
 #pragma unroll
         for (int j = 0; j < PF; ++j) pend[j] = pfv[j];
