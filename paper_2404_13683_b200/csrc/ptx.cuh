@@ -34,6 +34,17 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
         : "memory");
 }
 
+// ---- cp.async (global -> shared without a register round trip) --------------
+// 8 bytes; valid == false zero-fills the destination (src-size 0, the source is not read)
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // One lane of a converged warp (elect.sync): keeps the tcgen05 issue code warp-uniform.
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred;

@@ -37,7 +37,7 @@ union MatU {
 };
 
 struct SmemF2 {
-    double up[4][F2::PLANE];          // ring: planes L, L+1 in use, L+2 parked, L+3 in flight
+    double up[5][F2::PLANE];          // ring: L-1 (its update may still run), L, L+1 in use, L+2, L+3 in flight
     double ysum[2][F2::EY][EX][6];    // +y-corner x-sums of each element row (double-buffered)
     MatU mw[kMaxMat];                 // [0, nmat) and the zero material kZeroMat
 };
@@ -120,9 +120,13 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         else S.mw[id].w = MatW{m.L0, m.M0, m.M0x2, m.L1, m.M1, m.M1x3, m.C2, 0.0};
     }
     const int Lfirst = max(Z0 - 1, 0);
-    // synchronous first three planes (the loop prefetches two planes ahead); the fourth ring
-    // slot is zeroed: the prefetch never writes the out-of-domain halo entries
-    for (int idx = t; idx < PLANE; idx += NT) S.up[(Lfirst + 3) & 3][idx] = 0.0;
+    // synchronous first three planes (the loop prefetches three planes ahead); the other two ring
+    // slots are zeroed for the damped register path
+    auto r5 = [](int z) { return (z + 10) % 5; };        // ring slot of plane z >= -10
+    for (int idx = t; idx < PLANE; idx += NT) {   // the damped park never writes out-of-domain entries
+        S.up[r5(Lfirst + 3)][idx] = 0.0;
+        S.up[r5(Lfirst + 4)][idx] = 0.0;
+    }
     {   // all loads of the three planes first (one DRAM round trip per CTA), then the stores
         double v0[3][PF];
 #pragma unroll
@@ -136,22 +140,29 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         for (int j = 0; j < 3; ++j)
 #pragma unroll
             for (int k = 0; k < PF; ++k)
-                if (t + k * NT < PLANE) S.up[(Lfirst + j) & 3][t + k * NT] = v0[j][k];
+                if (t + k * NT < PLANE) S.up[r5(Lfirst + j)][t + k * NT] = v0[j][k];
     }
     __syncthreads();
 
-    // plane prefetched in the previous iteration, parked (before this layer's barrier) into the
-    // ring slot of plane L-1, which no thread reads any more
+    // Plane L+3 is fetched at layer L into the ring slot of plane L-2 (no thread reads it any more:
+    // the slowest thread is past this layer's predecessor barrier, after which only planes L-1 .. L+1
+    // are read).  Undamped: cp.async straight into shared memory (zero-fill outside the domain),
+    // waited for one layer later before the barrier.  Damped (ũ needs arithmetic): registers, parked
+    // into the slot one layer later before the barrier.
     double pend[PF];
     int pend_z = -1;
     auto park_prev = [&]() {
-        if (pend_z >= 0) {
-            double *dst = S.up[pend_z & 3];
+        if constexpr (DAMP) {
+            if (pend_z >= 0) {
+                double *dst = S.up[r5(pend_z)];
 #pragma unroll
-            for (int j = 0; j < PF; ++j) {
-                const int idx = t + j * NT;
-                if (pfok[j]) dst[idx] = pend[j];
+                for (int j = 0; j < PF; ++j) {
+                    const int idx = t + j * NT;
+                    if (pfok[j]) dst[idx] = pend[j];
+                }
             }
+        } else {
+            ptx::cp_async_wait<1>();   // the copies issued one layer ago (plane L+2) have landed
         }
     };
     double facc[3] = {0.0, 0.0, 0.0};   // plane L (receives layer L-1 top + layer L bottom)
@@ -175,9 +186,19 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         const int pz = L + 3;
         const bool pf = (pz > Lfirst + 2) && (L + 2 < Z1) && (L + 2 < nz);
         double pfv[PF];
+        if constexpr (DAMP) {
 #pragma unroll
-        for (int j = 0; j < PF; ++j)
-            if (pf && pfok[j]) pfv[j] = load_in(uplane + pfoff[j]);
+            for (int j = 0; j < PF; ++j)
+                if (pf && pfok[j]) pfv[j] = load_in(uplane + pfoff[j]);
+        } else {
+            if (pf) {
+                double *dst = S.up[r5(pz)];
+#pragma unroll
+                for (int j = 0; j < PF; ++j)
+                    if (t + j * NT < PLANE) ptx::cp_async8(dst + t + j * NT, p.u + uplane + pfoff[j], pfok[j]);
+            }
+            ptx::cp_async_commit();
+        }
         const bool upd = plane_done && own;
         // update operands of plane L were loaded one layer ahead; fetch those of plane L+1
         double upv[3] = {nupv[0], nupv[1], nupv[2]};
@@ -204,7 +225,7 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         double(*ys)[EX][6] = S.ysum[L & 1];
         if (layer_ok) {
             double ue[24], fe[24];
-            gather<F2::PY>(ue, S.up[L & 3], S.up[(L + 1) & 3], lx, ly);
+            gather<F2::PY>(ue, S.up[r5(L)], S.up[r5(L + 1)], lx, ly);
             if constexpr (VF) element_force_vfem_wht(ue, S.mw[mcur].v, fe);   // zero material outside
             else element_force_wht(ue, S.mw[mcur].w, fe);                    // the domain -> fe = 0
             // x-sums at this element's -x node column: own -x corners + lane lx-1's +x corners
@@ -241,7 +262,7 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
         }
         // ---- plane L complete: update ----
         if (upd) {
-            const double *up = &S.up[L & 3][(ly * PX + lx) * 3];
+            const double *up = &S.up[r5(L)][(ly * PX + lx) * 3];
             if (MODE == MODE_STEP) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
@@ -275,7 +296,10 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
             mnx2 = mfar;
         }
 #pragma unroll
-        for (int j = 0; j < PF; ++j) pend[j] = pfv[j];
-        pend_z = pf ? pz : -1;
+        if constexpr (DAMP) {
+#pragma unroll
+            for (int j = 0; j < PF; ++j) pend[j] = pfv[j];
+            pend_z = pf ? pz : -1;
+        }
     }
 }
