@@ -340,6 +340,14 @@ def main() -> None:
 
     # FP64 CUDA-core path measured beside the INT8 path (same workload, same clock record)
     R_nn, R_ne, R_lps = R.nn, R.ne, R.launches_per_step
+    # INT8 MMA work actually issued per launch (padding, ⊗I₂ structure, the Eq. 9 diagonal K-steps and
+    # the recomputed halo elements included): tiles × computed layers × 2 M-tiles × 20 MMAs of
+    # M128·N48·K32 (393,216 ops each); computed layers = nz + (z-chunks − 1)
+    issued_ops = None
+    if world == 1 and path == OVX_INT8:
+        ctas = R.s.get_launch_config()[0]
+        txy = -(-(args.n + 1) // 31) * -(-(args.n + 1) // 7)
+        issued_ops = txy * (args.n + ctas // txy - 1) * 2 * 20 * 393216
     if world > 1:   # the job's launches: step kernels of every rank + the interface updates
         t = torch.tensor([float(R_lps)], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -377,6 +385,22 @@ def main() -> None:
                 "bytes_per_launch": bytes_launch, "kernel_ms_per_launch": kernel_ms,
                 "kernel": {0: "step_i8w<M=8>", 1: "step_f64", 2: "step_v1<FP64_DENSE>", 3: "step_f64<VF>",
                            4: "step_v1<FP64_DENSE> (VFEM matrices)"}[path]}
+    # SURVEY §8(d)'s per-run ncu figures for the dominant kernel, from the committed capture of the
+    # same command (profiles/; ncu numbers are never taken inside this timed run)
+    ncu = None
+    prof = {0: "r1_int8_v26", 1: "r1_fp64_v27"}.get(path)
+    if world == 1 and prof and os.path.exists(os.path.join(ROOT, "profiles", prof + ".json")):
+        try:
+            l0 = json.load(open(os.path.join(ROOT, "profiles", prof + ".json")))["launches"][0]
+            g = lambda k: l0.get(k, [None])[0]
+            ncu = {"source": f"profiles/{prof}.md", "kernel_ms": g("gpu__time_duration.sum"),
+                   "issue_active_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                   "tensor_pipe_active_pct": g("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "fp64_pipe_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "dram_gbytes_per_launch": (g("dram__bytes_read.sum") + g("dram__bytes_write.sum")) / 1e3,
+                   "warp_instructions": g("smsp__inst_executed.sum")}
+        except Exception:
+            ncu = None
     nodes_total = (args.n + 1) ** 2 * (args.n * world + 1)
     out = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
@@ -394,12 +418,14 @@ def main() -> None:
         "dof_steps_per_s": 3 * nodes_total * args.steps / (ms / 1e3),
         "roofline": roof,
         "int8_tops_useful": (18432 * R_ne / (kernel_ms / 1e3) / 1e12) if (path == OVX_INT8 and kernel_ms) else None,
+        "int8_tops_issued": (issued_ops / (kernel_ms / 1e3) / 1e12) if (issued_ops and kernel_ms) else None,
         # BASELINE "INT8 tensor-pipe % peak": useful INT8 MACs×2 per second over the INT8 dense peak
         # (2 × the measured bf16 TF/s, the guide's nominal int8:bf16 ratio); ncu pipe activity in
         # profiles/r1_int8_v*.md (sm__pipe_tensor_cycles_active)
         "int8_tensor_pct_of_peak": (100.0 * 18432 * R_ne / (kernel_ms / 1e3) / 1e12 / (2.0 * pk["bf16_tflops"]))
                                    if (path == OVX_INT8 and kernel_ms) else None,
         "fp64_path": fp64,
+        "ncu_profile": ncu,
         "clocks": clocks,
         "gpu_launches": R_lps * args.steps,
         "e2e": {"value": E_total * args.steps / (ms_e2e / 1e3), "unit": METRIC,
