@@ -1,6 +1,11 @@
-"""Time the C2 INT8 step with ablated libovx builds (tools/abl/libovx_abl<k>.so, -DOVX_ABLATE=k):
-0 none, 1 no main-block MMAs, 2 no scaling/F2I, 3 no limb recombination, 4 no update operand loads.
-The results are wrong by construction; only the timing is of interest."""
+"""Time the C2 INT8 step with ablated libovx builds (tools/abl/libovx_abl<k>.so).
+
+The numbers in DESIGN.md §6.1 came from a copy of the shared-memory-A kernel of commit c550195
+patched under `#if OVX_ABLATE == k` (built with tools/build_variant.sh abl<k> -DOVX_ABLATE=k):
+1 the 3 main-block MMAs per array skipped, 2 the conversion's DMUL/F2I replaced by a bit move,
+3 the limb recombination replaced by an XOR, 4 the update-operand loads skipped, 5 the A stores
+skipped, 7 the 2 identity-fold MMAs per array skipped.  The results are wrong by construction; only
+the timing is of interest."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
