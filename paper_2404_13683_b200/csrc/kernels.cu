@@ -295,8 +295,8 @@ cudaError_t launch_f64(const StepParams &p, int64_t ctas, cudaStream_t st) {
 template <int PATH>
 cudaError_t launch_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
     if constexpr (PATH == OVX_FP64 || PATH == OVX_VFEM) {   // dedicated shuffle/register kernel;
-        constexpr bool VF = PATH == OVX_VFEM;                   // debug records and slabs via step_v1
-        if (mode == MODE_STEP && p.slab_flags == 0)
+        constexpr bool VF = PATH == OVX_VFEM;                   // debug records via step_v1
+        if (mode == MODE_STEP)
             return p.damped ? launch_f64<MODE_STEP, true, VF>(p, ctas, st) : launch_f64<MODE_STEP, false, VF>(p, ctas, st);
         if (mode == MODE_APPLY) return launch_f64<MODE_APPLY, false, VF>(p, ctas, st);
     }

@@ -261,7 +261,17 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
             for (int c = 0; c < 3; ++c) facc[c] += nbot[c];
         }
         // ---- plane L complete: update ----
-        if (upd) {
+        // z-slab interfaces: plane 0 owned here, its partial from below arrives later
+        // (keep the bottom-face sum B); the top plane is owned by the rank above (send T + B = T + 0)
+        const bool bot_iface = (p.slab_flags & 1) && L == 0;
+        const bool top_iface = (p.slab_flags & 2) && L == nz;
+        if (upd && bot_iface) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) p.iface_bot_b[3 * ucol + c] = nbot[c];
+        } else if (upd && top_iface) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = facc[c];
+        } else if (upd) {
             const double *up = &S.up[r5(L)][(ly * PX + lx) * 3];
             if (MODE == MODE_STEP) {
 #pragma unroll
