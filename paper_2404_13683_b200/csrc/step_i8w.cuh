@@ -69,7 +69,8 @@ struct SmemI8 {
     uint8_t A[G::MT][4][TA ? 16 : A1_BYTES];   // [M-tile][half-word array], K-major canonical layout (TA: in TMEM)
     alignas(128) uint8_t B[6 * B1_PITCH];
     alignas(128) uint8_t BI[2][6 * BI_PITCH];
-    double up[5][G::PLANE];                         // ring: L-2, L-1 (updates), L, L+1 (gather), L+2
+    double up[5][3][G::NODES];                      // ring: L-2, L-1 (updates), L, L+1 (gather), L+2;
+                                                    // component-major: a warp's loads are contiguous
     unsigned long long nmax[5][G::NODES];           // max_c |u_c| of each node (bit patterns)
     double ysum[G::NS3][2][G::EY][G::EX][3];        // [layer slot][face] x-pair P of the +y corners
     double tf[2][G::NE][3];                         // [layer parity][tile node] top-face sums T
@@ -80,14 +81,14 @@ struct SmemI8 {
 };
 
 // ū values 8hf .. 8hf+15 of tile element (lx, ly) (local node order of reading Q1)
-template <int HF, int PX>
+template <int HF, int PX, int NODES>
 __device__ __forceinline__ void gather16(double (&ue)[16], const double *lo, const double *hi, int lx, int ly) {
     const int cx[4] = {0, 1, 1, 0}, cy[4] = {0, 0, 1, 1};
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         const int k = 8 * HF + j, a = k / 3, c = k - 3 * a;
         const double *pl = a < 4 ? lo : hi;
-        ue[j] = pl[((ly + cy[a & 3]) * PX + (lx + cx[a & 3])) * 3 + c];
+        ue[j] = pl[c * NODES + (ly + cy[a & 3]) * PX + (lx + cx[a & 3])];
     }
 }
 
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
             unsigned long long m = 0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                S.up[ring5(iz)][3 * li + c] = v3[c];
+                S.up[ring5(iz)][c][li] = v3[c];
                 const unsigned long long b = abs_bits(v3[c]);
                 m = b > m ? b : m;
             }
@@ -350,12 +351,11 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         {
             const double(*ys)[EX][3] = S.ysum[s3][hf];
             const double *tp = &S.tf[(Lp - 1) & 1][lx + EX * ly][0];
-            const double *up = &S.up[s5][(ly * PX + lx) * 3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 ysv[c] = ys[ly - 1][lx][c];
                 tfv[c] = tp[c];
-                ucv[c] = up[c];
+                ucv[c] = S.up[s5][c][ly * PX + lx];
             }
         }
         double face[3] = {0.0, 0.0, 0.0};
@@ -499,11 +499,11 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         const uint32_t ta = S.tmem + ((uint32_t)(qd * 32) << 16) + TA_A0;
         uint64_t *xbar = &S.mbar[C::MT - 1 - mt];
         if (hf == 0) {
-            gather16<0, PX>(ue, S.up[sL], S.up[sL1], lx, ly);
+            gather16<0, PX, C::NODES>(ue, &S.up[sL][0][0], &S.up[sL1][0][0], lx, ly);
             i8w_convert<MODE, M, 0, TA>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj, ta, xbar, xpar);
             if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
         } else {
-            gather16<1, PX>(ue, S.up[sL], S.up[sL1], lx, ly);
+            gather16<1, PX, C::NODES>(ue, &S.up[sL][0][0], &S.up[sL1][0][0], lx, ly);
             i8w_convert<MODE, M, 1, TA>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj, ta, xbar, xpar);
         }
         xpar ^= 1u;
@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
                 unsigned long long m = 0;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    S.up[q5_4][3 * li + c] = pfv[c];
+                    S.up[q5_4][c][li] = pfv[c];
                     const unsigned long long b = abs_bits(pfv[c]);
                     m = b > m ? b : m;
                 }
