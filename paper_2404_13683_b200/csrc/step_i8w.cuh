@@ -72,8 +72,8 @@ struct SmemI8 {
     double up[5][3][G::NODES];                      // ring: L-2, L-1 (updates), L, L+1 (gather), L+2;
                                                     // component-major: a warp's loads are contiguous
     unsigned long long nmax[5][G::NODES];           // max_c |u_c| of each node (bit patterns)
-    double ysum[G::NS3][2][G::EY][G::EX][3];        // [layer slot][face] x-pair P of the +y corners
-    double tf[2][G::NE][3];                         // [layer parity][tile node] top-face sums T
+    double ysum[G::NS3][2][3][G::EY][G::EX];        // [layer slot][face][c] x-pair P of the +y corners
+    double tf[2][3][G::NE];                         // [layer parity][c][tile node] top-face sums T
     double2 mc[kMaxMat];                            // (cG, c1) per material, staged from c_mat
     uint8_t mid[5][G::NE];                          // material id of each tile element, ring like up
     uint64_t mbar[G::MT];
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     if (warp == 0) ptx::tmem_alloc<C::TMEM_COLS>(&S.tmem);
     if (t == 0)
         for (int mm = 0; mm < C::MT; ++mm) ptx::mbar_init(&S.mbar[mm], 1);
-    for (int i = t; i < 2 * C::NE * 3; i += NT) (&S.tf[0][0][0])[i] = 0.0;
+    for (int i = t; i < 2 * 3 * C::NE; i += NT) (&S.tf[0][0][0])[i] = 0.0;
     for (int i = t; i < p.nmat + 1; i += NT) {      // a per-lane indexed constant-bank load serialises
         const int id = i < p.nmat ? i : kZeroMat;
         S.mc[id] = make_double2(c_mat[id].cG, c_mat[id].c1);
@@ -349,12 +349,10 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         // y-pair P(iy-1), T of plane Lp (half 0) and u of the node (indices in range for every thread)
         double ysv[3], tfv[3], ucv[3];
         {
-            const double(*ys)[EX][3] = S.ysum[s3][hf];
-            const double *tp = &S.tf[(Lp - 1) & 1][lx + EX * ly][0];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                ysv[c] = ys[ly - 1][lx][c];
-                tfv[c] = tp[c];
+            for (int c = 0; c < 3; ++c) {   // component-major: a warp's loads are contiguous
+                ysv[c] = S.ysum[s3][hf][c][ly - 1][lx];
+                tfv[c] = S.tf[(Lp - 1) & 1][c][lx + EX * ly];
                 ucv[c] = S.up[s5][c][ly * PX + lx];
             }
         }
@@ -366,7 +364,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         TR(9);
         if (hf == 1) {        // top face of layer Lp: T of plane Lp+1
 #pragma unroll
-            for (int c = 0; c < 3; ++c) S.tf[Lp & 1][lx + EX * ly][c] = face[c];
+            for (int c = 0; c < 3; ++c) S.tf[Lp & 1][c][lx + EX * ly] = face[c];
         } else if (own && plane_done) {
             const int64_t un_id = ucol + PSTRIDE * Lp;
             if (bot_iface) {  // interface plane: B waits for T from the rank below
@@ -459,13 +457,12 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         ptx::tc_fence_before();
         // x-pairs: P(iy) of node (lx, ly) = own (-x,-y) corner + lane lx-1's (+x,-y) corner;
         // the +y corners give P(iy-1) of node (lx, ly+1), exchanged through smem
-        double(*ys)[EX][3] = S.ysum[s3][hf];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const double pm = __shfl_up_sync(0xffffffffu, fc[3 * 1 + c], 1, EX);   // (+x,-y) of lx-1
             const double pp = __shfl_up_sync(0xffffffffu, fc[3 * 2 + c], 1, EX);   // (+x,+y) of lx-1
             plo[c] = __dadd_rn(fc[3 * 0 + c], pm);
-            ys[ly][lx][c] = __dadd_rn(fc[3 * 3 + c], pp);
+            S.ysum[s3][hf][c][ly][lx] = __dadd_rn(fc[3 * 3 + c], pp);
         }
     };
 
