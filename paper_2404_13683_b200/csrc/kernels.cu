@@ -386,6 +386,8 @@ cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, c
     if ((e = cudaMemcpyToSymbolAsync(c_K8, k8, 1152, 0, cudaMemcpyHostToDevice, st))) return e;
     if ((e = cudaMemcpyToSymbolAsync(c_Kk, kk, 576 * 8, 0, cudaMemcpyHostToDevice, st))) return e;
     if ((e = cudaMemcpyToSymbolAsync(c_Kg, kg, 576 * 8, 0, cudaMemcpyHostToDevice, st))) return e;
+    i8_bimg_kernel<<<1, 512, 0, st>>>();   // the INT8 kernel's B-operand image from c_K8
+    if ((e = cudaGetLastError())) return e;
     return cudaStreamSynchronize(st);
 }
 
