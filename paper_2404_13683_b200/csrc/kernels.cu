@@ -347,6 +347,11 @@ int num_sms() {
 }
 
 int choose_zchunk(int64_t planes, int64_t tiles_xy, int ctas_per_sm) {
+    static const int forced = [] {   // tuning knob (tools): OVX_ZCHUNKS=n forces n z-chunks
+        const char *e = std::getenv("OVX_ZCHUNKS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) return (int)((planes + forced - 1) / forced);
     const int64_t slots = (int64_t)num_sms() * ctas_per_sm;
     const int64_t nmax = std::max<int64_t>(1, planes / 8);
     int64_t best_n = 1, best_cost = -1;
