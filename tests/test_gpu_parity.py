@@ -446,3 +446,34 @@ def test_full_size_c4_sampled(ovxmod, name, path):
     pts = [(0, 0, 0), (891, 352, 1056), (cx, 100, cz), (cx + 41, 5, cz), (cx - 41, 351, cz), (cx, 200, cz + 41),
            (400, 176, 1056 - 52), (10, 10, 1056 - 211), (890, 1, 1056 - 475)]
     _sampled_apply_check(ovxmod, m, path, u, pts)
+
+
+def test_smem_a_variant_bit_exact(ovxmod):
+    """The alternate INT8 kernel (OVX_I8_KERNEL=smem: A operand in shared memory instead of TMEM),
+    selected once per process, in a subprocess: apply_K and a 30-step trajectory bit-exact vs the
+    oracle on the ragged multi-tile grid."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tests')
+import oracle, workloads as wl
+from paper_2404_13683_b200 import Ovx
+m = wl.small_random(40, 8, 70, ds=0.01, dt=1e-6)
+wl.point_source(m, 17, 3, 35, 1, 1e5, 2e-5, 30, scale=1.0)
+u = wl.random_field(m) * 1e-3
+s = Ovx(0); s.load_model(m, 0)
+f = s.apply_K(u)
+assert np.array_equal(f, oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=oracle.PATH_INT8))
+s.set_state(u, u, 0); s.step(30)
+v, vp, _ = s.get_state()
+r, rp, _, st = oracle.run(m.as_dict(), u, u, 0, 30, path=oracle.PATH_INT8)
+assert st == 0 and np.array_equal(v, r) and np.array_equal(vp, rp)
+print('ok')
+"""
+    env = dict(os.environ, OVX_I8_KERNEL="smem")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
