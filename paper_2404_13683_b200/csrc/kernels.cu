@@ -10,13 +10,13 @@
 //
 // Kernels (paths of include/ovx.h):
 //   step_i8w  OVX_INT8: PAPER.md Eq. 9 via Eqs. 10-17 — s_e = max|ū_e|, v = trunc(2^{7M} ū_e/s_e),
-//             byte slices of v + 2^{7M} (variant B) as the u8 A operand of tcgen05.mma.kind::i8
-//             (M=128 elements, N=48, 4 half-word arrays), −K_e^INT8 ⊗ I_2 and the folded Eq. 9
+//             byte slices of v + 2^{7M} (variant B) as the u8 A operand (in TMEM) of
+//             tcgen05.mma.kind::i8 (M=128 elements, N=48, 4 half-word arrays), −K_e^INT8 ⊗ I_2 and the folded Eq. 9
 //             diagonal (variant D) as the resident s8 B operand, s32 accumulators in TMEM, exact
 //             two-limb recombination, f_e = RN(c1 s_e 2^{-7M})·RN(y).
 //   step_f64  OVX_FP64 / OVX_VFEM: factored FP64 element forces (Walsh-Hadamard modes of the
 //             corner values; OVFEM or trilinear VFEM weights), shuffle / SMEM node sums.
-//   step_v1   OVX_FP64_DENSE / OVX_VFEM_DENSE (and the FP64 z-slab / debug variants): the literal
+//   step_v1   OVX_FP64_DENSE / OVX_VFEM_DENSE (and the FP64 / VFEM debug records): the literal
 //             dense form with sequential _rn sums, a bit-exact mirror of the test oracle's definition.
 #include <algorithm>
 #include <cstdlib>

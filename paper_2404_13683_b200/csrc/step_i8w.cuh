@@ -1,14 +1,15 @@
 // step_i8w.cuh — fused time step of the INT8 tensor-core path (OVX_INT8); included by kernels.cu.
 //
 // CTA = 32 × 8 elements per layer (one halo ring recomputed by the neighbour tiles), marching in
-// z over a chunk of node planes; 512 threads, two per element.  The TMEM budget (2 M-tiles × 256
-// columns = all 512) and ~200 KB of shared memory allow one CTA per SM, so each element's work is
-// split across two threads to double the resident warps:
+// z over a chunk of node planes; 512 threads, two per element.  The TMEM budget (D of both M-tiles,
+// 2 × 192 columns, plus the shared A operand, 112: all 512 allocated) and the register file allow
+// one CTA per SM, so each element's work is split across two threads to double the resident warps:
 //   * warp w: M-tile mt = w/8, half hf = (w/4)&1, TMEM lane quadrant q = w&3; element row
 //     32q + lane of M-tile mt = tile element (lx = lane, ly = 4mt + q);
 //   * conversion (Eqs. 10-16): s_e = max|ū_e| from per-node maxima |u| kept with each
 //     smem u plane; half 0 writes A chunks {0,1,3} (ū values 0-15 and the G copy of 0-7), half 1
-//     chunks {2,4,5}; one elected lane per M-tile issues the tcgen05.mma.kind::i8 chain
+//     chunks {2,4,5}, with tcgen05.st into the TMEM A operand (TA; OVX_I8_KERNEL=smem: shared
+//     memory); one elected lane per M-tile issues the tcgen05.mma.kind::i8 chain
 //     (4 arrays × [3 K-steps against −K_e^INT8 ⊗ I_2 + 2 K-steps of the G bytes against
 //     −128·I ⊗ I_2] = Eq. 17 with the Eq. 9 diagonal folded in, variant D);
 //   * epilogue: half hf reads the accumulators of outputs 12hf..12hf+11 = the 4 corner nodes of
