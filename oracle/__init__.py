@@ -29,10 +29,11 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 
 def build(force: bool = False) -> str:
-    """Compile the C oracle with gcc (no fast-math, no FMA contraction)."""
+    """Compile the C oracle with gcc (no fast-math, no FMA contraction; OpenMP over the independent
+    element forces only — results are bit-identical for any OMP_NUM_THREADS)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-std=c11",
-                               "-ffp-contract=off", "-fno-fast-math", "-o", _LIB, _SRC, "-lm"])
+                               "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 
@@ -56,9 +57,11 @@ def lib() -> ctypes.CDLL:
                                       _dp, _i64p, _i32p, _i64p, _i64p, _i64p, _dp]
     L.oracle_element_int8.restype = _int
     L.oracle_apply_K.argtypes = [_i64, _i64, _i64, _d, _u8p, _dp, _dp, _int,
-                                 _i32p, _i32p, _i8p, _int, _int, _dp, _dp]
+                                 _i32p, _i32p, _i8p, _int, _int, _int, _dp, _dp]
+    L.oracle_apply_K3.argtypes = [_i64, _i64, _i64, _d, _u8p, _dp, _dp, _int,
+                                  _i32p, _i32p, _i8p, _int, _int, _dp, _dp, _dp, _dp]
     L.oracle_run.argtypes = [_i64, _i64, _i64, _d, _u8p, _dp, _dp, _dp, _u8p,
-                             _int, _i32p, _i32p, _i8p, _int, _int,
+                             _int, _i32p, _i32p, _i8p, _int, _int, _int,
                              _int, _i64p, _i32p, _i64, _dp, _d, _d, _d, _dp, _dp, _i64p, _i64]
     L.oracle_run.restype = _int
     L.oracle_element_nodes.argtypes = [_i64, _i64, _i64, _i64p]
@@ -100,6 +103,12 @@ def element_vfem(ue, kappa: float, G: float, ds: float) -> np.ndarray:
                               _p(fe, _dp))
     return fe
 DIGITS_PAPER, DIGITS_BYTES = 0, 1
+# Summation order of f_n = Σ_e f_e[n] (ovx_oracle.c, oracle_apply_K):
+#   ORDER_ELEMENT — the definition: plain scatter in element id order;
+#   ORDER_U2      — MIRROR VARIANT of the B200 kernels' per-node pairwise tree (reading U2),
+#                   used only where a test wants the kernels' bits; never the reference physics.
+#   ORDER_ABS     — not a product: Σ_e |f_e[n]|, the scale of the cross-order rounding bound.
+ORDER_ELEMENT, ORDER_U2, ORDER_ABS = 0, 1, 2
 DIGITS_BYTES_FOLD = 3      # byte slices + Eq. 9 diagonal term in the integer product (variant D)
 
 
@@ -169,7 +178,8 @@ def _path_matrices(path):
     return K8, Kk, Kg
 
 
-def apply_K(nx, ny, nz, ds, mat, kappa, G, u, path=PATH_FP64, M=8, digits=DIGITS_BYTES_FOLD) -> np.ndarray:
+def apply_K(nx, ny, nz, ds, mat, kappa, G, u, path=PATH_FP64, M=8, digits=DIGITS_BYTES_FOLD,
+            order=ORDER_ELEMENT) -> np.ndarray:
     K8, Kk, Kg = _path_matrices(path)
     mat = np.ascontiguousarray(mat, dtype=np.uint8)
     kappa = np.ascontiguousarray(kappa, dtype=np.float64)
@@ -177,12 +187,28 @@ def apply_K(nx, ny, nz, ds, mat, kappa, G, u, path=PATH_FP64, M=8, digits=DIGITS
     u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
     f = np.zeros_like(u)
     lib().oracle_apply_K(nx, ny, nz, ds, _p(mat, _u8p), _p(kappa, _dp), _p(G, _dp), path,
-                         _p(Kk, _i32p), _p(Kg, _i32p), _p(K8, _i8p), M, digits,
+                         _p(Kk, _i32p), _p(Kg, _i32p), _p(K8, _i8p), M, digits, int(order),
                          _p(u, _dp), _p(f, _dp))
     return f
 
 
-def run(model, u, u_prev, it: int, nsteps: int, path=PATH_FP64, M=8, digits=DIGITS_BYTES_FOLD):
+def apply_K_orders(nx, ny, nz, ds, mat, kappa, G, u, path=PATH_FP64, M=8, digits=DIGITS_BYTES_FOLD):
+    """One element pass, three scatters: (f in element order = the definition, f in the U2 mirror
+    order, Σ_e |f_e[n]| = the cross-order rounding-bound scale)."""
+    K8, Kk, Kg = _path_matrices(path)
+    mat = np.ascontiguousarray(mat, dtype=np.uint8)
+    kappa = np.ascontiguousarray(kappa, dtype=np.float64)
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
+    fa, fb, fc = np.zeros_like(u), np.zeros_like(u), np.zeros_like(u)
+    lib().oracle_apply_K3(nx, ny, nz, ds, _p(mat, _u8p), _p(kappa, _dp), _p(G, _dp), path,
+                          _p(Kk, _i32p), _p(Kg, _i32p), _p(K8, _i8p), M, digits,
+                          _p(u, _dp), _p(fa, _dp), _p(fb, _dp), _p(fc, _dp))
+    return fa, fb, fc
+
+
+def run(model, u, u_prev, it: int, nsteps: int, path=PATH_FP64, M=8, digits=DIGITS_BYTES_FOLD,
+        order=ORDER_ELEMENT):
     """Advance (u, u_prev, it) by nsteps with the model dict produced by workloads.
 
     model keys: nx, ny, nz, ds, mat (uint8 per element), rho/kappa/G (per material),
@@ -207,7 +233,7 @@ def run(model, u, u_prev, it: int, nsteps: int, path=PATH_FP64, M=8, digits=DIGI
     itp = np.array([it], dtype=np.int64)
     st = lib().oracle_run(nx, ny, nz, ds, _p(mat, _u8p), _p(kappa, _dp), _p(G, _dp), _p(w, _dp),
                           None if dm is None else _p(dm, _u8p),
-                          path, _p(Kk, _i32p), _p(Kg, _i32p), _p(K8, _i8p), M, digits,
+                          path, _p(Kk, _i32p), _p(Kg, _i32p), _p(K8, _i8p), M, digits, int(order),
                           len(src_node), _p(src_node, _i64p), _p(src_axis, _i32p), n_t,
                           _p(amp, _dp), float(model["dt"]), float(model.get("alpha", 0.0)),
                           float(model.get("beta", 0.0)), _p(u, _dp), _p(up, _dp), _p(itp, _i64p), nsteps)

@@ -209,9 +209,19 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
     return degenerate;
 }
 
-/* f = Σ_e scatter(K_e u_e).  The paper adds element results directly into the global vector
- * (atomic adds: order unspecified); reading U2 fixes one order, a
- * pairwise tree per node n = (ix, iy, iz):
+/* f = Σ_e scatter(K_e u_e) (Eq. 2 assembled element by element; SURVEY
+ * §8(c)(i) step 4).  The paper adds element results straight into the global vector (atomics, order
+ * unspecified); the DEFINITION used here is the plain one:
+ *
+ *   order == ORDER_ELEMENT (0):  f = +0.0;  for e = 0 .. E-1 (element id order),
+ *                                for local node a = 0 .. 7, for axis c = 0 .. 2:
+ *                                    f[3·node_a(e) + c] += fe_e[3a + c].
+ *
+ * order == ORDER_ABS (2) is not a product: Σ_e |f_e[n]| (element order), the scale of the rounding
+ * bound  |Σ in one order − Σ in another| ≤ 2·γ_7·Σ_e |f_e[n]|  that tests use across orders.
+ * order == ORDER_U2 (1) is a MIRROR VARIANT, not the definition: the per-node pairwise tree the
+ * B200 kernels sum in (reading U2), kept so that tests can also compare the kernels bit
+ * for bit.  Any two orders differ only by the rounding of an 8-term sum (≤ 2·γ_7·Σ|terms|):
  *   f_n = T_n + B_n,  T_n = face(iz-1, top corners),  B_n = face(iz, bottom corners),
  *   face(ez, z) = P(iy) + P(iy-1),
  *   P(iy)   = f(ix, iy,   ez)[(-x,-y,z)] + f(ix-1, iy,   ez)[(+x,-y,z)],
@@ -238,34 +248,80 @@ static double face_sum(const double *fe_all, int64_t nx, int64_t ny, int64_t nz,
     return p0 + p1;
 }
 
-void oracle_apply_K(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat,
-                    const double *kappa, const double *G, int path,
-                    const int32_t *Kk, const int32_t *Kg, const int8_t *K8, int M, int digits,
-                    const double *u, double *f) {
+/* Element forces of every element (f_e of the chosen path), 24 per element in element id order. */
+static double *element_forces_all(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat,
+                                  const double *kappa, const double *G, int path,
+                                  const int32_t *Kk, const int32_t *Kg, const int8_t *K8, int M, int digits,
+                                  const double *u) {
     int64_t ne = nx * ny * nz;
     double *fe_all = (double *)malloc(sizeof(double) * 24 * (size_t)(ne > 0 ? ne : 1));
-    int64_t nodes[8];
-    double ue[24];
+    /* The element forces are independent of each other (each depends only on u_e); OpenMP may
+     * compute them on several host threads (OMP_NUM_THREADS; 1 = the plain serial loop) — the
+     * arithmetic of every element and the summations are unchanged, so the result is the same
+     * bits for any thread count. */
+#pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < ne; ++e) {
-        oracle_element_nodes(nx, ny, e, nodes);
+        int64_t en[8];
+        double ue[24];
+        oracle_element_nodes(nx, ny, e, en);
         for (int a = 0; a < 8; ++a)
-            for (int c = 0; c < 3; ++c) ue[3 * a + c] = u[3 * nodes[a] + c];
+            for (int c = 0; c < 3; ++c) ue[3 * a + c] = u[3 * en[a] + c];
         int m = mat[e];
         if (path == 0) oracle_element_fp64(ue, kappa[m], G[m], ds, Kk, Kg, fe_all + 24 * e);
         else if (path == 2) oracle_element_vfem(ue, kappa[m], G[m], ds, Kk, Kg, fe_all + 24 * e);
         else oracle_element_int8(ue, kappa[m], G[m], ds, K8, M, digits,
                                  NULL, NULL, NULL, NULL, NULL, NULL, fe_all + 24 * e);
     }
-    for (int64_t iz = 0; iz <= nz; ++iz)
-        for (int64_t iy = 0; iy <= ny; ++iy)
-            for (int64_t ix = 0; ix <= nx; ++ix) {
-                int64_t n = oracle_node_id(nx, ny, ix, iy, iz);
+    return fe_all;
+}
+
+/* Scatter of the element forces into node forces in one order (0 element, 1 U2 mirror, 2 |·| bound). */
+static void scatter(int64_t nx, int64_t ny, int64_t nz, const double *fe_all, int order, double *f) {
+    int64_t ne = nx * ny * nz, nn = (nx + 1) * (ny + 1) * (nz + 1);
+    int64_t nodes[8];
+    if (order == 0 || order == 2) {       /* the definition: element order (2: magnitudes) */
+        for (int64_t i = 0; i < 3 * nn; ++i) f[i] = 0.0;
+        for (int64_t e = 0; e < ne; ++e) {
+            oracle_element_nodes(nx, ny, e, nodes);
+            for (int a = 0; a < 8; ++a)
                 for (int c = 0; c < 3; ++c) {
-                    double T = face_sum(fe_all, nx, ny, nz, ix, iy, iz - 1, 1, c);
-                    double B = face_sum(fe_all, nx, ny, nz, ix, iy, iz, 0, c);
-                    f[3 * n + c] = T + B;
+                    double t = fe_all[24 * e + 3 * a + c];
+                    f[3 * nodes[a] + c] += order == 2 ? fabs(t) : t;
                 }
-            }
+        }
+    } else {                              /* mirror variant U2 */
+        for (int64_t iz = 0; iz <= nz; ++iz)
+            for (int64_t iy = 0; iy <= ny; ++iy)
+                for (int64_t ix = 0; ix <= nx; ++ix) {
+                    int64_t n = oracle_node_id(nx, ny, ix, iy, iz);
+                    for (int c = 0; c < 3; ++c) {
+                        double T = face_sum(fe_all, nx, ny, nz, ix, iy, iz - 1, 1, c);
+                        double B = face_sum(fe_all, nx, ny, nz, ix, iy, iz, 0, c);
+                        f[3 * n + c] = T + B;
+                    }
+                }
+    }
+}
+
+void oracle_apply_K(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat,
+                    const double *kappa, const double *G, int path,
+                    const int32_t *Kk, const int32_t *Kg, const int8_t *K8, int M, int digits,
+                    int order, const double *u, double *f) {
+    double *fe_all = element_forces_all(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, u);
+    scatter(nx, ny, nz, fe_all, order, f);
+    free(fe_all);
+}
+
+/* The three scatters of one set of element forces (any output may be NULL): the definition
+ * (element order), the U2 mirror, and the |·| bound scale — one element pass for all three. */
+void oracle_apply_K3(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat,
+                     const double *kappa, const double *G, int path,
+                     const int32_t *Kk, const int32_t *Kg, const int8_t *K8, int M, int digits,
+                     const double *u, double *f_elem, double *f_u2, double *f_abs) {
+    double *fe_all = element_forces_all(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, u);
+    if (f_elem) scatter(nx, ny, nz, fe_all, 0, f_elem);
+    if (f_u2) scatter(nx, ny, nz, fe_all, 1, f_u2);
+    if (f_abs) scatter(nx, ny, nz, fe_all, 2, f_abs);
     free(fe_all);
 }
 
@@ -286,7 +342,7 @@ void oracle_apply_K(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t
 int oracle_run(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat,
                const double *kappa, const double *G, const double *w, const uint8_t *dmask,
                int path, const int32_t *Kk, const int32_t *Kg, const int8_t *K8, int M, int digits,
-               int nsrc, const int64_t *src_node, const int32_t *src_axis, int64_t n_t,
+               int order, int nsrc, const int64_t *src_node, const int32_t *src_axis, int64_t n_t,
                const double *amp, double dt, double alpha, double beta,
                double *u, double *u_prev, int64_t *it, int64_t nsteps) {
     int64_t nn = (nx + 1) * (ny + 1) * (nz + 1);
@@ -302,9 +358,9 @@ int oracle_run(int64_t nx, int64_t ny, int64_t nz, double ds, const uint8_t *mat
                 double d = u[i] - u_prev[i];
                 ut[i] = u[i] + cb * d;
             }
-            oracle_apply_K(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, ut, f);
+            oracle_apply_K(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, order, ut, f);
         } else {
-            oracle_apply_K(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, u, f);
+            oracle_apply_K(nx, ny, nz, ds, mat, kappa, G, path, Kk, Kg, K8, M, digits, order, u, f);
         }
         for (int k = 0; k < nsrc; ++k)
             F[3 * src_node[k] + src_axis[k]] += (*it < n_t) ? amp[(int64_t)k * n_t + *it] : 0.0;

@@ -2,7 +2,8 @@
 
 Implements the same begin / iface / end contract as paper_2404_13683_b200.dist.OvxCompute,
 with the oracle's element forces and update, so the distributed protocol in dist.py can be
-checked bit-for-bit against the monolithic oracle run on CPU (world size 2, 3 over gloo)."""
+checked bit-for-bit against the monolithic oracle run in the same summation order (the mirror
+variant ORDER_U2) on CPU, and within round-off of the plain element-order definition (world size 2, 3 over gloo)."""
 import numpy as np
 import torch
 
@@ -39,7 +40,9 @@ class OracleSlabCompute:
 
     def begin(self):
         lm, nn2 = self.lm, self.nn2
-        f = oracle.apply_K(lm.nx, lm.ny, lm.nz, lm.ds, lm.mat, lm.kappa, lm.G, self.u, path=self.path)
+        # the z-slab protocol reproduces the kernels' per-node tree f = T + B (mirror order U2)
+        f = oracle.apply_K(lm.nx, lm.ny, lm.nz, lm.ds, lm.mat, lm.kappa, lm.G, self.u, path=self.path,
+                           order=oracle.ORDER_U2)
         F = self._forces()
         self.F = F
         if self.slab.flags & 2:

@@ -88,9 +88,11 @@ def test_gloo_slabs_equal_monolithic_run(tmp_path, world, path):
     m = _model()
     rng = np.random.default_rng(5)
     u0 = rng.standard_normal(3 * m.n_nodes) * 1e-6
-    ru, rup, _, st = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=path)
+    ru, rup, _, st = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=path, order=oracle.ORDER_U2)
     assert st == 0
     assert np.array_equal(got[0], ru) and np.array_equal(got[1], rup)
+    pu, _, _, _ = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=path)   # the definition's order
+    assert np.linalg.norm(got[0] - pu) <= 1e-12 * np.linalg.norm(pu)
 
 
 def test_host_staged_transport_equals_monolithic(tmp_path):
@@ -103,6 +105,6 @@ def test_host_staged_transport_equals_monolithic(tmp_path):
     m = _model()
     rng = np.random.default_rng(5)
     u0 = rng.standard_normal(3 * m.n_nodes) * 1e-6
-    ru, rup, _, st = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=oracle.PATH_INT8)
+    ru, rup, _, st = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=oracle.PATH_INT8, order=oracle.ORDER_U2)
     assert st == 0
     assert np.array_equal(got[0], ru) and np.array_equal(got[1], rup)

@@ -44,10 +44,57 @@ def test_ebe_matches_dense_assembly(dims):
         assert np.linalg.norm(f - ref) <= 1e-14 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("path", [oracle.PATH_FP64, oracle.PATH_INT8, oracle.PATH_VFEM])
+@pytest.mark.parametrize("order", [oracle.ORDER_ELEMENT, oracle.ORDER_U2])
+def test_scatter_exact_arithmetic_equals_dense_assembly(path, order):
+    """Pin of the scatter that does not restate it: with κ = 256, G = 384,
+    ds = 1 the element matrices are integer (A_κ·256 + A_G·384 = K^κ + K̄^G + 128 I; VFEM: Vk·256/72 +
+    Vg·384/216 is not integer, so VFEM uses κ = 72, G = 216) and u ∈ {−2..2}, so every element force
+    and every partial sum is an exact integer: f must equal the brute-force dense assembly K @ u bit
+    for bit in ANY summation order.  A transposed corner, a wrong node id, a dropped or duplicated
+    element fails.  INT8: every s_e ∈ {1, 2} is a power of two and cG = 1, so ū/s_e·2^56 is exact,
+    no truncation happens and f_e = K_e u_e exactly (Eqs. 10-17 reduce to the exact product)."""
+    m = wl.small_random(3, 4, 2, ds=1.0)
+    if path == oracle.PATH_VFEM:
+        m.kappa = np.full_like(m.kappa, 72.0)
+        m.G = np.full_like(m.G, 216.0)
+        from fractions import Fraction as Fr
+        from oracle.element import vfem_element_stiffness
+        K = np.zeros((3 * m.n_nodes, 3 * m.n_nodes))
+        Ke = np.array([[float(x) for x in r] for r in vfem_element_stiffness(Fr(72), Fr(216), Fr(1))])
+        for e in range(m.n_elems):
+            d = np.concatenate([[3 * n, 3 * n + 1, 3 * n + 2] for n in oracle.element_nodes(m.nx, m.ny, e)])
+            K[np.ix_(d, d)] += Ke
+    else:
+        m.kappa = np.full_like(m.kappa, 256.0)
+        m.G = np.full_like(m.G, 384.0)
+        K = assemble.assemble_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G)
+    assert np.array_equal(K, np.round(K))
+    rng = np.random.default_rng(11)
+    u = rng.integers(-2, 3, size=3 * m.n_nodes).astype(np.float64)
+    f = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=path, order=order)
+    assert np.array_equal(f, K @ u)
+    assert np.abs(f).max() > 0
+
+
 @pytest.mark.parametrize("path", [oracle.PATH_FP64, oracle.PATH_INT8])
-def test_summation_order_is_the_u2_tree(path):
-    """Reading U2: f_n = T_n + B_n with face(ez) = P(iy) + P(iy-1), P = x-pair of corner values
-    (missing elements 0.0), rebuilt here from the per-element forces one node at a time."""
+def test_u2_mirror_differs_from_the_definition_only_by_summation_rounding(path):
+    """The mirror variant (ORDER_U2, the kernels' tree) and the definition (element order) sum the
+    same 8 terms per node: |f_U2 − f_elem| ≤ 2·γ_7·Σ_e |f_e[n]| ≤ 2·γ_7·(|K| |u|)_n (γ_7 = 7u/(1−7u))."""
+    m = wl.small_random(5, 4, 3, ds=0.01)
+    u = wl.random_field(m) * np.exp(np.random.default_rng(5).uniform(-8, 8, 3 * m.n_nodes))
+    fa = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=path)
+    fb = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=path, order=oracle.ORDER_U2)
+    K = assemble.assemble_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G)
+    bound = 2 * 8 * 2.0 ** -53 * 1.001 * (np.abs(K) @ np.abs(u))
+    assert np.all(np.abs(fa - fb) <= bound)
+    assert not np.array_equal(fa, fb)          # the two orders are really different
+
+
+def test_u2_mirror_variant_is_the_documented_tree():
+    """Implementation check of the MIRROR variant (not a pin of the definition): the oracle's
+    ORDER_U2 equals reading U2 rebuilt node by node from the per-element forces."""
+    path = oracle.PATH_INT8
     m = wl.small_random(3, 2, 2, ds=0.01)
     u = wl.random_field(m) * np.exp(np.random.default_rng(5).uniform(-8, 8, 3 * m.n_nodes))
     nx, ny, nz = m.nx, m.ny, m.nz
@@ -56,9 +103,7 @@ def test_summation_order_is_the_u2_tree(path):
         nodes = oracle.element_nodes(nx, ny, e)
         ue = np.concatenate([u[3 * q:3 * q + 3] for q in nodes])
         k = m.mat[e]
-        fe[(e % nx, (e // nx) % ny, e // (nx * ny))] = (
-            oracle.element_fp64(ue, m.kappa[k], m.G[k], m.ds) if path == oracle.PATH_FP64
-            else oracle.element_int8(ue, m.kappa[k], m.G[k], m.ds)["fe"])
+        fe[(e % nx, (e // nx) % ny, e // (nx * ny))] = oracle.element_int8(ue, m.kappa[k], m.G[k], m.ds)["fe"]
     corner = {(0, 0): 0, (0, 1): 1, (1, 1): 2, (1, 0): 3}   # (dy, dx) -> local node of e(ix-dx, iy-dy)
 
     def val(ix, iy, ez, dx, dy, top, c):
@@ -75,7 +120,7 @@ def test_summation_order_is_the_u2_tree(path):
                             (val(ix, iy, ez, 0, 1, top, c) + val(ix, iy, ez, 1, 1, top, c))
                             for ez, top in ((iz - 1, 1), (iz, 0))]
                     ref[3 * n + c] = face[0] + face[1]
-    f = oracle.apply_K(nx, ny, nz, m.ds, m.mat, m.kappa, m.G, u, path=path)
+    f = oracle.apply_K(nx, ny, nz, m.ds, m.mat, m.kappa, m.G, u, path=path, order=oracle.ORDER_U2)
     assert np.array_equal(f, ref)
 
 
@@ -180,3 +225,84 @@ def test_int8_and_fp64_trajectories_agree():
     a, _, _, _ = oracle.run(m.as_dict(), z, z, 0, 300, path=oracle.PATH_FP64)
     b, _, _, _ = oracle.run(m.as_dict(), z, z, 0, 300, path=oracle.PATH_INT8)
     assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(a)
+
+
+def _impulse_model(amp_series, node=(2, 1, 3), axis=1):
+    m = wl.small_random(4, 3, 4, ds=0.01, dt=1e-6)
+    m.dirichlet = wl.corner_mask(m.nx, m.ny, m.nz)
+    n = m.node(*node)
+    m.src_node = np.array([n], dtype=np.int64)
+    m.src_axis = np.array([axis], dtype=np.int32)
+    m.amp = np.array(amp_series, dtype=np.float64).reshape(1, -1)
+    return m, 3 * n + axis
+
+
+@pytest.mark.parametrize("path", [oracle.PATH_FP64, oracle.PATH_INT8])
+def test_source_impulse_enters_at_its_dof_and_step(path):
+    """Source term of Eq. 3 (M ü + K u = F, F^{it} at t = it·dt):
+    from u^0 = u^{-1} = 0 a single impulse amp[0] = a gives u^1 = w_n·a at exactly that DOF and 0
+    elsewhere (K·0 = 0); u^2 = 2u^1 − w ⊙ (K u^1) (brute-force K); an impulse at amp[1] leaves u^1 = 0
+    and gives u^2 = w_n·a; a run started at it = 5 uses amp[5]; it ≥ n_t contributes nothing.
+    A wrong sign of F, an amp[it+1] index or a wrong DOF fails here."""
+    a = 3.25e3
+    m, dof = _impulse_model([a, 0.0, 0.0, 0.0])
+    z = np.zeros(3 * m.n_nodes)
+    w = oracle.node_w(m.nx, m.ny, m.nz, m.ds, m.mat, m.rho, m.dt)
+    u1, u0, it, st = oracle.run(m.as_dict(), z, z, 0, 1, path=path)
+    assert st == 0 and it == 1 and np.all(u0 == 0)
+    exp1 = np.zeros_like(z)
+    exp1[dof] = w[dof // 3] * a
+    assert np.array_equal(u1, exp1)
+    u2, u1b, _, _ = oracle.run(m.as_dict(), u1, u0, 1, 1, path=path)
+    assert np.array_equal(u1b, u1)
+    K = assemble.assemble_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G)
+    ref2 = 2 * u1 - np.repeat(w, 3) * (K @ u1)
+    ref2[(np.tile([1, 2, 4], m.n_nodes) & np.repeat(m.dirichlet, 3)) > 0] = 0.0   # fixed components
+    assert np.abs(u2 - ref2).max() <= 1e-13 * np.abs(ref2).max()
+    # impulse one step later
+    m, dof = _impulse_model([0.0, a, 0.0])
+    u1, _, _, _ = oracle.run(m.as_dict(), z, z, 0, 1, path=path)
+    assert np.all(u1 == 0)
+    u2, _, _, _ = oracle.run(m.as_dict(), z, z, 0, 2, path=path)
+    assert u2[dof] == w[dof // 3] * a and np.count_nonzero(u2) == 1
+    # start at it = 5: amp[5] is used; beyond n_t nothing
+    m, dof = _impulse_model([0, 0, 0, 0, 0, -a])
+    u6, _, it, _ = oracle.run(m.as_dict(), z, z, 5, 1, path=path)
+    assert it == 6 and u6[dof] == -w[dof // 3] * a and np.count_nonzero(u6) == 1
+    u7, _, _, _ = oracle.run(m.as_dict(), z, z, 6, 1, path=path)
+    assert np.all(u7 == 0)
+
+
+@pytest.mark.parametrize("path", [oracle.PATH_FP64, oracle.PATH_INT8])
+def test_energy_balance_with_a_ricker_source(path):
+    """Discrete work-energy balance of Eq. 3 with a source (derived by multiplying the scheme by
+    (u^{n+1} − u^{n−1})/2, M and K symmetric):
+        E_{n+½} − E_{n−½} = F^nᵀ (u^{n+1} − u^{n−1}) / 2,
+        E_{n+½} = ½ v_{n+½}ᵀ M v_{n+½} + ½ u^nᵀ K u^{n+1},  v_{n+½} = (u^{n+1} − u^n)/dt,
+    with M and K assembled by brute force, checked at every step of a Ricker run."""
+    m = wl.small_random(4, 3, 3, ds=1.0, dt=1e-4)
+    m.dirichlet = None
+    f0 = 400.0
+    wl.point_source(m, 2, 1, 3, 2, f0, 1.2 / f0, 80, scale=1e9)
+    K = assemble.assemble_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G)
+    md = assemble.assemble_M_diag(m.nx, m.ny, m.nz, m.ds, m.mat, m.rho)
+    F = np.zeros(3 * m.n_nodes)
+    dof = 3 * int(m.src_node[0]) + int(m.src_axis[0])
+    u = [np.zeros(3 * m.n_nodes), np.zeros(3 * m.n_nodes)]     # u^{-1}, u^0
+    for n in range(80):
+        un, _, _, st = oracle.run(m.as_dict(), u[-1], u[-2], n, 1, path=path)
+        assert st == 0
+        u.append(un)
+    E = [physics.leapfrog_energy(K, md, u[k], u[k + 1], m.dt) for k in range(1, 81)]   # E_{n+½}, n = 0..79
+    scale = max(abs(e) for e in E)
+    assert scale > 0
+    worst = 0.0
+    for n in range(1, 80):
+        F[:] = 0.0
+        F[dof] = m.amp[0, n]
+        work = F @ (u[n + 2] - u[n]) / 2.0     # u[k] = u^{k-1}
+        worst = max(worst, abs((E[n] - E[n - 1]) - work))
+    assert worst <= 1e-12 * scale
+    # the same balance with the amplitude one step late is violated (the index pin is sharp)
+    late = max(abs((E[n] - E[n - 1]) - m.amp[0, n + 1] * (u[n + 2] - u[n])[dof] / 2.0) for n in range(1, 79))
+    assert late > 1e3 * max(worst, 1e-300)
