@@ -70,3 +70,39 @@ def leapfrog_energy(K, m_diag, u_n, u_np1, dt) -> float:
 def ricker(t: np.ndarray, f0: float, t0: float) -> np.ndarray:
     a = (math.pi * f0 * (t - t0)) ** 2
     return (1.0 - 2.0 * a) * np.exp(-a)
+
+
+def bloch_symbol(kappa: float, G: float, ds: float, k) -> np.ndarray:
+    """OVFEM Bloch symbol Ŝ(k) (3×3, real symmetric) of the assembled K on a homogeneous voxel
+    lattice (derived from PAPER.md Eqs. 5-8 with the seven ψ modes, L80-L89):
+    s_i = sin(k_i ds/2), c_i = cos(k_i ds/2), λ = κ − 2G/3, μ = G,
+        Ŝ = ds Σ_β w_β [(λ+μ) conj(g_β) g_βᵀ + μ |g_β|² I],
+    with the mode weights w_β = 1/(Gram of ψ_β)·(ds³ normalisation) = 1, 3, 3, 3, 9, 9, 9 and
+        g_1 = 2i(s_x c_y c_z, c_x s_y c_z, c_x c_y s_z),
+        g_2 = −(0, s_x s_y c_z, s_x c_y s_z),  g_3 = −(s_x s_y c_z, 0, c_x s_y s_z),
+        g_4 = −(s_x c_y s_z, c_x s_y s_z, 0),
+        g_5 = −(i/2)(0, 0, s_x s_y s_z),  g_6 = −(i/2)(s_x s_y s_z, 0, 0),  g_7 = −(i/2)(0, s_x s_y s_z, 0).
+    Plane-wave eigenvalues of M⁻¹K: eig(Ŝ)/(ρ ds³)."""
+    sx, sy, sz = (math.sin(kk * ds / 2) for kk in k)
+    cx, cy, cz = (math.cos(kk * ds / 2) for kk in k)
+    sss = sx * sy * sz
+    g = [(1, 2j * np.array([sx * cy * cz, cx * sy * cz, cx * cy * sz])),
+         (3, -np.array([0.0, sx * sy * cz, sx * cy * sz])),
+         (3, -np.array([sx * sy * cz, 0.0, cx * sy * sz])),
+         (3, -np.array([sx * cy * sz, cx * sy * sz, 0.0])),
+         (9, -0.5j * np.array([0.0, 0.0, sss])),
+         (9, -0.5j * np.array([sss, 0.0, 0.0])),
+         (9, -0.5j * np.array([0.0, sss, 0.0]))]
+    lam, mu = kappa - 2.0 * G / 3.0, G
+    S = np.zeros((3, 3), dtype=complex)
+    for w, gb in g:
+        gb = gb.astype(complex)
+        S += w * ((lam + mu) * np.outer(np.conj(gb), gb) + mu * np.vdot(gb, gb) * np.eye(3))
+    assert np.abs(S.imag).max() <= 1e-15 * max(1.0, np.abs(S.real).max())
+    return ds * S.real
+
+
+def bloch_modes(kappa: float, G: float, rho: float, ds: float, k):
+    """(λ_i, U_i): eigenvalues of M⁻¹K (ascending) and unit eigenvectors of Ŝ(k) for a plane wave k."""
+    ev, U = np.linalg.eigh(bloch_symbol(kappa, G, ds, k))
+    return ev / (rho * ds ** 3), U

@@ -44,8 +44,10 @@ def test_slabs_on_one_gpu_equal_monolithic(world, path, overlap):
     # same kernel (step_i8w / step_f64) and summation order on slabs and on one context -> bit-identical
     assert np.array_equal(u, mu) and np.array_equal(up, mup)
     if path == 0:
-        ru, rup, _, _ = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=oracle.PATH_INT8)
+        ru, rup, _, _ = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=oracle.PATH_INT8, order=oracle.ORDER_U2)
         assert np.array_equal(u, ru)
+        pu, _, _, _ = oracle.run(m.as_dict(), u0, u0, 0, nsteps, path=oracle.PATH_INT8)   # the definition
+        assert np.linalg.norm(u - pu) <= 1e-12 * np.linalg.norm(pu)
 
 
 @pytest.mark.parametrize("path", [0, 1])
@@ -110,7 +112,7 @@ def test_damped_slabs_equal_monolithic(world, path):
     assert np.array_equal(u, mu) and np.array_equal(up, mup)
     if path in (0, 2):
         ru, rup, _, st = oracle.run(m.as_dict(), u0, up0, 0, nsteps,
-                                    path=oracle.PATH_INT8 if path == 0 else oracle.PATH_FP64)
+                                    path=oracle.PATH_INT8 if path == 0 else oracle.PATH_FP64, order=oracle.ORDER_U2)
         assert st == 0 and np.array_equal(u, ru) and np.array_equal(up, rup)
     ud, _, _, _ = oracle.run(m.as_dict() | {"alpha": 0.0, "beta": 0.0}, u0, up0, 0, nsteps, path=oracle.PATH_FP64)
     assert np.linalg.norm(u - ud) > 1e-6 * np.linalg.norm(ud)   # the damping acts

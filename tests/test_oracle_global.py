@@ -306,3 +306,38 @@ def test_energy_balance_with_a_ricker_source(path):
     # the same balance with the amplitude one step late is violated (the index pin is sharp)
     late = max(abs((E[n] - E[n - 1]) - m.amp[0, n + 1] * (u[n + 2] - u[n])[dof] / 2.0) for n in range(1, 79))
     assert late > 1e3 * max(worst, 1e-300)
+
+
+def test_bloch_symbol_axis_aligned_reduces_to_the_bar():
+    """Ŝ(k e_x) has the textbook 1-D lattice eigenvalues 4V²/ds² sin²(k ds/2) for V = Vp (×1) and
+    V = Vs (×2) — the closed form the axis-aligned GPU test uses."""
+    kap, G, rho, ds = 5.0 / 3.0, 1.0, 1.3, 0.7
+    for kk in (0.1, 1.0, 2.5):
+        lam, _ = physics.bloch_modes(kap, G, rho, ds, (kk, 0.0, 0.0))
+        vp, vs = math.sqrt((kap + 4 * G / 3) / rho), math.sqrt(G / rho)
+        ref = sorted([physics.lattice_lambda_axis(vs, kk, ds)] * 2 + [physics.lattice_lambda_axis(vp, kk, ds)])
+        assert np.allclose(lam, ref, rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("nu", ["0.25", "0.35"])
+@pytest.mark.parametrize("mvec", [(1, 2, 3), (3, 3, 3), (5, 1, 0), (4, 4, 0)])
+def test_oblique_roller_box_modes_are_exact_eigenvectors(nu, mvec):
+    """on a roller box, u_a = U_a sin(k_a x_a) Π_{b≠a} cos(k_b x_b) with U an
+    eigenvector of Ŝ(k) satisfies K u = λ M u exactly at every free DOF (the oracle's product,
+    independent of the symbol's derivation); then the time stepper follows cos(nθ),
+    cos θ = 1 − λ dt²/2 (Eq. 3 recurrence)."""
+    m = wl.c2_block(8, nu=nu)
+    k = [math.pi * mv / (8 * m.ds) for mv in mvec]
+    lam, U = physics.bloch_modes(m.kappa[0], m.G[0], m.rho[0], m.ds, k)
+    free = (np.tile([1, 2, 4], m.n_nodes) & np.repeat(m.dirichlet, 3)) == 0
+    md = assemble.assemble_M_diag(m.nx, m.ny, m.nz, m.ds, m.mat, m.rho)
+    for i in range(3):
+        u0 = wl.standing_wave(m, mvec=mvec, U=tuple(U[:, i]))
+        f = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u0)
+        res = f[free] - lam[i] * md[free] * u0[free]
+        assert np.linalg.norm(res) <= 1e-13 * np.linalg.norm(f[free])
+    th = math.acos(1 - lam[-1] * m.dt ** 2 / 2)
+    u0 = wl.standing_wave(m, mvec=mvec, U=tuple(U[:, -1]))
+    u, _, _, st = oracle.run(m.as_dict(), u0, math.cos(th) * u0, 0, 60)
+    assert st == 0
+    assert np.linalg.norm(u - math.cos(60 * th) * u0) <= 1e-12 * np.linalg.norm(u0)
