@@ -106,26 +106,43 @@ def _workload(n: int):
 
 
 def _slab_workload(n: int, world: int, rank: int):
-    """This rank's z-slab of the C5 weak-scaling grid n × n × (n·world) (homogeneous roller box
-    with a standing P wave along x), built locally: (local model, Slab, u0 of planes ez0..ez1)."""
+    """This rank's z-slab of the C5 weak-scaling grid (BASELINE configs[4]):
+    n × n × (n·world) elements, ds = 1 m, soil / rock alternating every 64 element layers (C3
+    materials), the 4 bottom corners fixed, a Ricker z-force (f0 = 25 Hz) at the top-surface
+    centre, dt = 1e-4 s; the initial field is a smooth standing wave along x (so that every element
+    carries data from the first step).  Built locally per rank: (local model, Slab, u0 of planes
+    ez0..ez1)."""
     import workloads as wl
     from paper_2404_13683_b200 import dist as D
     from types import SimpleNamespace
     nz = n * world
     ez0, ez1 = D.partition(nz, world, rank)
     slab = D.Slab(rank, world, ez0, ez1)
-    g = wl.c2_block(8)                       # materials / dt of C2 (ν = 0.25)
+    rho, kappa, G = wl._materials(wl.SOIL, wl.ROCK)
     nzl = ez1 - ez0
-    mask = wl.roller_mask(n, n, nz).reshape(nz + 1, -1)[ez0:ez1 + 1].reshape(-1)
-    lm = SimpleNamespace(nx=n, ny=n, nz=nzl, ds=1.0, rho=g.rho, kappa=g.kappa, G=g.G, dt=g.dt,
-                         mat=np.zeros(n * n * nzl, np.uint8),
-                         mat_below=np.zeros(n * n, np.uint8) if rank > 0 else None,
-                         dirichlet=np.ascontiguousarray(mask), src_node=np.zeros(0, np.int64),
-                         src_axis=np.zeros(0, np.int32), amp=np.zeros((0, 1)))
+    lay = ((np.arange(ez0 - (1 if rank > 0 else 0), ez1) // 64) % 2).astype(np.uint8)
+    mats = np.broadcast_to(lay[:, None], (lay.size, n * n)).reshape(-1)
+    nn2 = (n + 1) * (n + 1)
+    mask = np.zeros((nzl + 1) * nn2, np.uint8)
+    if rank == 0:
+        for ix, iy in ((0, 0), (n, 0), (0, n), (n, n)):
+            mask[ix + (n + 1) * iy] = 7
+    dt, f0 = 1e-4, 25.0
+    steps = 1 << 14
+    if rank == world - 1:
+        src = np.array([(n // 2) + (n + 1) * (n // 2) + nzl * nn2], dtype=np.int64)
+        amp = (1.0e6 * wl.ricker(np.arange(steps) * dt, f0, 1.2 / f0)).reshape(1, -1)
+        axis = np.array([2], dtype=np.int32)
+    else:
+        src, amp, axis = np.zeros(0, np.int64), np.zeros((0, 1)), np.zeros(0, np.int32)
+    lm = SimpleNamespace(nx=n, ny=n, nz=nzl, ds=1.0, rho=rho, kappa=kappa, G=G, dt=dt,
+                         mat=np.ascontiguousarray(mats[(n * n if rank > 0 else 0):]),
+                         mat_below=np.ascontiguousarray(mats[:n * n]) if rank > 0 else None,
+                         dirichlet=mask, src_node=src, src_axis=axis, amp=amp)
     k = math.pi * 16 / n
     x = np.arange(n + 1, dtype=np.float64)
     u = np.zeros((nzl + 1, n + 1, n + 1, 3))
-    u[..., 0] = np.sin(k * x)[None, None, :]
+    u[..., 0] = 1e-3 * np.sin(k * x)[None, None, :]
     return lm, slab, u.reshape(-1)
 
 
@@ -135,28 +152,87 @@ def _algorithmic_bytes(nn: int, ne: int) -> int:
     return 80 * nn + ne + nn
 
 
-def cpu_oracle_sample(path_name: str, steps: int, n: int = 64) -> dict:
-    """Time the oracle as it stands (single thread) on an n³ block of the C2 workload."""
+def _cpu_info() -> dict:
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def _oracle_path(path_name: str):
     import oracle
-    m, u0 = _workload(n)
     po = {"int8": oracle.PATH_INT8, "vfem": oracle.PATH_VFEM, "vfem_dense": oracle.PATH_VFEM}.get(path_name, oracle.PATH_FP64)
+    what = {"int8": "INT8-path emulation (int128)", "vfem": "VFEM path", "vfem_dense": "VFEM path"}.get(path_name, "FP64 path")
+    return po, what
+
+
+def _set_omp_threads(n: int) -> None:
+    """Thread count of the oracle's OpenMP element loop (libgomp reads it per parallel region via
+    omp_set_num_threads; results are bit-identical for any count)."""
+    import ctypes
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+    except OSError:
+        pass
+
+
+def _oracle_rate(path_name: str, n: int, steps: int, threads: int) -> tuple[float, float]:
+    """(element-updates/s, seconds) of the oracle as it stands on an n³ block of the C2 workload."""
+    import oracle
+    po, _ = _oracle_path(path_name)
+    m, u0 = _workload(n)
+    _set_omp_threads(threads)
     t0 = time.perf_counter()
     oracle.run(m.as_dict(), u0, u0, 0, steps, path=po)
     dt = time.perf_counter() - t0
-    what = {"int8": "INT8-path emulation (int128)", "vfem": "VFEM path", "vfem_dense": "VFEM path"}.get(path_name, "FP64 path")
-    return {"value": m.n_elems * steps / dt, "unit": METRIC, "cores": 1, "kind": "oracle",
-            "sample": f"{n}^3 block of the C2 workload (ν=0.25 roller box, standing P wave), {steps} steps, "
-                      f"{what}, 1 thread, {dt:.1f} s"}
+    return m.n_elems * steps / dt, dt
+
+
+def _sample_edge(path_name: str, threads: int, budget_s: float, steps: int) -> int:
+    """Largest n ≤ 256 (the C2 edge) whose `steps` oracle steps fit the time budget, from a 64³
+    calibration step (the oracle's cost is linear in the element count)."""
+    rate, _ = _oracle_rate(path_name, 64, 1, threads)
+    n = int((budget_s * rate / steps) ** (1.0 / 3.0))
+    return max(16, min(N_EDGE, n))
+
+
+def cpu_oracle_sample(path_name: str, budget_s: float = 20.0) -> dict:
+    """The oracle as it stands, timed on this host: (i) all cores (OpenMP over the independent
+    element forces; SURVEY §8(d) "oracle timing"), on the largest block of the C2 workload whose 2
+    steps fit ~budget_s (the full 256³ grid on a large host), and (ii) one thread on a 64³ block."""
+    info = _cpu_info()
+    cores = info["nproc"] or 1
+    _, what = _oracle_path(path_name)
+    n = _sample_edge(path_name, cores, budget_s, 2)
+    v_all, t_all = _oracle_rate(path_name, n, 2, cores)
+    v_one, t_one = _oracle_rate(path_name, 64, 2, 1)
+    return {"value": v_all, "unit": METRIC, "cores": cores, "kind": "oracle",
+            "sample": f"{n}^3 block of the C2 workload (ν=0.25 roller box, standing P wave; full C2 = 256^3), "
+                      f"2 steps, {what}, OpenMP over element forces on {cores} threads, {t_all:.1f} s",
+            "cpu_model": info["cpu_model"], "nproc": info["nproc"], "same_config": n == N_EDGE,
+            "single_thread": {"value": v_one, "unit": METRIC, "cores": 1,
+                              "sample": f"64^3 block, 2 steps, 1 thread, {t_one:.1f} s"}}
 
 
 def run_reference(args) -> None:
+    """The base contract's reference arm for this tier: the CPU oracle as it stands, on all host
+    cores, timed per step on the largest block of the C2 workload that keeps the whole
+    --steps/--warmup run within a few minutes (the full 256³ grid when the host is large enough)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = 48
     import oracle
+    info = _cpu_info()
+    cores = info["nproc"] or 1
+    po, what = _oracle_path(args.path)
+    n = _sample_edge(args.path, cores, args.ref_budget, args.steps + args.warmup)
     m, u0 = _workload(n)
-    po = {"int8": oracle.PATH_INT8, "vfem": oracle.PATH_VFEM, "vfem_dense": oracle.PATH_VFEM}.get(args.path, oracle.PATH_FP64)
+    _set_omp_threads(cores)
     u, up = u0, u0
     for _ in range(args.warmup):
         u, up, _, _ = oracle.run(m.as_dict(), u, up, 0, 1, path=po)
@@ -165,13 +241,15 @@ def run_reference(args) -> None:
         u, up, _, _ = oracle.run(m.as_dict(), u, up, 0, 1, path=po)
     dt = time.perf_counter() - t0
     value = m.n_elems * args.steps / dt
-    sample = f"{n}^3 block of the C2 workload per step ({m.n_elems} elements), oracle {args.path} path, 1 thread"
+    sample = (f"{n}^3 block of the C2 workload per step ({m.n_elems} elements; full C2 = 256^3), oracle {what}, "
+              f"OpenMP over element forces on {cores} threads")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": "C2 256^3 homogeneous block (sampled: %d^3)" % n,
-                                            "path": args.path},
-           "cpu_baseline": {"value": value, "unit": METRIC, "cores": 1, "kind": "oracle", "sample": sample},
+           "data": "synthetic", "config": {"workload": f"C2 256^3 homogeneous block (sampled: {n}^3)",
+                                            "path": args.path, "same_config": n == N_EDGE},
+           "cpu_baseline": {"value": value, "unit": METRIC, "cores": cores, "kind": "oracle", "sample": sample,
+                            "cpu_model": info["cpu_model"], "nproc": info["nproc"]},
            "e2e": {"value": value, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
@@ -237,6 +315,22 @@ class Sharded:
         return self.s.get_state(out_u=out_u, with_prev=False)[0]
 
 
+def _spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` outside torchrun: relaunch this command as N ranks (one process
+    per GPU, torch.distributed.run on 127.0.0.1); refuse (exit 2) when fewer than N GPUs exist."""
+    import socket
+    import torch
+    if os.environ.get("OVX_BENCH_DEVICE") is None and torch.cuda.device_count() < n:
+        print(f"bench.py: --gpus {n} needs {n} GPUs, {torch.cuda.device_count()} visible", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -247,11 +341,15 @@ def main() -> None:
     ap.add_argument("--n", type=int, default=N_EDGE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp64-companion", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="--impl reference: seconds of oracle work the whole run may take (sets the sample size)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args.gpus))
 
     import torch
     import torch.distributed as dist
@@ -259,6 +357,9 @@ def main() -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if os.environ.get("OVX_BENCH_DEVICE") is not None:   # test hook: all ranks on one device
         local = int(os.environ["OVX_BENCH_DEVICE"])
@@ -409,10 +510,14 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32 + f64" if path == OVX_INT8 else "f64",
-        "data": "synthetic (seeded; roller box with a standing P wave)",
+        "data": ("synthetic (seeded; roller box with a standing P wave)" if world == 1 else
+                 "synthetic (layered soil/rock, Ricker source, smooth initial field)"),
         "config": {"workload": (f"C2: {args.n}^3 homogeneous block" if world == 1 else
-                                f"C5: {args.n}x{args.n}x{args.n * world} homogeneous block, {args.n}^3 z-slab per GPU"),
-                   "material": "kappa=5/3, G=1, rho=1, ds=1, rollers", "path": args.path,
+                                f"C5: {args.n}x{args.n}x{args.n * world} layered soil/rock (64-layer period), "
+                                f"{args.n}^3 z-slab per GPU"),
+                   "material": ("kappa=5/3, G=1, rho=1, ds=1, rollers" if world == 1 else
+                                "soil (1800, 1000, 300) / rock (2500, 4000, 2000), ds=1 m, 4 bottom corners fixed"),
+                   "path": args.path,
                    "elements": E_total, "nodes": nodes_total,
                    "parallelism": "single GPU" if world == 1 else
                    (f"z-slabs x{world}, NCCL P2P interface exchange, {'overlapped' if Sharded.OVERLAP else 'serial'} schedule" if backend == "nccl" else
@@ -438,7 +543,7 @@ def main() -> None:
                         f"into a pinned host buffer (get_state)", "host_ms": e2e_host_ms},
     }
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_oracle_sample(args.path, steps=8)   # ~10 s of oracle work
+        out["cpu_baseline"] = cpu_oracle_sample(args.path)   # ~20-30 s of oracle work
     print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
