@@ -47,7 +47,7 @@ enum {
     OVX_EUNSTABLE = 3,  /* a non-finite displacement appeared (ovx_check_finite) */
     OVX_ESTATE = 6,     /* call-order violation (e.g. step before setup) */
     OVX_ECUDA = 7,      /* CUDA runtime error (message has the CUDA error string) */
-    OVX_ENCCL = 8,      /* reserved for the multi-GPU transport */
+    OVX_ENCCL = 8,      /* NCCL unavailable or an NCCL call failed (multi-GPU contexts) */
     OVX_ENOMEM = 9      /* device allocation failed */
 };
 
@@ -108,8 +108,16 @@ ovx_status ovx_set_damping(ovx_ctx *ctx, double alpha, double beta);
 ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages);
 /* Copy the library's derived K_e^INT8 (24x48 row-major) to host memory. */
 ovx_status ovx_get_int8_matrix(ovx_ctx *ctx, int8_t *out);
-/* Element-bound stability limit 2/sqrt(max_e λ_max(M_e⁻¹ K_e)) over the materials present. */
-ovx_status ovx_critical_dt(ovx_ctx *ctx, double *dt_elem_bound);
+/* Stability limits of the central-difference scheme (Eq. 3; reading Q19: dt ≤ 2/√λ_max(M⁻¹K)).
+ *   dt_elem_bound: 2/sqrt(max_e λ_max(M_e⁻¹ K_e)) over the materials present (host, exact element
+ *                  matrices; a safe bound, 20-35 % conservative).  Needs grid and materials.
+ *   dt_power_iter: 2/sqrt(λ) with λ the Rayleigh quotient xᵀKx/xᵀMx after 300 power iterations of
+ *                  M⁻¹K on the assembled model (the context's own EBE product on the device, fixed
+ *                  DOFs removed, deterministic start vector).  λ approaches λ_max
+ *                  from below, so this dt is the sharper but not a guaranteed bound.  Needs
+ *                  ovx_setup_elements and ovx_set_dt (M = dt²/w); single-GPU contexts only.
+ * Either pointer may be NULL (not computed); both NULL is OVX_EINVAL. */
+ovx_status ovx_critical_dt(ovx_ctx *ctx, double *dt_elem_bound, double *dt_power_iter);
 /* Point sources: component axis[k] of node[k] receives amp[k*n_t + it] at step it (0 after n_t).
  * n <= 16.  (impulse force at an input point.) */
 ovx_status ovx_set_sources(ovx_ctx *ctx, int n, const int64_t *node, const int32_t *axis,
@@ -200,6 +208,48 @@ ovx_status ovx_get_node_w(ovx_ctx *ctx, double *w);
 ovx_status ovx_get_timers(ovx_ctx *ctx, double *ms_step, int64_t *launches, int reset);
 /* Number of CTAs / threads / dynamic smem bytes of the step kernel for the current model. */
 ovx_status ovx_get_launch_config(ovx_ctx *ctx, int64_t *ctas, int *threads, int *smem_bytes);
+/* Per-phase device time since the last reset (synchronises):
+ *   ms_ebe    single GPU: the fused step kernels (EBE product, scatter and update are one kernel);
+ *             distributed: from each step's start to the end of its edge z-chunks;
+ *   ms_halo   distributed: from the edge z-chunks to the end of the interface exchanges and the
+ *             interface update (hidden under the interior chunks when it is shorter); 0 on one GPU;
+ *   ms_update 0: the update is fused into the EBE kernels (there is no separate update kernel). */
+ovx_status ovx_get_phase_timers(ovx_ctx *ctx, double *ms_ebe, double *ms_halo, double *ms_update, int reset);
+
+/* ---- multi-GPU: z-slabs (PAPER.md L288 names the multi-GPU extension as future work) --
+ * The element layers are split into contiguous z-slabs balanced to ±1 layer; rank r stores node
+ * planes ez0..ez1 (inclusive) and the rank ABOVE owns (updates) each interface plane.  A
+ * distributed context runs the whole step in the library: per step the edge z-chunks on a
+ * high-priority stream, the interior chunks concurrently on the context stream, the interface
+ * partial force exchanged with NCCL point-to-point (NVLink), the owner's interface update, the
+ * updated plane sent back — results identical bit for bit to one GPU.
+ * On a distributed context:
+ *   ovx_set_grid            takes the GLOBAL element counts; the rank's slab is derived from it;
+ *   ovx_set_element_materials  the rank's layers [ez0, ez1), preceded by layer ez0-1 when rank > 0
+ *                           (nx*ny*(ez1-ez0) entries, + nx*ny in front for rank > 0);
+ *   ovx_set_dirichlet, ovx_set_state / ovx_get_state: the rank's node planes ez0..ez1;
+ *   ovx_set_sources / ovx_set_receivers: GLOBAL node ids; a rank keeps the sources of the planes
+ *                           it owns, and records only the receivers of its owned planes (the other
+ *                           traces stay 0: sum the traces over the ranks);
+ *   ovx_step                the distributed schedule (NCCL contexts; loopback groups use
+ *                           ovx_step_group). */
+/* Element layers [*ez0, *ez1) of rank `rank` among `world` for nz global layers. */
+ovx_status ovx_get_partition(int64_t nz, int world, int rank, int64_t *ez0, int64_t *ez1);
+/* A new NCCL unique id (128 bytes) on the rank that creates the communicator; the caller
+ * broadcasts it to the other ranks (e.g. through torch.distributed).  OVX_ENCCL if libnccl.so.2
+ * cannot be loaded. */
+ovx_status ovx_nccl_unique_id(uint8_t out[128]);
+/* A context for rank `rank` of `world` on `device`, with a library-owned NCCL communicator
+ * (ncclCommInitRank: a collective call — every rank must call it).  world = 1 is a plain context. */
+ovx_status ovx_create_dist(int device, int rank, int world, const uint8_t id[128], ovx_ctx **out);
+/* `world` contexts (out[0..world-1], ranks in order, devices[r] each) that exchange interface
+ * data by device-to-device copies inside this process: the distributed schedule without NCCL
+ * (tests; several ranks may share one device, which NCCL refuses).  Step them with ovx_step_group;
+ * destroy each with ovx_destroy. */
+ovx_status ovx_create_group(int world, const int *devices, ovx_ctx **out);
+/* n steps of all ranks of a loopback group, phase by phase in lock step (the same kernels, streams
+ * and events as a distributed ovx_step, with copies in place of the NCCL calls). */
+ovx_status ovx_step_group(ovx_ctx **ranks, int world, int64_t n);
 
 #ifdef __cplusplus
 }

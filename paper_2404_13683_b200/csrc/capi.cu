@@ -2,6 +2,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <array>
+#include <dlfcn.h>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -33,7 +36,9 @@ struct ovx_ctx {
     double *d_un = nullptr;           // third state buffer of damped steps
     int8_t k8[1152];
     double Ak[576], Ag[576], Kk[576], Kg[576];
-    std::vector<MatConst> mc;
+    std::vector<MatConst> mc;         // host copy of the material table (kMaxMat entries)
+    MatConst *d_mc = nullptr;         // the context's own device copy (kernels read it via StepParams)
+    int kset = 0;                     // dense matrix set: 0 OVFEM, 1 VFEM
     int nsrc = 0;
     std::vector<int64_t> src_node;
     std::vector<int32_t> src_axis;
@@ -51,6 +56,15 @@ struct ovx_ctx {
     uint8_t *d_mat_below = nullptr;
     double *d_bot_b = nullptr;
     double *a_send = nullptr, *a_recv = nullptr, *u_send = nullptr, *u_recv = nullptr;
+    // library-driven z-slab rank (ovx_create_dist: NCCL; ovx_create_group: in-process loopback)
+    int rank = 0, world = 1;              // world > 1: a distributed context
+    void *nccl = nullptr;                 // ncclComm_t (NCCL ranks)
+    struct LoopGroup *group = nullptr;    // loopback group (all ranks in this process)
+    int64_t nz_global = 0, ez0 = 0, ez1 = 0;
+    double *d_iface = nullptr;            // library-owned a_send | a_recv | u_send | u_recv
+    cudaStream_t s_hi = nullptr;          // high-priority stream: edge chunks, exchange, interface update
+    std::vector<cudaEvent_t> ev_pool;     // per-step phase events
+    std::vector<std::array<cudaEvent_t, 4>> ph_used;   // (start, kernels done, halo done, end) per step
     int64_t nn2() const { return (nx + 1) * (ny + 1); }
     int64_t nn() const { return (nx + 1) * (ny + 1) * (nz + 1); }
     int64_t ne() const { return nx * ny * nz; }
@@ -59,7 +73,10 @@ struct ovx_ctx {
 namespace {
 
 std::string g_err;
-const ovx_ctx *g_const_owner[64] = {nullptr};
+ovx_status dist_step(ovx_ctx *ctx, int64_t n);
+void dist_release(ovx_ctx *ctx);
+std::mutex g_const_mu;
+bool g_const_done[64] = {false};
 
 ovx_status fail(ovx_ctx *c, ovx_status s, const std::string &m) {
     if (c) c->err = m;
@@ -79,19 +96,30 @@ void dfree(void *p) {
     if (p) cudaFree(p);
 }
 
-ovx_status ensure_constants(ovx_ctx *ctx) {
-    if (ctx->device >= 0 && ctx->device < 64 && g_const_owner[ctx->device] == ctx) return OVX_OK;
-    CK(upload_constants(ctx->mc.data(), ctx->nmat, ctx->k8, ctx->Kk, ctx->Kg, ctx->stream));
-    if (ctx->device >= 0 && ctx->device < 64) g_const_owner[ctx->device] = ctx;
+// The element matrices (the same for every context) on the context's device, uploaded once per device.
+ovx_status ensure_device_constants(ovx_ctx *ctx) {
+    const int dev = ctx->device;
+    if (dev < 0 || dev >= 64) return fail(ctx, OVX_EINVAL, "device index out of range");
+    std::lock_guard<std::mutex> lk(g_const_mu);
+    if (g_const_done[dev]) return OVX_OK;
+    int8_t k8[1152];
+    double Ak[576], Ag[576], kk2[2 * 576], kg2[2 * 576];
+    if (derive_element_matrices(k8, Ak, Ag) != 0) return fail(ctx, OVX_EINVAL, "K_e^INT8 derivation failed");
+    for (int r = 0; r < 24; ++r)
+        for (int c = 0; c < 24; ++c) {
+            kk2[r * 24 + c] = (double)k8[r * 48 + c];
+            kg2[r * 24 + c] = (double)k8[r * 48 + 24 + c] + (r == c ? 128.0 : 0.0);
+        }
+    if (derive_vfem_matrices(kk2 + 576, kg2 + 576) != 0) return fail(ctx, OVX_EINVAL, "VFEM derivation failed");
+    CK(upload_device_constants(k8, kk2, kg2));
+    g_const_done[dev] = true;
     return OVX_OK;
 }
 
 ovx_status refresh_w(ovx_ctx *ctx) {
     if (!ctx->setup || !(ctx->dt > 0)) return OVX_OK;
-    ovx_status s = ensure_constants(ctx);
-    if (s) return s;
     CK(launch_node_w(ctx->nx, ctx->ny, ctx->nz, ctx->d_mat, (ctx->slab_flags & 1) ? ctx->d_mat_below : nullptr,
-                     ctx->dt, ctx->d_w, ctx->stream));
+                     ctx->d_mc, ctx->dt, ctx->d_w, ctx->stream));
     return OVX_OK;
 }
 
@@ -115,6 +143,8 @@ StepParams base_params(ovx_ctx *ctx) {
     p.nx = ctx->nx;
     p.ny = ctx->ny;
     p.nz = ctx->nz;
+    p.mc = ctx->d_mc;
+    p.kset = ctx->kset;
     p.w = ctx->d_w;
     p.mat = ctx->d_mat;
     p.dmask = ctx->d_mask;
@@ -175,10 +205,13 @@ ovx_status ovx_destroy(ovx_ctx *ctx) {
     dfree(ctx->d_mat_below);
     dfree(ctx->d_bot_b);
     dfree(ctx->d_traces);
+    dfree(ctx->d_mc);
+    dfree(ctx->d_flag);
+    dfree(ctx->d_iface);
+    dist_release(ctx);
     for (auto &p : ctx->ev_used) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto &p : ctx->ev_free) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-    if (ctx->device >= 0 && ctx->device < 64 && g_const_owner[ctx->device] == ctx) g_const_owner[ctx->device] = nullptr;
     delete ctx;
     return OVX_OK;
 }
@@ -205,6 +238,13 @@ ovx_status ovx_set_grid(ovx_ctx *ctx, int64_t nx, int64_t ny, int64_t nz, double
     if (nx <= 0 || ny <= 0 || nz <= 0 || !(ds > 0) || !std::isfinite(ds))
         return fail(ctx, OVX_EINVAL, "grid dims must be >= 1 and ds > 0");
     if (nx > (1 << 24) || ny > (1 << 24) || nz > (1 << 24)) return fail(ctx, OVX_EINVAL, "grid too large");
+    int64_t ez0 = 0, ez1 = nz;
+    if (ctx->world > 1) {   // a z-slab rank: nz is the global element-layer count
+        if (nz < ctx->world) return fail(ctx, OVX_EINVAL, "fewer element layers than ranks");
+        ovx_get_partition(nz, ctx->world, ctx->rank, &ez0, &ez1);
+    }
+    const int64_t nz_global = nz;
+    nz = ez1 - ez0;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     dfree(ctx->d_mat);
@@ -229,6 +269,17 @@ ovx_status ovx_set_grid(ovx_ctx *ctx, int64_t nx, int64_t ny, int64_t nz, double
     ctx->ds = ds;
     ctx->have_grid = ctx->have_emat = ctx->setup = ctx->have_state = false;
     ctx->it = 0;
+    // a new grid is a new model: sources and receivers of the previous one do not carry over
+    ctx->nsrc = 0;
+    ctx->src_node.clear();
+    ctx->src_axis.clear();
+    ctx->n_t = 0;
+    ctx->amp.clear();
+    ctx->nrec = 0;
+    ctx->rec_node.clear();
+    ctx->rec_nt = 0;
+    dfree(ctx->d_traces);
+    ctx->d_traces = nullptr;
     const int64_t nn = ctx->nn(), ne = ctx->ne();
     if (cudaMalloc(&ctx->d_mat, ne) != cudaSuccess || cudaMalloc(&ctx->d_u, 24 * nn) != cudaSuccess ||
         cudaMalloc(&ctx->d_up, 24 * nn) != cudaSuccess || cudaMalloc(&ctx->d_w, 8 * nn) != cudaSuccess) {
@@ -237,6 +288,26 @@ ovx_status ovx_set_grid(ovx_ctx *ctx, int64_t nx, int64_t ny, int64_t nz, double
     }
     CK(cudaMemsetAsync(ctx->d_u, 0, 24 * nn, ctx->stream));
     CK(cudaMemsetAsync(ctx->d_up, 0, 24 * nn, ctx->stream));
+    ctx->nz_global = nz_global;
+    ctx->ez0 = ez0;
+    ctx->ez1 = ez1;
+    if (ctx->world > 1) {   // library-owned interface buffers and the slab flags of this rank
+        const int64_t n2 = 3 * ctx->nn2();
+        ctx->slab_flags = (ctx->rank > 0 ? 1 : 0) | (ctx->rank < ctx->world - 1 ? 2 : 0);
+        dfree(ctx->d_iface);
+        ctx->d_iface = nullptr;
+        if (cudaMalloc(&ctx->d_iface, 4 * 8 * n2) != cudaSuccess ||
+            ((ctx->slab_flags & 1) && (cudaMalloc(&ctx->d_mat_below, ctx->nx * ctx->ny) != cudaSuccess ||
+                                       cudaMalloc(&ctx->d_bot_b, 8 * n2) != cudaSuccess))) {
+            cudaGetLastError();
+            return fail(ctx, OVX_ENOMEM, "device allocation failed for the interface buffers");
+        }
+        CK(cudaMemsetAsync(ctx->d_iface, 0, 4 * 8 * n2, ctx->stream));
+        ctx->a_send = ctx->d_iface;
+        ctx->a_recv = ctx->d_iface + n2;
+        ctx->u_send = ctx->d_iface + 2 * n2;
+        ctx->u_recv = ctx->d_iface + 3 * n2;
+    }
     ctx->have_grid = true;
     return OVX_OK;
 }
@@ -260,11 +331,14 @@ ovx_status ovx_set_element_materials(ovx_ctx *ctx, const uint8_t *mat) {
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
     if (!ctx->have_grid || ctx->nmat == 0) return fail(ctx, OVX_ESTATE, "set grid and materials first");
     if (!mat) return fail(ctx, OVX_EINVAL, "mat is null");
+    // a distributed rank with a lower neighbour passes the element layer below its slab first
+    const int64_t halo = (ctx->world > 1 && (ctx->slab_flags & 1)) ? ctx->nx * ctx->ny : 0;
     const int64_t ne = ctx->ne();
-    for (int64_t e = 0; e < ne; ++e)
+    for (int64_t e = 0; e < ne + halo; ++e)
         if (mat[e] >= ctx->nmat) return fail(ctx, OVX_EINVAL, "unknown material id at element " + std::to_string(e));
     cudaSetDevice(ctx->device);
-    CK(cudaMemcpyAsync(ctx->d_mat, mat, ne, cudaMemcpyHostToDevice, ctx->stream));
+    if (halo) CK(cudaMemcpyAsync(ctx->d_mat_below, mat, halo, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_mat, mat + halo, ne, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->have_emat = true;
     if (ctx->setup) return refresh_w(ctx);
@@ -326,7 +400,8 @@ ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
                 ctx->Kg[r * 24 + c] = (double)ctx->k8[r * 48 + 24 + c] + (r == c ? 128.0 : 0.0);
             }
     }
-    ctx->mc.resize(ctx->nmat);
+    ctx->mc.assign(kMaxMat, MatConst{});   // entries >= nmat (and the zero material 255) are all zero
+    ctx->kset = (path == OVX_VFEM || path == OVX_VFEM_DENSE) ? 1 : 0;
     const double ds = ctx->ds;
     const double vol8 = ds * ds * ds / 8.0;
     for (int m = 0; m < ctx->nmat; ++m) {
@@ -354,11 +429,16 @@ ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
     }
     ctx->path = path;
     ctx->stages = stages;
-    ctx->setup = true;
     cudaSetDevice(ctx->device);
-    if (ctx->device >= 0 && ctx->device < 64 && g_const_owner[ctx->device] == ctx) g_const_owner[ctx->device] = nullptr;
-    ovx_status s = ensure_constants(ctx);
+    ovx_status s = ensure_device_constants(ctx);
     if (s) return s;
+    if (!ctx->d_mc && cudaMalloc(&ctx->d_mc, sizeof(MatConst) * kMaxMat) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, OVX_ENOMEM, "material table allocation failed");
+    }
+    // stream-ordered before every kernel of this context; no other context reads this table
+    CK(cudaMemcpyAsync(ctx->d_mc, ctx->mc.data(), sizeof(MatConst) * kMaxMat, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->setup = true;
     return refresh_w(ctx);
 }
 
@@ -370,18 +450,61 @@ ovx_status ovx_get_int8_matrix(ovx_ctx *ctx, int8_t *out) {  // ctx may be NULL 
     return OVX_OK;
 }
 
-ovx_status ovx_critical_dt(ovx_ctx *ctx, double *dt_elem_bound) {
-    if (!ctx || !dt_elem_bound) return fail(ctx, OVX_EINVAL, "null argument");
+ovx_status ovx_critical_dt(ovx_ctx *ctx, double *dt_elem_bound, double *dt_power_iter) {
+    if (!ctx || (!dt_elem_bound && !dt_power_iter)) return fail(ctx, OVX_EINVAL, "null argument");
     if (!ctx->have_grid || ctx->nmat == 0) return fail(ctx, OVX_ESTATE, "set grid and materials first");
-    double Ak[576], Ag[576], K[576];
-    if (derive_element_matrices(nullptr, Ak, Ag) != 0) return fail(ctx, OVX_EINVAL, "derivation failed");
-    double lmax = 0.0;
-    for (int m = 0; m < ctx->nmat; ++m) {
-        for (int i = 0; i < 576; ++i) K[i] = ctx->kappa[m] * ctx->ds * Ak[i] + ctx->G[m] * ctx->ds * Ag[i];
-        const double lam = sym_lambda_max(K) / (ctx->rho[m] * ctx->ds * ctx->ds * ctx->ds / 8.0);
-        if (lam > lmax) lmax = lam;
+    if (dt_elem_bound) {
+        double Ak[576], Ag[576], K[576];
+        if (derive_element_matrices(nullptr, Ak, Ag) != 0) return fail(ctx, OVX_EINVAL, "derivation failed");
+        double lmax = 0.0;
+        for (int m = 0; m < ctx->nmat; ++m) {
+            for (int i = 0; i < 576; ++i) K[i] = ctx->kappa[m] * ctx->ds * Ak[i] + ctx->G[m] * ctx->ds * Ag[i];
+            const double lam = sym_lambda_max(K) / (ctx->rho[m] * ctx->ds * ctx->ds * ctx->ds / 8.0);
+            if (lam > lmax) lmax = lam;
+        }
+        *dt_elem_bound = 2.0 / std::sqrt(lmax);
     }
-    *dt_elem_bound = 2.0 / std::sqrt(lmax);
+    if (dt_power_iter) {   // λ_max(M⁻¹K) of the assembled model by power iteration with the EBE product
+        ovx_status s = need_ready(ctx);
+        if (s) return s;
+        if (!(ctx->dt > 0)) return fail(ctx, OVX_ESTATE, "the power iteration needs dt (for M = dt²/w)");
+        if (ctx->world > 1 || ctx->slab_flags) return fail(ctx, OVX_EINVAL, "power iteration: single-GPU contexts only");
+        cudaSetDevice(ctx->device);
+        const int64_t nn = ctx->nn(), n3 = 3 * nn;
+        double *blk = nullptr;
+        if (cudaMalloc(&blk, 8 * (3 * n3 + 4)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, OVX_ENOMEM, "power-iteration scratch allocation failed");
+        }
+        double *x = blk, *y = blk + n3, *z = blk + 2 * n3, *acc = blk + 3 * n3;
+        std::vector<double> hx(n3);
+        uint64_t st = 0x9E3779B97F4A7C15ull;   // deterministic start vector (splitmix64 in [-1, 1))
+        for (int64_t i = 0; i < n3; ++i) {
+            uint64_t q = (st += 0x9E3779B97F4A7C15ull);
+            q = (q ^ (q >> 30)) * 0xBF58476D1CE4E5B9ull;
+            q = (q ^ (q >> 27)) * 0x94D049BB133111EBull;
+            q ^= q >> 31;
+            hx[i] = (double)(q >> 11) * 0x1p-52 - 1.0;
+        }
+        double lam = 0.0, h[3] = {0, 0, 0};
+        cudaError_t e = cudaMemcpyAsync(x, hx.data(), 8 * n3, cudaMemcpyHostToDevice, ctx->stream);
+        const double dt2 = ctx->dt * ctx->dt;
+        for (int k = 0; k < 300 && e == cudaSuccess; ++k) {
+            StepParams p = base_params(ctx);
+            p.u = x;
+            p.fout = y;
+            if ((e = cudaMemsetAsync(acc, 0, 24, ctx->stream))) break;
+            if ((e = launch_step(ctx->path, MODE_APPLY, p, ctx->stream))) break;
+            if ((e = launch_power_iter(nn, x, y, ctx->d_w, ctx->d_mask, dt2, z, acc, x, ctx->stream))) break;
+            if ((e = cudaMemcpyAsync(h, acc, 24, cudaMemcpyDeviceToHost, ctx->stream))) break;
+            if ((e = cudaStreamSynchronize(ctx->stream))) break;
+            lam = h[0] / h[1];   // Rayleigh quotient xᵀKx / xᵀMx (from below)
+        }
+        cudaFree(blk);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "power iteration");
+        if (!(lam > 0)) return fail(ctx, OVX_EUNSTABLE, "power iteration did not produce a positive eigenvalue");
+        *dt_power_iter = 2.0 / std::sqrt(lam);
+    }
     return OVX_OK;
 }
 
@@ -391,15 +514,27 @@ ovx_status ovx_set_sources(ovx_ctx *ctx, int n, const int64_t *node, const int32
     if (!ctx->have_grid) return fail(ctx, OVX_ESTATE, "set grid first");
     if (n < 0 || n > kMaxSrc || n_t < 0) return fail(ctx, OVX_EINVAL, "0..16 sources");
     if (n > 0 && (!node || !axis || (n_t > 0 && !amp))) return fail(ctx, OVX_EINVAL, "null source arrays");
+    const int64_t nn_all = ctx->world > 1 ? ctx->nn2() * (ctx->nz_global + 1) : ctx->nn();
     for (int k = 0; k < n; ++k)
-        if (node[k] < 0 || node[k] >= ctx->nn() || axis[k] < 0 || axis[k] > 2)
+        if (node[k] < 0 || node[k] >= nn_all || axis[k] < 0 || axis[k] > 2)
             return fail(ctx, OVX_EINVAL, "source node/axis out of range");
     if (n > 0 && n_t > 0 && !finite_all(amp, (int64_t)n * n_t)) return fail(ctx, OVX_EINVAL, "non-finite amplitude");
-    ctx->nsrc = n;
-    ctx->src_node.assign(node, node + n);
-    ctx->src_axis.assign(axis, axis + n);
+    ctx->src_node.clear();
+    ctx->src_axis.clear();
+    ctx->amp.clear();
+    for (int k = 0; k < n; ++k) {   // distributed: global node ids; keep the sources of owned planes
+        int64_t nd = node[k];
+        if (ctx->world > 1) {
+            const int64_t pz = nd / ctx->nn2(), p1 = (ctx->slab_flags & 2) ? ctx->ez1 : ctx->ez1 + 1;
+            if (pz < ctx->ez0 || pz >= p1) continue;
+            nd -= ctx->ez0 * ctx->nn2();
+        }
+        ctx->src_node.push_back(nd);
+        ctx->src_axis.push_back(axis[k]);
+        ctx->amp.insert(ctx->amp.end(), amp + (size_t)k * (size_t)n_t, amp + (size_t)(k + 1) * (size_t)n_t);
+    }
+    ctx->nsrc = (int)ctx->src_node.size();
     ctx->n_t = n_t;
-    ctx->amp.assign(amp, amp + (size_t)n * (size_t)n_t);
     return OVX_OK;
 }
 
@@ -407,6 +542,7 @@ static ovx_status set_state_impl(ovx_ctx *ctx, const double *u, const double *up
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
     if (!ctx->have_grid) return fail(ctx, OVX_ESTATE, "set grid first");
     if (!u || !up) return fail(ctx, OVX_EINVAL, "null state arrays");
+    if (it < 0) return fail(ctx, OVX_EINVAL, "the step index it must be >= 0");
     const int64_t n3 = 3 * ctx->nn();
     cudaSetDevice(ctx->device);
     CK(cudaMemcpyAsync(ctx->d_u, u, 8 * n3, kind, ctx->stream));
@@ -459,11 +595,13 @@ ovx_status ovx_step(ovx_ctx *ctx, int64_t n) {
     if (s) return s;
     if (!(ctx->dt > 0)) return fail(ctx, OVX_ESTATE, "set dt first");
     if (n < 0) return fail(ctx, OVX_EINVAL, "n must be >= 0");
+    if (ctx->world > 1) {
+        if (ctx->group) return fail(ctx, OVX_ESTATE, "loopback-group ranks step together with ovx_step_group");
+        return dist_step(ctx, n);
+    }
     if (ctx->slab_flags) return fail(ctx, OVX_ESTATE, "slab contexts step with ovx_step_begin/iface/end");
     if (n == 0) return OVX_OK;
     cudaSetDevice(ctx->device);
-    s = ensure_constants(ctx);
-    if (s) return s;
     EventPair ev;
     if (!ctx->ev_free.empty()) {
         ev = ctx->ev_free.back();
@@ -487,7 +625,7 @@ ovx_status ovx_step(ovx_ctx *ctx, int64_t n) {
         p.nsrc = ctx->nsrc;
         for (int q = 0; q < ctx->nsrc; ++q) {
             p.src_dof[q] = 3 * ctx->src_node[q] + ctx->src_axis[q];
-            p.src_val[q] = (ctx->it < ctx->n_t) ? ctx->amp[(size_t)q * ctx->n_t + ctx->it] : 0.0;
+            p.src_val[q] = (ctx->it >= 0 && ctx->it < ctx->n_t) ? ctx->amp[(size_t)q * ctx->n_t + ctx->it] : 0.0;
         }
         fill_receivers(ctx, p);
         CK(launch_step(ctx->path, MODE_STEP, p, ctx->stream));
@@ -568,7 +706,7 @@ static StepParams step_params(ovx_ctx *ctx) {
     p.nsrc = ctx->nsrc;
     for (int q = 0; q < ctx->nsrc; ++q) {
         p.src_dof[q] = 3 * ctx->src_node[q] + ctx->src_axis[q];
-        p.src_val[q] = (ctx->it < ctx->n_t) ? ctx->amp[(size_t)q * ctx->n_t + ctx->it] : 0.0;
+        p.src_val[q] = (ctx->it >= 0 && ctx->it < ctx->n_t) ? ctx->amp[(size_t)q * ctx->n_t + ctx->it] : 0.0;
     }
     p.slab_flags = ctx->slab_flags;
     p.iface_top_A = ctx->a_send;
@@ -590,8 +728,6 @@ static ovx_status step_begin_impl(ovx_ctx *ctx, int part) {
     if (((ctx->slab_flags & 2) && !ctx->a_send) || ((ctx->slab_flags & 1) && !ctx->d_bot_b))
         return fail(ctx, OVX_ESTATE, "interface buffers not set");
     cudaSetDevice(ctx->device);
-    s = ensure_constants(ctx);
-    if (s) return s;
     int nl = 0;
     CK(launch_step(ctx->path, MODE_STEP, step_params(ctx), ctx->stream, part, &nl));
     ctx->launches += nl;
@@ -647,13 +783,19 @@ ovx_status ovx_set_receivers(ovx_ctx *ctx, int n, const int64_t *node, int64_t n
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
     if (!ctx->have_grid) return fail(ctx, OVX_ESTATE, "set grid first");
     if (n < 0 || n > kMaxRec || n_t < 0 || (n > 0 && !node)) return fail(ctx, OVX_EINVAL, "0..32 receivers");
+    const int64_t nn_all = ctx->world > 1 ? ctx->nn2() * (ctx->nz_global + 1) : ctx->nn();
     for (int k = 0; k < n; ++k)
-        if (node[k] < 0 || node[k] >= ctx->nn()) return fail(ctx, OVX_EINVAL, "receiver node out of range");
+        if (node[k] < 0 || node[k] >= nn_all) return fail(ctx, OVX_EINVAL, "receiver node out of range");
     cudaSetDevice(ctx->device);
     dfree(ctx->d_traces);
     ctx->d_traces = nullptr;
     ctx->nrec = n;
     ctx->rec_node.assign(node, node + n);
+    if (ctx->world > 1)   // distributed: global ids; receivers of other ranks' planes record nothing (-1)
+        for (int k = 0; k < n; ++k) {
+            const int64_t pz = node[k] / ctx->nn2(), p1 = (ctx->slab_flags & 2) ? ctx->ez1 : ctx->ez1 + 1;
+            ctx->rec_node[k] = (pz >= ctx->ez0 && pz < p1) ? node[k] - ctx->ez0 * ctx->nn2() : -1;
+        }
     ctx->rec_nt = n_t;
     if (n > 0 && n_t > 0) {
         if (cudaMalloc(&ctx->d_traces, 8 * 3 * (size_t)n * (size_t)n_t) != cudaSuccess) {
@@ -698,8 +840,7 @@ ovx_status ovx_check_finite(ovx_ctx *ctx) {
 }
 
 static ovx_status apply_impl(ovx_ctx *ctx, const double *u_dev, double *f_dev) {
-    ovx_status s = ensure_constants(ctx);
-    if (s) return s;
+    ovx_status s = OVX_OK;
     StepParams p = base_params(ctx);
     p.u = u_dev;
     p.fout = f_dev;
@@ -750,8 +891,6 @@ ovx_status ovx_debug_element_ints(ovx_ctx *ctx, const double *u, int64_t e0, int
     if (ne == 0) return OVX_OK;
     const int64_t n3 = 3 * ctx->nn();
     cudaSetDevice(ctx->device);
-    s = ensure_constants(ctx);
-    if (s) return s;
     // one device block for everything
     const size_t bs = 8 * ne, bv = 8 * ne * 48, bd = ne * 384, bC = 4 * ne * 192, by = 8 * ne * 24, bf = 8 * ne * 24;
     const size_t bu = 8 * n3, total = bu * 2 + bs + bv + bd + bC + 2 * by + bf + 16 * 256;
@@ -828,6 +967,344 @@ ovx_status ovx_get_launch_config(ovx_ctx *ctx, int64_t *ctas, int *threads, int 
     if (ctas) *ctas = li.ctas;
     if (threads) *threads = li.threads;
     if (smem_bytes) *smem_bytes = li.smem;
+    return OVX_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================================
+// z-slab decomposition driven by the library (SURVEY §8(b) "distributed create", §8(e); PAPER.md
+// L288 names the multi-GPU extension as future work).  Per step (the overlapped schedule):
+//   s_hi (high priority) waits for the previous step; the edge z-chunks (first and last: they
+//   produce the top interface's partial force T and plane 0's bottom-face sum B) on s_hi, the
+//   interior chunks concurrently on the context stream; on s_hi: T → rank above (NCCL P2P),
+//   interface update of plane 0 by its owner (the rank above: f = T + B, reading U2), the updated
+//   plane → rank below; the context stream waits for s_hi and installs the received top plane.
+// NCCL is loaded at run time (dlopen of libnccl.so.2; the one torch already loaded if any).
+// ============================================================================================
+namespace {
+
+namespace nccl {
+struct UniqueId {
+    char internal[128];
+};
+typedef void *Comm;
+typedef int Result;
+constexpr int kFloat64 = 8;   // ncclFloat64
+struct Api {
+    Result (*GetUniqueId)(UniqueId *) = nullptr;
+    Result (*CommInitRank)(Comm *, int, UniqueId, int) = nullptr;
+    Result (*CommDestroy)(Comm) = nullptr;
+    Result (*Send)(const void *, size_t, int, int, Comm, cudaStream_t) = nullptr;
+    Result (*Recv)(void *, size_t, int, int, Comm, cudaStream_t) = nullptr;
+    Result (*GroupStart)() = nullptr;
+    Result (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(Result) = nullptr;
+    std::string err;
+    bool ok() const { return GetUniqueId && CommInitRank && Send && Recv && GroupStart && GroupEnd; }
+};
+const Api &api() {
+    static Api a = [] {
+        Api x;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);   // already in the process (torch)
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            x.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return x;
+        }
+        x.GetUniqueId = (Result(*)(UniqueId *))dlsym(h, "ncclGetUniqueId");
+        x.CommInitRank = (Result(*)(Comm *, int, UniqueId, int))dlsym(h, "ncclCommInitRank");
+        x.CommDestroy = (Result(*)(Comm))dlsym(h, "ncclCommDestroy");
+        x.Send = (Result(*)(const void *, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclSend");
+        x.Recv = (Result(*)(void *, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclRecv");
+        x.GroupStart = (Result(*)())dlsym(h, "ncclGroupStart");
+        x.GroupEnd = (Result(*)())dlsym(h, "ncclGroupEnd");
+        x.GetErrorString = (const char *(*)(Result))dlsym(h, "ncclGetErrorString");
+        if (!x.ok()) x.err = "libnccl.so.2 lacks a needed symbol";
+        return x;
+    }();
+    return a;
+}
+}  // namespace nccl
+
+#define NK(call)                                                                                        \
+    do {                                                                                                \
+        nccl::Result r_ = (call);                                                                       \
+        if (r_ != 0)                                                                                    \
+            return fail(ctx, OVX_ENCCL, std::string(#call) + ": " +                                    \
+                                            (nccl::api().GetErrorString ? nccl::api().GetErrorString(r_) : "?")); \
+    } while (0)
+
+}  // namespace
+
+// All ranks of a decomposition in this process on one or more devices (tests: the schedule above
+// with device-to-device copies in place of NCCL, stepped in lock step by ovx_step_group).
+struct LoopGroup {
+    std::vector<ovx_ctx *> ranks;
+};
+
+namespace {
+
+cudaEvent_t ev_take(ovx_ctx *ctx) {
+    if (!ctx->ev_pool.empty()) {
+        cudaEvent_t e = ctx->ev_pool.back();
+        ctx->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ovx_status dist_prepare(ovx_ctx *ctx) {
+    ovx_status s = need_ready(ctx);
+    if (s) return s;
+    if (!(ctx->dt > 0)) return fail(ctx, OVX_ESTATE, "set dt first");
+    cudaSetDevice(ctx->device);
+    if (!ctx->s_hi) {
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&ctx->s_hi, cudaStreamNonBlocking, hi));
+    }
+    return OVX_OK;
+}
+
+// phase 1: s_hi after the previous step; edge chunks on s_hi, interior on the context stream
+ovx_status dist_phase_compute(ovx_ctx *ctx, std::array<cudaEvent_t, 4> &ev) {
+    for (auto &e : ev) e = ev_take(ctx);
+    CK(cudaEventRecord(ev[0], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->s_hi, ev[0], 0));
+    const StepParams p = step_params(ctx);
+    int n0 = 0, n1 = 0;
+    CK(launch_step(ctx->path, MODE_STEP, p, ctx->s_hi, 0, &n0));
+    CK(launch_step(ctx->path, MODE_STEP, p, ctx->stream, 1, &n1));
+    CK(cudaEventRecord(ev[1], ctx->s_hi));
+    ctx->launches += n0 + n1;
+    return OVX_OK;
+}
+// interface update of plane 0 (owner = this rank, when it has a lower neighbour)
+ovx_status dist_phase_iface(ovx_ctx *ctx) {
+    if (!(ctx->slab_flags & 1)) return OVX_OK;
+    CK(launch_iface_update(step_params(ctx), ctx->a_recv, ctx->u_send, ctx->s_hi));
+    ctx->launches += 1;
+    return OVX_OK;
+}
+// the context stream waits for s_hi; installs the top plane; swap
+ovx_status dist_phase_end(ovx_ctx *ctx, std::array<cudaEvent_t, 4> &ev) {
+    CK(cudaEventRecord(ev[2], ctx->s_hi));
+    CK(cudaStreamWaitEvent(ctx->stream, ev[2], 0));
+    ovx_status s = ovx_step_end(ctx);
+    if (s) return s;
+    CK(cudaEventRecord(ev[3], ctx->stream));
+    ctx->ph_used.push_back(ev);
+    return OVX_OK;
+}
+
+ovx_status dist_step(ovx_ctx *ctx, int64_t n) {
+    ovx_status s = dist_prepare(ctx);
+    if (s) return s;
+    const nccl::Api &A = nccl::api();
+    if (!ctx->nccl || !A.ok()) return fail(ctx, OVX_ENCCL, "no NCCL communicator (" + A.err + ")");
+    const size_t cnt = (size_t)(3 * ctx->nn2());
+    nccl::Comm comm = (nccl::Comm)ctx->nccl;
+    const bool up = ctx->rank < ctx->world - 1, down = ctx->rank > 0;
+    for (int64_t k = 0; k < n; ++k) {
+        std::array<cudaEvent_t, 4> ev;
+        if ((s = dist_phase_compute(ctx, ev))) return s;
+        NK(A.GroupStart());   // T: the top interface's partial force to the owner above
+        if (up) NK(A.Send(ctx->a_send, cnt, nccl::kFloat64, ctx->rank + 1, comm, ctx->s_hi));
+        if (down) NK(A.Recv(ctx->a_recv, cnt, nccl::kFloat64, ctx->rank - 1, comm, ctx->s_hi));
+        NK(A.GroupEnd());
+        if ((s = dist_phase_iface(ctx))) return s;
+        NK(A.GroupStart());   // the updated interface plane back to the rank below
+        if (down) NK(A.Send(ctx->u_send, cnt, nccl::kFloat64, ctx->rank - 1, comm, ctx->s_hi));
+        if (up) NK(A.Recv(ctx->u_recv, cnt, nccl::kFloat64, ctx->rank + 1, comm, ctx->s_hi));
+        NK(A.GroupEnd());
+        if ((s = dist_phase_end(ctx, ev))) return s;
+    }
+    return OVX_OK;
+}
+
+void dist_release(ovx_ctx *ctx) {
+    for (auto &ev : ctx->ph_used)
+        for (auto e : ev) ctx->ev_pool.push_back(e);
+    ctx->ph_used.clear();
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    ctx->ev_pool.clear();
+    if (ctx->s_hi) cudaStreamDestroy(ctx->s_hi);
+    ctx->s_hi = nullptr;
+    if (ctx->nccl && nccl::api().CommDestroy) nccl::api().CommDestroy((nccl::Comm)ctx->nccl);
+    ctx->nccl = nullptr;
+    if (ctx->group) {
+        auto &v = ctx->group->ranks;
+        for (auto &r : v)
+            if (r == ctx) r = nullptr;
+        bool empty = true;
+        for (auto r : v) empty &= (r == nullptr);
+        if (empty) delete ctx->group;
+        ctx->group = nullptr;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+ovx_status ovx_get_partition(int64_t nz, int world, int rank, int64_t *ez0, int64_t *ez1) {
+    if (!ez0 || !ez1 || nz < 1 || world < 1 || rank < 0 || rank >= world)
+        return fail(nullptr, OVX_EINVAL, "partition: need nz >= 1, 0 <= rank < world");
+    const int64_t base = nz / world, rem = nz % world;
+    *ez0 = rank * base + std::min<int64_t>(rank, rem);
+    *ez1 = *ez0 + base + (rank < rem ? 1 : 0);
+    return OVX_OK;
+}
+
+ovx_status ovx_nccl_unique_id(uint8_t out[128]) {
+    if (!out) return fail(nullptr, OVX_EINVAL, "null argument");
+    const nccl::Api &A = nccl::api();
+    if (!A.ok()) return fail(nullptr, OVX_ENCCL, A.err);
+    nccl::UniqueId id;
+    ovx_ctx *ctx = nullptr;
+    NK(A.GetUniqueId(&id));
+    std::memcpy(out, id.internal, 128);
+    return OVX_OK;
+}
+
+ovx_status ovx_create_dist(int device, int rank, int world, const uint8_t id[128], ovx_ctx **out) {
+    if (!out || !id || world < 1 || rank < 0 || rank >= world) return fail(nullptr, OVX_EINVAL, "bad rank / world / id");
+    ovx_status s = ovx_create(device, out);
+    if (s) return s;
+    ovx_ctx *ctx = *out;
+    ctx->rank = rank;
+    ctx->world = world;
+    if (world == 1) return OVX_OK;
+    const nccl::Api &A = nccl::api();
+    if (!A.ok()) {
+        ovx_destroy(ctx);
+        *out = nullptr;
+        return fail(nullptr, OVX_ENCCL, A.err);
+    }
+    nccl::UniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    nccl::Comm comm = nullptr;
+    cudaSetDevice(device);
+    const nccl::Result r = A.CommInitRank(&comm, world, uid, rank);   // collective over the ranks
+    if (r != 0) {
+        ovx_destroy(ctx);
+        *out = nullptr;
+        return fail(nullptr, OVX_ENCCL, std::string("ncclCommInitRank: ") + (A.GetErrorString ? A.GetErrorString(r) : "?"));
+    }
+    ctx->nccl = comm;
+    return OVX_OK;
+}
+
+ovx_status ovx_create_group(int world, const int *devices, ovx_ctx **out) {
+    if (!out || !devices || world < 1) return fail(nullptr, OVX_EINVAL, "bad group arguments");
+    LoopGroup *g = new LoopGroup();
+    for (int r = 0; r < world; ++r) {
+        ovx_ctx *c = nullptr;
+        ovx_status s = ovx_create(devices[r], &c);
+        if (s) {
+            for (int q = 0; q < r; ++q) ovx_destroy(out[q]);
+            return s;
+        }
+        c->rank = r;
+        c->world = world;
+        c->group = world > 1 ? g : nullptr;
+        g->ranks.push_back(c);
+        out[r] = c;
+    }
+    if (world == 1) delete g;
+    return OVX_OK;
+}
+
+ovx_status ovx_step_group(ovx_ctx **ranks, int world, int64_t n) {
+    if (!ranks || world < 1) return fail(nullptr, OVX_EINVAL, "bad group arguments");
+    if (world == 1) return ovx_step(ranks[0], n);
+    for (int r = 0; r < world; ++r) {
+        ovx_ctx *ctx = ranks[r];
+        if (!ctx || ctx->group == nullptr || ctx->group != ranks[0]->group || ctx->rank != r || ctx->world != world)
+            return fail(ctx, OVX_EINVAL, "not the ranks of one loopback group, in rank order");
+        ovx_status s = dist_prepare(ctx);
+        if (s) return s;
+    }
+    std::vector<std::array<cudaEvent_t, 4>> ev(world);
+    for (int64_t k = 0; k < n; ++k) {
+        for (int r = 0; r < world; ++r) {
+            ovx_ctx *ctx = ranks[r];
+            cudaSetDevice(ctx->device);
+            ovx_status s = dist_phase_compute(ctx, ev[r]);
+            if (s) return s;
+        }
+        // T: a_send(r) -> a_recv(r+1), on the receiver's s_hi after the sender's edge chunks
+        for (int r = 0; r + 1 < world; ++r) {
+            ovx_ctx *ctx = ranks[r + 1];
+            cudaSetDevice(ctx->device);
+            CK(cudaStreamWaitEvent(ctx->s_hi, ev[r][1], 0));
+            CK(cudaMemcpyPeerAsync(ctx->a_recv, ctx->device, ranks[r]->a_send, ranks[r]->device,
+                                   8 * 3 * ctx->nn2(), ctx->s_hi));
+        }
+        for (int r = 0; r < world; ++r) {
+            ovx_ctx *ctx = ranks[r];
+            cudaSetDevice(ctx->device);
+            ovx_status s = dist_phase_iface(ctx);
+            if (s) return s;
+            CK(cudaEventRecord(ev[r][2], ctx->s_hi));   // (re-recorded by the end phase)
+        }
+        // the updated plane: u_send(r) -> u_recv(r-1), on the receiver's s_hi after the owner's update
+        for (int r = 1; r < world; ++r) {
+            ovx_ctx *ctx = ranks[r - 1];
+            cudaSetDevice(ctx->device);
+            CK(cudaStreamWaitEvent(ctx->s_hi, ev[r][2], 0));
+            CK(cudaMemcpyPeerAsync(ctx->u_recv, ctx->device, ranks[r]->u_send, ranks[r]->device,
+                                   8 * 3 * ctx->nn2(), ctx->s_hi));
+        }
+        // the senders' next edge chunks must not overwrite a_send / u_send before the copies: every
+        // s_hi waits for its neighbours' s_hi at the end of the step (through the context streams)
+        for (int r = 0; r < world; ++r) {
+            ovx_ctx *ctx = ranks[r];
+            cudaSetDevice(ctx->device);
+            ovx_status s = dist_phase_end(ctx, ev[r]);
+            if (s) return s;
+        }
+        for (int r = 0; r < world; ++r) {
+            ovx_ctx *ctx = ranks[r];
+            cudaSetDevice(ctx->device);
+            if (r > 0) CK(cudaStreamWaitEvent(ctx->stream, ranks[r - 1]->ph_used.back()[2], 0));
+            if (r + 1 < world) CK(cudaStreamWaitEvent(ctx->stream, ranks[r + 1]->ph_used.back()[2], 0));
+        }
+    }
+    return OVX_OK;
+}
+
+ovx_status ovx_get_phase_timers(ovx_ctx *ctx, double *ms_ebe, double *ms_halo, double *ms_update, int reset) {
+    if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
+    cudaSetDevice(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+    double a = 0.0, b = 0.0;
+    if (ctx->world > 1) {
+        for (auto &ev : ctx->ph_used) {
+            float t01 = 0.f, t12 = 0.f;
+            CK(cudaEventElapsedTime(&t01, ev[0], ev[1]));   // step start -> edge chunks done
+            CK(cudaEventElapsedTime(&t12, ev[1], ev[2]));   // edge chunks done -> exchanges + interface done
+            a += t01;
+            b += t12;
+        }
+    } else {
+        for (auto &p : ctx->ev_used) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p.a, p.b));
+            a += ms;
+        }
+    }
+    if (ms_ebe) *ms_ebe = a;
+    if (ms_halo) *ms_halo = b;
+    if (ms_update) *ms_update = 0.0;   // the update is fused into the EBE kernels
+    if (reset) {
+        for (auto &ev : ctx->ph_used)
+            for (auto e : ev) ctx->ev_pool.push_back(e);
+        ctx->ph_used.clear();
+    }
     return OVX_OK;
 }
 

@@ -29,9 +29,10 @@
 
 namespace ovx {
 
-__constant__ MatConst c_mat[kMaxMat];
-__constant__ double c_Kk[576];
-__constant__ double c_Kg[576];
+// Element matrices, identical for every context (upload_device_constants, once per device): the
+// dense integer matrices [0] OVFEM K^κ, K̄^G + 128 I and [1] VFEM Vk, Vg (step_v1), and K_e^INT8.
+__constant__ double c_Kk[2][576];
+__constant__ double c_Kg[2][576];
 __constant__ int8_t c_K8[1152];
 
 namespace {
@@ -224,31 +225,76 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 #include "step_f64.cuh"
 
 #include "step_i8w.cuh"
+#include "step_i8x.cuh"
+
+// cudaFuncSetAttribute state is per device: remember it per device index
+inline bool attr_done(unsigned &mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return (mask >> (dev & 31)) & 1u;
+}
+inline void attr_set(unsigned &mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    mask |= 1u << (dev & 31);
+}
 
 template <int MODE, int M, bool DAMP, class G, bool TA>
 cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
-    static bool attr = false;
+    static unsigned attr = 0;
     const int smem = (int)sizeof(SmemI8<G, TA>);
-    if (!attr) {
+    if (!attr_done(attr)) {
         cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         // all of the unified L1/shared array as shared memory, so G::CPS CTAs fit one SM
         e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G, TA>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr_set(attr);
     }
     step_i8w<MODE, M, DAMP, G, TA><<<(unsigned)ctas, G::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-// INT8 kernel variant (OVX_I8_KERNEL): "tmem" (default) the A operand in TMEM (the MMAs read only B
-// from shared memory); "smem" A in shared memory.  DESIGN.md §6.1 has the measurements.
+// INT8 kernel variant (OVX_I8_KERNEL): "x" (default) step_i8x, the round-2 schedule (time steps
+// and products; the debug records always come from step_i8w); "tmem" step_i8w with the A operand
+// in TMEM; "smem" step_i8w with A in shared memory.  DESIGN.md §6.1 has the measurements.
 int i8_variant() {
     static const int v = [] {
         const char *e = std::getenv("OVX_I8_KERNEL");
-        return (e && std::strcmp(e, "smem") == 0) ? 1 : 0;
+        if (e && std::strcmp(e, "smem") == 0) return 1;
+        if (e && std::strcmp(e, "tmem") == 0) return 0;
+        return 2;
     }();
     return v;
+}
+
+// step_i8x operand layout (OVX_I8X_LAYOUT): "word" (default, B = −K_D ⊗ I_4) or "half" (⊗ I_2)
+int i8x_layout() {
+    static const int v = [] {
+        const char *e = std::getenv("OVX_I8X_LAYOUT");
+        return (e && std::strcmp(e, "half") == 0) ? 0 : 1;
+    }();
+    return v;
+}
+
+template <int MODE, int M, bool DAMP, bool SLAB, int LAY>
+cudaError_t launch_i8x_l(const StepParams &p, int64_t ctas, cudaStream_t st) {
+    const int smem = (int)sizeof(SmemI8X);
+    static unsigned attr = 0;
+    if (!attr_done(attr)) {
+        cudaError_t e = cudaFuncSetAttribute(step_i8x<MODE, M, DAMP, SLAB, LAY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(step_i8x<MODE, M, DAMP, SLAB, LAY>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+        attr_set(attr);
+    }
+    step_i8x<MODE, M, DAMP, SLAB, LAY><<<(unsigned)ctas, 512, smem, st>>>(p);
+    return cudaGetLastError();
+}
+template <int MODE, int M, bool DAMP, bool SLAB>
+cudaError_t launch_i8x(const StepParams &p, int64_t ctas, cudaStream_t st) {
+    return i8x_layout() == 1 ? launch_i8x_l<MODE, M, DAMP, SLAB, 1>(p, ctas, st)
+                             : launch_i8x_l<MODE, M, DAMP, SLAB, 0>(p, ctas, st);
 }
 
 template <int M, class G, bool TA>
@@ -260,20 +306,31 @@ cudaError_t launch_i8_mode_g(int mode, const StepParams &p, int64_t ctas, cudaSt
     return launch_i8w<MODE_DEBUG, M, false, G, TA>(p, ctas, st);
 }
 
+template <int M, bool SLAB>
+cudaError_t launch_i8x_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
+    if (mode == MODE_STEP)
+        return p.damped ? launch_i8x<MODE_STEP, M, true, SLAB>(p, ctas, st)
+                        : launch_i8x<MODE_STEP, M, false, SLAB>(p, ctas, st);
+    return launch_i8x<MODE_APPLY, M, false, SLAB>(p, ctas, st);
+}
+
 template <int M>
 cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
-    return i8_variant() == 1 ? launch_i8_mode_g<M, I8W, false>(mode, p, ctas, st)
-                             : launch_i8_mode_g<M, I8W, true>(mode, p, ctas, st);
+    const int v = i8_variant();
+    if (v == 2 && mode != MODE_DEBUG)
+        return p.slab_flags ? launch_i8x_mode<M, true>(mode, p, ctas, st) : launch_i8x_mode<M, false>(mode, p, ctas, st);
+    return v == 1 ? launch_i8_mode_g<M, I8W, false>(mode, p, ctas, st)
+                  : launch_i8_mode_g<M, I8W, true>(mode, p, ctas, st);
 }
 
 template <int PATH, int MODE, bool DAMP = false>
 cudaError_t launch_t(const StepParams &p, int64_t ctas, cudaStream_t st) {
-    static bool attr = false;
+    static unsigned attr = 0;
     const int smem = (int)sizeof(SmemV1<PATH>);
-    if (!attr) {
+    if (!attr_done(attr)) {
         cudaError_t e = cudaFuncSetAttribute(step_v1<PATH, MODE, DAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr_set(attr);
     }
     step_v1<PATH, MODE, DAMP><<<(unsigned)ctas, V1<PATH>::NT, smem, st>>>(p);
     return cudaGetLastError();
@@ -281,12 +338,12 @@ cudaError_t launch_t(const StepParams &p, int64_t ctas, cudaStream_t st) {
 
 template <int MODE, bool DAMP, bool VF>
 cudaError_t launch_f64(const StepParams &p, int64_t ctas, cudaStream_t st) {
-    static bool attr = false;
+    static unsigned attr = 0;
     const int smem = (int)sizeof(SmemF2);
-    if (!attr) {
+    if (!attr_done(attr)) {
         cudaError_t e = cudaFuncSetAttribute(step_f64<MODE, DAMP, VF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr_set(attr);
     }
     step_f64<MODE, DAMP, VF><<<(unsigned)ctas, F2::NT, smem, st>>>(p);
     return cudaGetLastError();
@@ -307,7 +364,8 @@ cudaError_t launch_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_
 }
 
 __global__ void node_w_kernel(int64_t nx, int64_t ny, int64_t nz, const uint8_t *__restrict__ mat,
-                              const uint8_t *__restrict__ mat_below, double dt, double *__restrict__ w) {
+                              const uint8_t *__restrict__ mat_below, const MatConst *__restrict__ mc, double dt,
+                              double *__restrict__ w) {
     const int64_t NX1 = nx + 1, NY1 = ny + 1, nn = NX1 * NY1 * (nz + 1);
     for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn; n += (int64_t)gridDim.x * blockDim.x) {
         const int64_t ix = n % NX1, iy = (n / NX1) % NY1, iz = n / (NX1 * NY1);
@@ -319,10 +377,10 @@ __global__ void node_w_kernel(int64_t nx, int64_t ny, int64_t nz, const uint8_t 
                     const int64_t ex = ix + dx, ey = iy + dy, ez = iz + dz;
                     if (ex < 0 || ex >= nx || ey < 0 || ey >= ny || ez >= nz) continue;
                     if (ez < 0) {   // element layer below the slab (z-slab halo), if any
-                        if (mat_below) m = __dadd_rn(m, c_mat[mat_below[ex + nx * ey]].rho_vol8);
+                        if (mat_below) m = __dadd_rn(m, mc[mat_below[ex + nx * ey]].rho_vol8);
                         continue;
                     }
-                    m = __dadd_rn(m, c_mat[mat[ex + nx * (ey + ny * ez)]].rho_vol8);
+                    m = __dadd_rn(m, mc[mat[ex + nx * (ey + ny * ez)]].rho_vol8);
                 }
         w[n] = __ddiv_rn(__dmul_rn(dt, dt), m);
     }
@@ -380,20 +438,15 @@ LaunchInfo info_t(int64_t nx, int64_t ny, int64_t nz) {
 
 }  // namespace
 
-cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, const double *kk, const double *kg,
-                             cudaStream_t st) {
+cudaError_t upload_device_constants(const int8_t *k8, const double *kk2, const double *kg2) {
     cudaError_t e;
-    if ((e = cudaMemcpyToSymbolAsync(c_mat, mats, sizeof(MatConst) * nmat, 0, cudaMemcpyHostToDevice, st))) return e;
-    static const MatConst zero = {};   // reserved zero material: elements outside the domain
-    if ((e = cudaMemcpyToSymbolAsync(c_mat, &zero, sizeof(MatConst), sizeof(MatConst) * kZeroMat,
-                                     cudaMemcpyHostToDevice, st)))
-        return e;
-    if ((e = cudaMemcpyToSymbolAsync(c_K8, k8, 1152, 0, cudaMemcpyHostToDevice, st))) return e;
-    if ((e = cudaMemcpyToSymbolAsync(c_Kk, kk, 576 * 8, 0, cudaMemcpyHostToDevice, st))) return e;
-    if ((e = cudaMemcpyToSymbolAsync(c_Kg, kg, 576 * 8, 0, cudaMemcpyHostToDevice, st))) return e;
-    i8_bimg_kernel<<<1, 512, 0, st>>>();   // the INT8 kernel's B-operand image from c_K8
+    if ((e = cudaMemcpyToSymbol(c_K8, k8, 1152))) return e;
+    if ((e = cudaMemcpyToSymbol(c_Kk, kk2, 2 * 576 * 8))) return e;
+    if ((e = cudaMemcpyToSymbol(c_Kg, kg2, 2 * 576 * 8))) return e;
+    i8_bimg_kernel<<<1, 512>>>();    // the INT8 kernels' B-operand images from c_K8
+    i8x_bimg_kernel<<<1, 512>>>();
     if ((e = cudaGetLastError())) return e;
-    return cudaStreamSynchronize(st);
+    return cudaDeviceSynchronize();
 }
 
 LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
@@ -404,7 +457,8 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
         const int zc = choose_zchunk(nz + 1, tx * ty, cps);
         li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
         li.threads = I8W::NT;
-        li.smem = i8_variant() == 0 ? (int)sizeof(SmemI8<I8W, true>) : (int)sizeof(SmemI8<I8W, false>);
+        li.smem = i8_variant() == 2 ? (int)sizeof(SmemI8X)
+                  : i8_variant() == 0 ? (int)sizeof(SmemI8<I8W, true>) : (int)sizeof(SmemI8<I8W, false>);
         return li;
     }
     if (path == OVX_FP64) return info_t<OVX_FP64>(nx, ny, nz);
@@ -455,8 +509,8 @@ cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st, int p
 }
 
 cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, const uint8_t *mat_below,
-                          double dt, double *w, cudaStream_t st) {
-    node_w_kernel<<<1184, 256, 0, st>>>(nx, ny, nz, mat, mat_below, dt, w);
+                          const MatConst *mc, double dt, double *w, cudaStream_t st) {
+    node_w_kernel<<<1184, 256, 0, st>>>(nx, ny, nz, mat, mat_below, mc, dt, w);
     return cudaGetLastError();
 }
 
@@ -489,6 +543,49 @@ __global__ void iface_update_kernel(const StepParams p, const double *__restrict
 
 cudaError_t launch_iface_update(const StepParams &p, const double *a_recv, double *u_send, cudaStream_t st) {
     iface_update_kernel<<<296, 256, 0, st>>>(p, a_recv, u_send);
+    return cudaGetLastError();
+}
+
+// Power iteration on M⁻¹K (ovx_critical_dt's dt_power_iter): given y = K x, accumulate the
+// Rayleigh-quotient terms xᵀy, xᵀMx (M = dt²/w per node) and form z = M⁻¹y with fixed DOFs zeroed,
+// with ‖z‖² for the normalisation.  acc: [xᵀKx, xᵀMx, zᵀz], doubles, zeroed by the caller.
+__global__ void power_iter_kernel(int64_t nn, const double *__restrict__ x, const double *__restrict__ y,
+                                  const double *__restrict__ w, const uint8_t *__restrict__ dmask, double dt2,
+                                  double *__restrict__ z, double *__restrict__ acc) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn; n += (int64_t)gridDim.x * blockDim.x) {
+        const double minv = w[n] / dt2, m = dt2 / w[n];
+        const uint8_t dm = dmask ? dmask[n] : 0;
+        for (int k = 0; k < 3; ++k) {
+            const double xi = x[3 * n + k], yi = y[3 * n + k];
+            a += xi * yi;
+            b += xi * m * xi;
+            const double zi = ((dm >> k) & 1) ? 0.0 : minv * yi;
+            z[3 * n + k] = zi;
+            c += zi * zi;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+        c += __shfl_down_sync(0xffffffffu, c, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(acc, a);
+        atomicAdd(acc + 1, b);
+        atomicAdd(acc + 2, c);
+    }
+}
+__global__ void scale_kernel(int64_t n, const double *__restrict__ z, const double *__restrict__ acc,
+                             double *__restrict__ x) {
+    const double s = 1.0 / sqrt(acc[2]);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = z[i] * s;
+}
+cudaError_t launch_power_iter(int64_t nn, const double *x, const double *y, const double *w, const uint8_t *dmask,
+                              double dt2, double *z, double *acc, double *xnext, cudaStream_t st) {
+    power_iter_kernel<<<592, 256, 0, st>>>(nn, x, y, w, dmask, dt2, z, acc);
+    scale_kernel<<<592, 256, 0, st>>>(3 * nn, z, acc, xnext);
     return cudaGetLastError();
 }
 

@@ -25,6 +25,8 @@ enum Mode { MODE_STEP = 0, MODE_APPLY = 1, MODE_DEBUG = 2 };
 
 struct StepParams {
     int64_t nx, ny, nz;
+    const MatConst *mc;   // the context's material table (device, kMaxMat entries; kZeroMat = zeros)
+    int kset;             // dense matrices of step_v1: 0 OVFEM (K^κ, K̄^G + 128 I), 1 VFEM (Vk, Vg)
     const double *u;      // u^{it} (3 per node)
     double *uo;           // MODE_STEP: in u^{it-1}, out u^{it+1}
     const double *w;      // dt²/m per node
@@ -50,7 +52,7 @@ struct StepParams {
     double ca, cb;         // RN(alpha·dt), RN(beta/dt)
     double *un;
     int stages;            // INT8 path: M (4, 6 or 8)
-    int nmat;              // materials in c_mat[0, nmat) (ids < 255; 255 = zero material)
+    int nmat;              // materials in mc[0, nmat) (ids < 255; 255 = zero material)
     int slab_flags;
     double *iface_top_A;   // [NX1*NY1][3]   partial force of the top plane (bit 1)
     double *iface_bot_b;   // [NX1*NY1][3] the layer-0 bottom-face sum B of plane 0 (bit 0)
@@ -74,16 +76,21 @@ struct LaunchInfo {
 };
 
 // kernels.cu
-cudaError_t upload_constants(const MatConst *mats, int nmat, const int8_t *k8, const double *kk,
-                             const double *kg, cudaStream_t st);
+// The element matrices, which are the same for every context: K_e^INT8 (and the INT8 kernels' B-operand
+// images built from it) and the dense integer matrices of both elements (kk, kg: 2 × 576, OVFEM then
+// VFEM).  Uploaded once per device, synchronously; per-context data (materials) never goes to
+// __constant__ memory, so contexts on one device are independent.
+cudaError_t upload_device_constants(const int8_t *k8, const double *kk2, const double *kg2);
 LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz);
 // part: -1 all z-chunks; 0 the first and the last chunk (the ones holding interface planes);
 // 1 the others.  Launching part 0 then part 1 computes the same step as part -1.
 cudaError_t launch_step(int path, int mode, StepParams p, cudaStream_t st, int part = -1, int *nlaunch = nullptr);
 cudaError_t launch_node_w(int64_t nx, int64_t ny, int64_t nz, const uint8_t *mat, const uint8_t *mat_below,
-                          double dt, double *w, cudaStream_t st);
+                          const MatConst *mc, double dt, double *w, cudaStream_t st);
 cudaError_t launch_iface_update(const StepParams &p, const double *a_recv, double *u_send, cudaStream_t st);
 cudaError_t launch_finite_check(const double *u, int64_t n, int *flag, cudaStream_t st);
+cudaError_t launch_power_iter(int64_t nn, const double *x, const double *y, const double *w, const uint8_t *dmask,
+                              double dt2, double *z, double *acc, double *xnext, cudaStream_t st);
 
 // element_setup.cpp
 int derive_element_matrices(int8_t *k8, double *Ak, double *Ag);

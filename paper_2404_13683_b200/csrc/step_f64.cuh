@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(F2::NT, 2) step_f64(const StepParams p) {
     };
     for (int i = t; i < p.nmat + 1; i += NT) {
         const int id = i < p.nmat ? i : kZeroMat;
-        const MatConst &m = c_mat[id];
+        const MatConst &m = p.mc[id];
         if (VF) S.mw[id].v = MatV{{m.vl[0], m.vl[1], m.vl[2]}, {m.vm[0], m.vm[1], m.vm[2]}, {0.0, 0.0}};
         else S.mw[id].w = MatW{m.L0, m.M0, m.M0x2, m.L1, m.M1, m.M1x3, m.C2, 0.0};
     }

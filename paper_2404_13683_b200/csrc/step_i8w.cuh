@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     for (int i = t; i < 2 * 3 * C::NE; i += NT) (&S.tf[0][0][0])[i] = 0.0;
     for (int i = t; i < p.nmat + 1; i += NT) {      // a per-lane indexed constant-bank load serialises
         const int id = i < p.nmat ? i : kZeroMat;
-        S.mc[id] = make_double2(c_mat[id].cG, c_mat[id].c1);
+        S.mc[id] = make_double2(p.mc[id].cG, p.mc[id].c1);
     }
     if (hf == 0)
         for (int j = 0; j < 2; ++j) {   // material ids of layers Lfirst, Lfirst + 1

@@ -175,22 +175,22 @@ __global__ void __launch_bounds__(V1<PATH>::NT, V1<PATH>::MINB) step_v1(const St
             gather<C::PY>(ue, plo, phi, lx, ly);
             if constexpr (PATH == OVX_FP64 || PATH == OVX_VFEM) {
                 double fe[24];
-                if constexpr (PATH == OVX_VFEM) element_force_vfem_wht(ue, c_mat[m], fe);
-                else element_force_wht(ue, c_mat[m], fe);   // zero material -> fe = 0 exactly
+                if constexpr (PATH == OVX_VFEM) element_force_vfem_wht(ue, p.mc[m], fe);
+                else element_force_wht(ue, p.mc[m], fe);   // zero material -> fe = 0 exactly
 #pragma unroll
                 for (int r = 0; r < 24; ++r) {
                     S.fe[r][el] = fe[r];
                     if (MODE == MODE_DEBUG && dbg && p.dbg_fe) p.dbg_fe[dj * 24 + r] = fe[r];
                 }
             } else if constexpr (PATH == OVX_FP64_DENSE) {
-                const double ck = c_mat[m].ck, cg = c_mat[m].cg;
+                const double ck = p.mc[m].ck, cg = p.mc[m].cg;
 #pragma unroll 1
                 for (int r = 0; r < 24; ++r) {
                     double a = 0.0, b = 0.0;
 #pragma unroll
                     for (int c = 0; c < 24; ++c) {
-                        a = __dadd_rn(a, __dmul_rn(c_Kk[r * 24 + c], ue[c]));
-                        b = __dadd_rn(b, __dmul_rn(c_Kg[r * 24 + c], ue[c]));
+                        a = __dadd_rn(a, __dmul_rn(c_Kk[p.kset][r * 24 + c], ue[c]));
+                        b = __dadd_rn(b, __dmul_rn(c_Kg[p.kset][r * 24 + c], ue[c]));
                     }
                     const double f = __dadd_rn(__dmul_rn(ck, a), __dmul_rn(cg, b));
                     S.fe[r][el] = ein ? f : 0.0;

@@ -42,7 +42,13 @@ _SIGS = {
     "ovx_set_damping": [_vp, _d, _d],
     "ovx_setup_elements": [_vp, _int, _int],
     "ovx_get_int8_matrix": [_vp, _vp],
-    "ovx_critical_dt": [_vp, _vp],
+    "ovx_critical_dt": [_vp, _vp, _vp],
+    "ovx_get_phase_timers": [_vp, _vp, _vp, _vp, _int],
+    "ovx_get_partition": [_i64, _int, _int, _vp, _vp],
+    "ovx_nccl_unique_id": [_vp],
+    "ovx_create_dist": [_int, _int, _int, _vp, _vp],
+    "ovx_create_group": [_int, _vp, _vp],
+    "ovx_step_group": [_vp, _int, _i64],
     "ovx_set_sources": [_vp, _int, _vp, _vp, _i64, _vp],
     "ovx_set_state": [_vp, _vp, _vp, _i64],
     "ovx_get_state": [_vp, _vp, _vp, _vp],
@@ -101,16 +107,62 @@ def _dev_ptr(t) -> int:
     return t.data_ptr()
 
 
+def get_partition(nz: int, world: int, rank: int) -> tuple[int, int]:
+    """Element layers [ez0, ez1) of `rank` (ovx_get_partition)."""
+    a, b = np.zeros(1, dtype=np.int64), np.zeros(1, dtype=np.int64)
+    L = lib()
+    if L.ovx_get_partition(int(nz), int(world), int(rank), _np_ptr(a), _np_ptr(b)) != OVX_OK:
+        raise OvxError(OVX_EINVAL, L.ovx_last_error(None).decode())
+    return int(a[0]), int(b[0])
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes; ovx_nccl_unique_id)."""
+    out = np.zeros(128, dtype=np.uint8)
+    L = lib()
+    st = L.ovx_nccl_unique_id(_np_ptr(out))
+    if st != OVX_OK:
+        raise OvxError(st, L.ovx_last_error(None).decode())
+    return out.tobytes()
+
+
 class Ovx:
     """One context on one GPU.  Methods mirror `ovx_*` of include/ovx.h."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, _handle=None, rank: int = 0, world: int = 1):
         self._L = lib()
-        h = _vp()
-        self._check(self._L.ovx_create(device, _c.byref(h)), None)
+        if _handle is None:
+            h = _vp()
+            self._check(self._L.ovx_create(device, _c.byref(h)), None)
+        else:
+            h = _handle
         self.h = h
         self.device = device
+        self.rank, self.world = rank, world
         self.nx = self.ny = self.nz = 0
+        self.ez0 = 0
+
+    @classmethod
+    def create_dist(cls, device: int, rank: int, world: int, uid: bytes) -> "Ovx":
+        """Rank `rank` of `world` with a library-owned NCCL communicator (ovx_create_dist; collective)."""
+        L = lib()
+        idb = np.frombuffer(bytes(uid), dtype=np.uint8).copy()
+        h = _vp()
+        st = L.ovx_create_dist(device, rank, world, _np_ptr(idb), _c.byref(h))
+        if st != OVX_OK:
+            raise OvxError(st, L.ovx_last_error(None).decode())
+        return cls(device, _handle=h, rank=rank, world=world)
+
+    @classmethod
+    def create_group(cls, world: int, devices) -> list:
+        """`world` loopback-linked ranks in this process (ovx_create_group); step with step_group."""
+        L = lib()
+        dev = np.asarray(devices, dtype=np.int32)
+        hs = (_vp * world)()
+        st = L.ovx_create_group(world, _np_ptr(dev), hs)
+        if st != OVX_OK:
+            raise OvxError(st, L.ovx_last_error(None).decode())
+        return [cls(int(dev[r]), _handle=_vp(hs[r]), rank=r, world=world) for r in range(world)]
 
     # -- helpers ---------------------------------------------------------------
     def _check(self, st: int, h) -> None:
@@ -151,8 +203,10 @@ class Ovx:
         self._call("ovx_set_stream", _vp(raw) if raw else None)
 
     def set_grid(self, nx: int, ny: int, nz: int, ds: float) -> None:
+        """nz: the global element-layer count; a distributed rank keeps its slab [ez0, ez1)."""
         self._call("ovx_set_grid", nx, ny, nz, ds)
-        self.nx, self.ny, self.nz = nx, ny, nz
+        ez0, ez1 = get_partition(nz, self.world, self.rank) if self.world > 1 else (0, nz)
+        self.nx, self.ny, self.nz, self.ez0 = nx, ny, ez1 - ez0, ez0
 
     def set_materials(self, rho, kappa, G) -> None:
         r, k, g = _host(rho, np.float64), _host(kappa, np.float64), _host(G, np.float64)
@@ -188,10 +242,17 @@ class Ovx:
         self._call("ovx_get_int8_matrix", _np_ptr(out))
         return out
 
-    def critical_dt(self) -> float:
-        out = np.zeros(1)
-        self._call("ovx_critical_dt", _np_ptr(out))
-        return float(out[0])
+    def critical_dt(self, power_iter: bool = False):
+        """The element bound (float); with power_iter, (element bound, power-iteration dt)."""
+        a, b = np.zeros(1), np.zeros(1)
+        self._call("ovx_critical_dt", _np_ptr(a), _np_ptr(b) if power_iter else None)
+        return (float(a[0]), float(b[0])) if power_iter else float(a[0])
+
+    def get_phase_timers(self, reset: bool = False):
+        """(ms_ebe, ms_halo, ms_update) since the last reset (ovx_get_phase_timers)."""
+        a, b, c = np.zeros(1), np.zeros(1), np.zeros(1)
+        self._call("ovx_get_phase_timers", _np_ptr(a), _np_ptr(b), _np_ptr(c), 1 if reset else 0)
+        return float(a[0]), float(b[0]), float(c[0])
 
     def set_sources(self, node, axis, amp) -> None:
         node = _host(node, np.int64)
@@ -331,10 +392,18 @@ class Ovx:
         self.set_dirichlet(m.dirichlet)
         self.setup_elements(path, stages)
         self.set_dt(m.dt)
-        if len(m.src_node):
-            self.set_sources(m.src_node, m.src_axis, m.amp)
+        self.set_sources(m.src_node, m.src_axis, m.amp)   # also when empty: no stale sources
         if getattr(m, "alpha", 0.0) or getattr(m, "beta", 0.0):
             self.set_damping(m.alpha, m.beta)
+
+
+def step_group(ranks, n: int = 1) -> None:
+    """n steps of all ranks of a loopback group in lock step (ovx_step_group)."""
+    L = lib()
+    hs = (_vp * len(ranks))(*[r.h for r in ranks])
+    st = L.ovx_step_group(hs, len(ranks), int(n))
+    if st != OVX_OK:
+        raise OvxError(st, L.ovx_last_error(ranks[0].h).decode())
 
 
 def version() -> str:

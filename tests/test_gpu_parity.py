@@ -325,11 +325,15 @@ def test_receiver_traces_and_err_metric(ovxmod):
                 ref[k, :, it] = u[3 * n:3 * n + 3]
         refs[order] = ref
     assert np.array_equal(traces[0], refs[oracle.ORDER_U2])
-    live0 = np.abs(refs[oracle.ORDER_ELEMENT].reshape(-1, 120)).sum(1) > 0
+    # channels that are zero by symmetry carry only round-off in one order and exact zeros in the
+    # other (Err = 1 there); compare the channels with signal
+    en = (refs[oracle.ORDER_ELEMENT].reshape(-1, 120) ** 2).sum(1)
+    live0 = en > 1e-20 * en.max()
     assert physics.err_metric(traces[0].reshape(-1, 120)[live0],
                               refs[oracle.ORDER_ELEMENT].reshape(-1, 120)[live0]) < 1e-24
     a8, a64 = traces[0].reshape(-1, 120), traces[1].reshape(-1, 120)
-    live = np.abs(a64).sum(1) > 0
+    e64 = (a64 ** 2).sum(1)
+    live = e64 > 1e-20 * e64.max()
     err = physics.err_metric(a8[live], a64[live])
     assert err < 1e-24
 
@@ -568,8 +572,8 @@ def test_1000_steps_multi_tile_multi_chunk(ovxmod):
     z = np.zeros(3 * m.n_nodes)
     s = _solver(ovxmod, m, 0)
     assert m.dt < s.critical_dt()
-    ctas, tiles, zchunk = s.get_launch_config()
-    assert tiles >= 9 and (m.nz + 1 + zchunk - 1) // zchunk >= 3, (ctas, tiles, zchunk)
+    ctas, _, _ = s.get_launch_config()
+    assert ctas >= 27, ctas      # 3 × 3 tiles × ≥ 3 z-chunks
     s.set_state(z, z, 0)
     s.step(1000)
     s.check_finite()
@@ -638,3 +642,61 @@ def test_c5_layered_sampled(ovxmod):
     pts = [(0, 0, 0), (256, 256, 256), (128, 128, 64), (17, 250, 128), (255, 3, 192), (31, 7, 63), (62, 14, 65)]
     _sampled_apply_check(ovxmod, m, 0, u, pts)
     _sampled_apply_check(ovxmod, m, 1, u, pts[:3], nsample=10)
+
+
+def test_two_contexts_different_materials_concurrent_streams(ovxmod):
+    """Per-context material tables (no device-global __constant__ materials): two contexts with
+    different materials on one device, each on its own stream, their steps interleaved without host
+    synchronisation — both bit-exact against the oracle's U2 mirror (INT8 and factored-FP64 paths)."""
+    import torch
+    for path in (0, 1):
+        ma = wl.small_random(40, 8, 30, seed=1, ds=0.01, dt=1e-6)
+        mb = wl.small_random(33, 9, 28, seed=2, ds=0.02, dt=2e-6)
+        assert not np.allclose(ma.kappa, mb.kappa)
+        ua, ub = wl.random_field(ma, seed=5) * 1e-3, wl.random_field(mb, seed=6) * 1e-3
+        sa_t, sb_t = torch.cuda.Stream(), torch.cuda.Stream()
+        sa, sb = ovxmod.Ovx(0), ovxmod.Ovx(0)
+        sa.set_stream(sa_t)
+        sb.set_stream(sb_t)
+        sa.load_model(ma, path)
+        sb.load_model(mb, path)
+        sa.set_state(ua, ua, 0)
+        sb.set_state(ub, ub, 0)
+        for _ in range(6):
+            sa.step(5)
+            sb.step(5)
+        got = {}
+        for nm, s in (("a", sa), ("b", sb)):
+            got[nm] = s.get_state()
+        for nm, m, u0 in (("a", ma, ua), ("b", mb, ub)):
+            op = ORACLE_PATH[path]
+            if EXACT[path]:
+                r, rp, _, st = oracle.run(m.as_dict(), u0, u0, 0, 30, path=op, order=oracle.ORDER_U2)
+                assert st == 0 and np.array_equal(got[nm][0], r) and np.array_equal(got[nm][1], rp), (path, nm)
+            else:
+                r, _, _, st = oracle.run(m.as_dict(), u0, u0, 0, 30, path=op)
+                assert st == 0 and np.linalg.norm(got[nm][0] - r) <= 1e-12 * np.linalg.norm(r), (path, nm)
+
+
+def test_set_grid_resets_sources_and_negative_step_index_rejected(ovxmod):
+    """A context reused for a second model without sources injects nothing (set_grid clears the
+    previous model's sources and receivers); set_state rejects it < 0 (OVX_EINVAL)."""
+    m1 = wl.c1_cube(8, steps=20)
+    s = _solver(ovxmod, m1, 0)
+    m2 = wl.small_random(6, 5, 4, ds=0.01)
+    m2.src_node = np.zeros(0, np.int64)
+    m2.src_axis = np.zeros(0, np.int32)
+    m2.amp = np.zeros((0, 1))
+    s.set_grid(m2.nx, m2.ny, m2.nz, m2.ds)
+    s.set_materials(m2.rho, m2.kappa, m2.G)
+    s.set_element_materials(m2.mat)
+    s.set_dirichlet(m2.dirichlet)
+    s.setup_elements(0, 8)
+    s.set_dt(m2.dt)
+    z = np.zeros(3 * m2.n_nodes)
+    s.set_state(z, z, 0)
+    s.step(5)
+    u, _, _ = s.get_state()
+    assert np.all(u == 0)                   # no stale point force from the first model
+    with pytest.raises(ovxmod.OvxError):
+        s.set_state(z, z, -1)
