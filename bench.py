@@ -277,8 +277,53 @@ class Single:
         return self.s.get_state(out_u=out_u, with_prev=False)[0]
 
 
+class ShardedLib:
+    """One rank of the C5 z-slab decomposition, stepped by the library (ovx_create_dist: a
+    library-owned NCCL communicator; ovx_step runs the overlapped schedule — edge z-chunks on a
+    high-priority stream, interior chunks concurrently, NCCL P2P interface exchange, interface
+    update).  The NCCL unique id travels through torch.distributed."""
+
+    def __init__(self, n, path, local, stream, world, rank):
+        import torch.distributed as dist
+        from paper_2404_13683_b200 import ovx as O
+        lm, slab, self.u0 = _slab_workload(n, world, rank)
+        uid = [O.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        s = O.Ovx.create_dist(local, rank, world, uid[0])
+        s.set_stream(stream)
+        s.set_grid(n, n, n * world, lm.ds)               # global layer count; the library derives the slab
+        assert (s.ez0, s.nz) == (slab.ez0, slab.nzl)
+        s.set_materials(lm.rho, lm.kappa, lm.G)
+        s.set_element_materials(lm.mat if lm.mat_below is None else np.concatenate([lm.mat_below, lm.mat]))
+        s.set_dirichlet(lm.dirichlet)
+        s.setup_elements(path, 8)
+        s.set_dt(lm.dt)
+        nn2 = (n + 1) * (n + 1)
+        s.set_sources(lm.src_node + slab.ez0 * nn2, lm.src_axis, lm.amp)   # global node ids
+        self.s = s
+        self.nn = (n + 1) * (n + 1) * (slab.nzl + 1)
+        self.ne = n * n * slab.nzl
+        self.launches_per_step = None
+
+    def set_state(self, u, up):
+        self.s.set_state(u, up, 0)
+
+    def step(self, k):
+        if self.launches_per_step is None and k > 0:
+            _, n0 = self.s.get_timers()
+            self.s.step(1)
+            _, n1 = self.s.get_timers()
+            self.launches_per_step = n1 - n0
+            k -= 1
+        self.s.step(k)
+
+    def get_state(self, out_u=None):
+        return self.s.get_state(out_u=out_u, with_prev=False)[0]
+
+
 class Sharded:
-    """One rank of the C5 z-slab decomposition (NCCL interface exchange)."""
+    """One rank of the C5 z-slab decomposition driven from Python (dist.py; the test hook with
+    several ranks on one device and a gloo host-staged exchange, or OVX_BENCH_DIST=python)."""
 
     def __init__(self, n, path, local, stream, world, rank):
         from paper_2404_13683_b200 import dist as D
@@ -391,7 +436,12 @@ def main() -> None:
         return float(t.item())
 
     def timed_run(path_id: int, steps: int, warmup: int, sample_clocks: bool):
-        R = Single(args.n, path_id, local, stream) if world == 1 else Sharded(args.n, path_id, local, stream, world, rank)
+        if world == 1:
+            R = Single(args.n, path_id, local, stream)
+        elif backend == "nccl" and os.environ.get("OVX_BENCH_DIST", "library") == "library":
+            R = ShardedLib(args.n, path_id, local, stream, world, rank)
+        else:
+            R = Sharded(args.n, path_id, local, stream, world, rank)
         R.set_state(R.u0, R.u0)
         R.step(warmup)
         barrier()
@@ -520,7 +570,9 @@ def main() -> None:
                    "path": args.path,
                    "elements": E_total, "nodes": nodes_total,
                    "parallelism": "single GPU" if world == 1 else
-                   (f"z-slabs x{world}, NCCL P2P interface exchange, {'overlapped' if Sharded.OVERLAP else 'serial'} schedule" if backend == "nccl" else
+                   (f"z-slabs x{world}, NCCL P2P interface exchange, overlapped schedule in the library (ovx_step)"
+                    if backend == "nccl" and os.environ.get("OVX_BENCH_DIST", "library") == "library" else
+                    f"z-slabs x{world}, NCCL P2P interface exchange, {'overlapped' if Sharded.OVERLAP else 'serial'} schedule (dist.py)" if backend == "nccl" else
                     f"z-slabs x{world} on one device, {backend} host-staged interface exchange (test hook)"),
                    "l2": "inputs larger than L2 (%.2f GB touched per step per GPU)" % (_algorithmic_bytes(R_nn, R_ne) / 1e9)},
         "dof_steps_per_s": 3 * nodes_total * args.steps / (ms / 1e3),

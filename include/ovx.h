@@ -60,8 +60,12 @@ enum {
                            (Walsh-Hadamard modes) */
     OVX_VFEM_DENSE = 4, /* VFEM, literal dense form f_e = (κds/72)(Vk u_e) + (Gds/216)(Vg u_e) with
                            sequential sums (bit-exact mirror of the oracle's VFEM path) */
-    OVX_FP64_DENSE = 2  /* FP64, literal dense form f_e = (κds/256)(K^κ u_e) + (Gds/384)((K̄^G+128I)u_e)
+    OVX_FP64_DENSE = 2, /* FP64, literal dense form f_e = (κds/256)(K^κ u_e) + (Gds/384)((K̄^G+128I)u_e)
                            with sequential sums: bit-identical to the oracle's FP64 definition */
+    OVX_INT8_DIRECT = 5 /* NEXT-4: the paper's DIRECT FP64→INT8 method (Fig. 2 left, Eqs. 11-14, a = 2^7,
+                           N = 8 stages): every stage converts the FP64 remainder to an INT8 digit (2N
+                           conversions per value instead of one), same integer image and results as the
+                           hierarchical paper-digit path (L146); tensor cores as OVX_INT8.  M = 8, undamped. */
 };
 
 /* ---- lifetime ------------------------------------------------------------ */

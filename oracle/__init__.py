@@ -110,6 +110,8 @@ DIGITS_PAPER, DIGITS_BYTES = 0, 1
 #   ORDER_ABS     — not a product: Σ_e |f_e[n]|, the scale of the cross-order rounding bound.
 ORDER_ELEMENT, ORDER_U2, ORDER_ABS = 0, 1, 2
 DIGITS_BYTES_FOLD = 3      # byte slices + Eq. 9 diagonal term in the integer product (variant D)
+DIGITS_DIRECT = 4          # the direct N-stage FP64→INT8 conversion (Fig. 2 left, Eqs. 11-14, a = 2^7)
+DIGITS_DIRECT_FOLD = 6     # direct conversion + variant D
 
 
 def element_nodes(nx: int, ny: int, e: int) -> np.ndarray:
@@ -154,7 +156,7 @@ def element_int8(ue, kappa, G, ds, M: int = 8, digits: int = DIGITS_BYTES_FOLD) 
     """Bit-level integer path for one element; returns s, v, d, C, y (python ints), fe."""
     K8, _, _ = int_matrices()
     ue = np.ascontiguousarray(ue, dtype=np.float64)
-    nd = (7 * M + 1 + 7) // 8 if (digits & 1) else M
+    nd = (7 * M + 1 + 7) // 8 if (digits & 1) and not (digits & 4) else M
     s = np.zeros(1)
     v = np.zeros(48, dtype=np.int64)
     d = np.zeros(nd * 48, dtype=np.int32)

@@ -131,8 +131,15 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
     /* digits bit 1 ("fold", DESIGN.md variant D): the Eq. 9 diagonal term (256/3)(G/κ)u_e =
      * 128·ū_{e,G} is taken in the integer domain, y_D = K_D v with K_D = [K^κ | K̄^G + 128 I]
      * (= [256 A_κ | 384 A_G]), and f_e = RN(c1s·RN(y_D)), c1s = RN(c1·RN(s_e·2^-56)). */
+    /* digits bit 2 ("direct", Fig. 2 left; Eqs. 11-14 with a = 2^7, N = M stages): every
+     * stage converts the FP64 remainder to an INT8 digit, d_i = INT(a·r_{i-1}), r_i = a·r_{i-1} − d_i
+     * (r_0 = ū_es; each step exact in FP64), digits clamped to ±127 (reading Q9 for |x| = 1: the
+     * residual then carries 127 into every later stage, i.e. ±(2^{7M}−1) as in the paper-digit
+     * hierarchical path).  y = Σ_i a^{N−i} K d_i.  Stored lowest weight first (dall[k][0] = d_N). */
+    const int direct = (digits >> 2) & 1;
     const int fold = (digits >> 1) & 1;
     digits &= 1;
+    if (direct) digits = 0;
     double cG = (2.0 * G) / (3.0 * kappa);       /* (2/3) G/κ, */
     double c1 = kappa * ds / 256.0;              /* κ ds / 256, Eq. 9          */
     double c2 = (256.0 * G) / (3.0 * kappa);     /* (256/3) G/κ, Eq. 9         */
@@ -156,6 +163,20 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
         double r = 1.0 / s;                      /* reading Q7: one reciprocal  */
         for (int i = 0; i < 48; ++i) {
             double x = ub[i] * r;                /* ū_es, Eq. 10                */
+            if (direct) {
+                double rr = x;
+                int64_t V = 0;
+                for (int st = 0; st < M; ++st) {
+                    double t = 128.0 * rr;       /* a·r_{i-1}, exact                 */
+                    int64_t d = (int64_t)t;      /* INT(·): truncation toward 0 (Q8) */
+                    if (d > 127) d = 127;
+                    if (d < -127) d = -127;
+                    rr = t - (double)d;          /* r_i, exact (Sterbenz)            */
+                    V = V * 128 + d;
+                }
+                v[i] = V;
+                continue;
+            }
             double t = x * Ad;                   /* exact power-of-two scaling  */
             v[i] = (int64_t)t;                   /* truncation toward 0, Eq. 12 (Q8) */
             if (!digits) {                       /* reading Q9 clamp            */
@@ -167,7 +188,24 @@ int oracle_element_int8(const double *ue, double kappa, double G, double ds,
     if (v_out) memcpy(v_out, v, sizeof v);
     for (int r = 0; r < 24; ++r) y[r] = 0;
     int32_t dall[48][8];
-    for (int k = 0; k < 48; ++k) oracle_digits(v[k], M, digits, dall[k]);
+    if (direct) {   /* the digits of the direct recursion, recomputed (lowest weight first) */
+        double r = degenerate ? 0.0 : 1.0 / s;
+        for (int k = 0; k < 48; ++k) {
+            double rr = degenerate ? 0.0 : ub[k] * r;
+            int32_t tmp[8];
+            for (int st = 0; st < M; ++st) {
+                double t = 128.0 * rr;
+                int64_t d = (int64_t)t;
+                if (d > 127) d = 127;
+                if (d < -127) d = -127;
+                rr = t - (double)d;
+                tmp[st] = (int32_t)d;
+            }
+            for (int st = 0; st < M; ++st) dall[k][st] = tmp[M - 1 - st];
+        }
+    } else {
+        for (int k = 0; k < 48; ++k) oracle_digits(v[k], M, digits, dall[k]);
+    }
     for (int j = 0; j < nd; ++j) {
         int32_t d[48];
         for (int k = 0; k < 48; ++k) {

@@ -33,6 +33,7 @@ struct ovx_ctx {
     int *d_flag = nullptr;   // finiteness flag (allocated once: no cudaMalloc / cudaFree per state upload)
     double *d_u = nullptr, *d_up = nullptr, *d_w = nullptr;
     double alpha = 0, beta = 0;       // Rayleigh damping (reading R1)
+    int direct = 0;                   // OVX_INT8_DIRECT: the direct N-stage conversion (NEXT-4)
     double *d_un = nullptr;           // third state buffer of damped steps
     int8_t k8[1152];
     double Ak[576], Ag[576], Kk[576], Kg[576];
@@ -149,6 +150,7 @@ StepParams base_params(ovx_ctx *ctx) {
     p.mat = ctx->d_mat;
     p.dmask = ctx->d_mask;
     p.stages = ctx->stages;
+    p.direct = ctx->direct;
     p.nmat = ctx->nmat;
     return p;
 }
@@ -377,8 +379,12 @@ ovx_status ovx_set_dt(ovx_ctx *ctx, double dt) {
 ovx_status ovx_setup_elements(ovx_ctx *ctx, int path, int stages) {
     if (!ctx) return fail(nullptr, OVX_EINVAL, "null context");
     if (!ctx->have_grid || !ctx->have_emat) return fail(ctx, OVX_ESTATE, "set grid and element materials first");
-    if (path != OVX_INT8 && path != OVX_FP64 && path != OVX_FP64_DENSE && path != OVX_VFEM && path != OVX_VFEM_DENSE)
-        return fail(ctx, OVX_EINVAL, "path must be OVX_INT8, OVX_FP64, OVX_FP64_DENSE, OVX_VFEM or OVX_VFEM_DENSE");
+    if (path != OVX_INT8 && path != OVX_FP64 && path != OVX_FP64_DENSE && path != OVX_VFEM && path != OVX_VFEM_DENSE &&
+        path != OVX_INT8_DIRECT)
+        return fail(ctx, OVX_EINVAL, "path must be OVX_INT8, OVX_INT8_DIRECT, OVX_FP64, OVX_FP64_DENSE, OVX_VFEM or OVX_VFEM_DENSE");
+    if (path == OVX_INT8_DIRECT && stages != 8) return fail(ctx, OVX_EINVAL, "the direct path is built for M = 8");
+    ctx->direct = path == OVX_INT8_DIRECT ? 1 : 0;
+    if (path == OVX_INT8_DIRECT) path = OVX_INT8;   // the INT8 kernels, direct conversion
     if (stages != 8 && !(path == OVX_INT8 && (stages == 4 || stages == 6)))
         return fail(ctx, OVX_EINVAL, "stages: M = 8 (all paths), or M = 4 / 6 on the INT8 path");
     if (derive_element_matrices(ctx->k8, ctx->Ak, ctx->Ag) != 0)
@@ -595,6 +601,8 @@ ovx_status ovx_step(ovx_ctx *ctx, int64_t n) {
     if (s) return s;
     if (!(ctx->dt > 0)) return fail(ctx, OVX_ESTATE, "set dt first");
     if (n < 0) return fail(ctx, OVX_EINVAL, "n must be >= 0");
+    if (ctx->direct && (ctx->alpha != 0.0 || ctx->beta != 0.0))
+        return fail(ctx, OVX_EINVAL, "the direct N-stage path (OVX_INT8_DIRECT) is undamped only");
     if (ctx->world > 1) {
         if (ctx->group) return fail(ctx, OVX_ESTATE, "loopback-group ranks step together with ovx_step_group");
         return dist_step(ctx, n);
@@ -1177,8 +1185,7 @@ ovx_status ovx_create_dist(int device, int rank, int world, const uint8_t id[128
     ovx_ctx *ctx = *out;
     ctx->rank = rank;
     ctx->world = world;
-    if (world == 1) return OVX_OK;
-    const nccl::Api &A = nccl::api();
+    const nccl::Api &A = nccl::api();   // world = 1: a communicator of one (checks the NCCL setup)
     if (!A.ok()) {
         ovx_destroy(ctx);
         *out = nullptr;

@@ -215,6 +215,18 @@ __device__ __forceinline__ double limb_biased(int32_t d0, int32_t d1, int32_t d2
     asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(p1), "r"(c_two16));
     return __longlong_as_double((long long)acc) - I8_LIMB_MAGIC;
 }
+// The same for the direct N-stage path (DIR): stages in base 2^7, D_j = −C_j + B (B = 16·127·127,
+// s8 digits): L = p0 + 2^14·p1 (p0 = D0 + 128·D1, p1 = D2 + 128·D3 < 2^26), L < 2^41, assembled as
+// two words under the magic exponent; the bias B·(1 + 2^7 + 2^14 + 2^21) comes out with the magic.
+template <int32_t B>
+__device__ __forceinline__ double limb_biased128(int32_t d0, int32_t d1, int32_t d2, int32_t d3) {
+    constexpr double MAGIC = 0x1.8p52 + (double)B * 2113665.0;
+    const uint32_t p0 = (uint32_t)(d0 + 128 * d1), p1 = (uint32_t)(d2 + 128 * d3);
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0x43380000;" : "=r"(lo), "=r"(hi) : "r"(p0), "r"(p1 << 14),
+        "r"(p1 >> 18));
+    return __hiloint2double((int)hi, (int)lo) - MAGIC;
+}
 // max_i |x_i| of finite / infinite doubles as the integer max of their magnitude bit patterns
 // (monotone for non-NaN values; a NaN sorts above +inf and makes the element degenerate)
 __device__ __forceinline__ unsigned long long abs_bits(double x) {
@@ -239,31 +251,32 @@ inline void attr_set(unsigned &mask) {
     mask |= 1u << (dev & 31);
 }
 
-template <int MODE, int M, bool DAMP, class G, bool TA>
+template <int MODE, int M, bool DAMP, class G, bool TA, bool DIR = false>
 cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     static unsigned attr = 0;
     const int smem = (int)sizeof(SmemI8<G, TA>);
     if (!attr_done(attr)) {
-        cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G, TA, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         // all of the unified L1/shared array as shared memory, so G::CPS CTAs fit one SM
-        e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G, TA>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        e = cudaFuncSetAttribute(step_i8w<MODE, M, DAMP, G, TA, DIR>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         attr_set(attr);
     }
-    step_i8w<MODE, M, DAMP, G, TA><<<(unsigned)ctas, G::NT, smem, st>>>(p);
+    step_i8w<MODE, M, DAMP, G, TA, DIR><<<(unsigned)ctas, G::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-// INT8 kernel variant (OVX_I8_KERNEL): "x" (default) step_i8x, the round-2 schedule (time steps
-// and products; the debug records always come from step_i8w); "tmem" step_i8w with the A operand
-// in TMEM; "smem" step_i8w with A in shared memory.  DESIGN.md §6.1 has the measurements.
+// INT8 kernel variant (OVX_I8_KERNEL): "tmem" (default) step_i8w with the A operand in TMEM;
+// "smem" step_i8w with A in shared memory; "x" step_i8x (time steps and products; word or half-word
+// operand layout, OVX_I8X_LAYOUT; the debug records always come from step_i8w).
+// has the measurements (the three are bit-identical).
 int i8_variant() {
     static const int v = [] {
         const char *e = std::getenv("OVX_I8_KERNEL");
         if (e && std::strcmp(e, "smem") == 0) return 1;
-        if (e && std::strcmp(e, "tmem") == 0) return 0;
-        return 2;
+        if (e && std::strcmp(e, "x") == 0) return 2;
+        return 0;
     }();
     return v;
 }
@@ -316,6 +329,14 @@ cudaError_t launch_i8x_mode(int mode, const StepParams &p, int64_t ctas, cudaStr
 
 template <int M>
 cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStream_t st) {
+    if (p.direct) {   // NEXT-4: the direct N-stage conversion (M = 8, undamped; OVX_INT8_DIRECT)
+        if constexpr (M == 8) {
+            if (mode == MODE_STEP) return launch_i8w<MODE_STEP, 8, false, I8W, true, true>(p, ctas, st);
+            if (mode == MODE_APPLY) return launch_i8w<MODE_APPLY, 8, false, I8W, true, true>(p, ctas, st);
+            return launch_i8w<MODE_DEBUG, 8, false, I8W, true, true>(p, ctas, st);
+        }
+        return cudaErrorInvalidValue;
+    }
     const int v = i8_variant();
     if (v == 2 && mode != MODE_DEBUG)
         return p.slab_flags ? launch_i8x_mode<M, true>(mode, p, ctas, st) : launch_i8x_mode<M, false>(mode, p, ctas, st);

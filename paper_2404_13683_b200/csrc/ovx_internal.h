@@ -52,6 +52,7 @@ struct StepParams {
     double ca, cb;         // RN(alpha·dt), RN(beta/dt)
     double *un;
     int stages;            // INT8 path: M (4, 6 or 8)
+    int direct;            // INT8 path: the direct N-stage conversion (OVX_INT8_DIRECT, NEXT-4)
     int nmat;              // materials in mc[0, nmat) (ids < 255; 255 = zero material)
     int slab_flags;
     double *iface_top_A;   // [NX1*NY1][3]   partial force of the top plane (bit 1)

@@ -122,7 +122,12 @@ __device__ __forceinline__ void gather16(double (&ue)[16], const double *lo, con
 // mt·192 + pa·48 (48 columns = N); A (shared by the two skewed M-tiles) at 384 + pa·28 + 4·chunk.
 constexpr uint32_t TA_D_TILE = 192, TA_D_ARR = 48, TA_A0 = 384, TA_A_ARR = 28;
 
-template <int MODE, int M, int HF, bool FAST, bool TA>
+// DIR (OVX_INT8_DIRECT, NEXT-4; Fig. 2 left, Eqs. 11-14 with a = 2^7, N = M): the
+// direct method — every one of the M stages converts the FP64 remainder to an INT8 digit,
+// d_i = INT(a·r_{i-1}) clamped to ±127, r_i = a·r_{i-1} − d_i (exact) — i.e. 2M conversions per value
+// (F2I and back) instead of one; the digits (signed, lowest weight first) take the byte slots of
+// the hierarchical path's v + 2^{7M}, the MMA reads A as s8, the stages recombine in base 2^7.
+template <int MODE, int M, int HF, bool FAST, bool TA, bool DIR = false>
 __device__ __forceinline__ void i8w_chunks(const StepParams &p, const double (&ue)[16], double cG, double r, double R,
                                            bool deg, uint8_t *Ab, uint32_t rowoff, bool dbg, int64_t dj,
                                            uint32_t ta, uint64_t *xbar, uint32_t xpar) {
@@ -136,6 +141,27 @@ __device__ __forceinline__ void i8w_chunks(const StepParams &p, const double (&u
         const bool gpart = ch >= 3;
         const int j0 = 8 * (gpart ? ch - 3 : ch) - 8 * HF;     // index into ue of value 0 of the chunk
         long long v[8];
+        uint32_t lo[8], hi[8];
+        if constexpr (DIR) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double ub = gpart ? __dmul_rn(cG, ue[j0 + q]) : ue[j0 + q];
+                double rr = deg ? 0.0 : __dmul_rn(ub, r);          // ū_es (Eq. 10)
+                unsigned long long w = 0;
+                long long V = 0;
+#pragma unroll
+                for (int st = 0; st < M; ++st) {                    // stage i = st + 1 (Eqs. 12-14)
+                    const double t = __dmul_rn(128.0, rr);          // a·r_{i-1}, exact
+                    const int d = max(-127, min(127, __double2int_rz(t)));
+                    rr = __dsub_rn(t, (double)d);                   // r_i, exact
+                    w |= (unsigned long long)(uint8_t)d << (8 * (M - 1 - st));
+                    V = V * 128 + d;
+                }
+                lo[q] = (uint32_t)w;
+                hi[q] = (uint32_t)(w >> 32);
+                v[q] = V;
+            }
+        } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const double ub = gpart ? __dmul_rn(cG, ue[j0 + q]) : ue[j0 + q];
@@ -144,10 +170,11 @@ __device__ __forceinline__ void i8w_chunks(const StepParams &p, const double (&u
             else        // tiny-normal or non-finite s: the two roundings of Eq. 10 as written
                 v[q] = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), SCALE));
         }
-        uint32_t lo[8], hi[8];
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            if constexpr (7 * M >= 32) {   // v + 2^{7M}: the offset only touches the high word
+            if constexpr (DIR) {
+            } else if constexpr (7 * M >= 32) {   // v + 2^{7M}: the offset only touches the high word
                 lo[q] = (uint32_t)(unsigned long long)v[q];
                 hi[q] = (uint32_t)((unsigned long long)v[q] >> 32) + (uint32_t)(AOFF >> 32);
             } else {                        // v + 2^{7M} < 2^32
@@ -160,7 +187,8 @@ __device__ __forceinline__ void i8w_chunks(const StepParams &p, const double (&u
                 if (p.dbg_v) p.dbg_v[dj * 48 + k] = v[q];
                 if (p.dbg_d)
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) p.dbg_d[dj * 384 + j * 48 + k] = j < NB ? (uint8_t)(vp >> (8 * j)) : 0;
+                    for (int j = 0; j < 8; ++j)
+                        p.dbg_d[dj * 384 + j * 48 + k] = (DIR ? j < M : j < NB) ? (uint8_t)(vp >> (8 * j)) : 0;
             }
         }
         const uint32_t off = rowoff + (uint32_t)ch * 128;
@@ -185,14 +213,16 @@ __device__ __forceinline__ void i8w_chunks(const StepParams &p, const double (&u
     }
 }
 
-template <int MODE, int M, int HF, bool TA>
+template <int MODE, int M, int HF, bool TA, bool DIR = false>
 __device__ __forceinline__ void i8w_convert(const StepParams &p, const double (&ue)[16], double cG, double s,
                                             bool deg, bool vzero, bool fast, uint8_t *Ab, uint32_t rowoff,
                                             bool dbg, int64_t dj, uint32_t ta, uint64_t *xbar, uint32_t xpar) {
     constexpr double SCALE = (double)(1ull << (7 * M));
     const double r = 1.0 / s;                                  // RN(1/s_e), reading Q7
     const double R = vzero ? 0.0 : __dmul_rn(r, SCALE);        // exact power-of-two scaling
-    if (__all_sync(0xffffffffu, fast))
+    if constexpr (DIR)
+        i8w_chunks<MODE, M, HF, false, TA, true>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj, ta, xbar, xpar);
+    else if (__all_sync(0xffffffffu, fast))
         i8w_chunks<MODE, M, HF, true, TA>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj, ta, xbar, xpar);
     else
         i8w_chunks<MODE, M, HF, false, TA>(p, ue, cG, r, R, deg, Ab, rowoff, dbg, dj, ta, xbar, xpar);
@@ -211,9 +241,13 @@ __device__ __forceinline__ int ring3(int x) { return (x + 12) % NS3; }  // x >= 
 // DAMP (MODE_STEP only): Rayleigh damping, reading R1 — the smem planes hold the EBE input
 // ũ = u + cb·(u − u_prev) (node maxima of ũ), the update reads u and u_prev from global memory and
 // writes u^{it+1} to p.un.
-template <int MODE, int M, bool DAMP, class G, bool TA>
+template <int MODE, int M, bool DAMP, class G, bool TA, bool DIR = false>
 __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     static_assert(!TA || G::MT == 2, "the TMEM A operand is shared by two skewed M-tiles");
+    // accumulator bias source: 16 padding bytes per row against B = 127: 255 (u8 A) or 127 (s8 A, DIR)
+    constexpr uint32_t PADW = DIR ? 0x7F7F7F7Fu : 0xFFFFFFFFu;
+    constexpr int32_t BIASV = DIR ? 16 * 127 * 127 : I8_BIAS;
+    constexpr uint32_t IDS = DIR ? (IDESC | (1u << 7)) : IDESC;   // a_format: signed 8-bit for DIR
     using C = G;
     constexpr int EX = C::EX, TX = C::TX, PX = C::PX;
     constexpr int NB = (7 * M + 1 + 7) / 8;
@@ -299,7 +333,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     for (int idx = t; idx < C::MT * 4 * 128; idx += NT) {   // K-padding bytes: 255 (bias source)
         const int a = idx >> 7, r = idx & 127;
         *reinterpret_cast<uint4 *>(&S.A[a >> 2][a & 3][(r >> 3) * A1_PITCH + 6 * 128 + (r & 7) * 16]) =
-            make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+            make_uint4(PADW, PADW, PADW, PADW);
     }
     if (warp == 0) ptx::tmem_alloc<C::TMEM_COLS>(&S.tmem);
     if (t == 0)
@@ -338,7 +372,7 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
     if (TA && wu < 4) {   // K-padding chunk 6 of the TMEM A arrays: 255 bytes (bias source), written once
 #pragma unroll
         for (int pa = 0; pa < 4; ++pa)
-            ptx::tmem_st4(S.tmem + ((uint32_t)(qd * 32) << 16) + TA_A0 + pa * TA_A_ARR + 24, ~0u, ~0u, ~0u, ~0u);
+            ptx::tmem_st4(S.tmem + ((uint32_t)(qd * 32) << 16) + TA_A0 + pa * TA_A_ARR + 24, PADW, PADW, PADW, PADW);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();   // ordered before the first MMA by the M-tile barrier of convert()
     }
@@ -446,20 +480,20 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
                 const int32_t c0 = (int32_t)R0[2 * q], c1_ = (int32_t)R0[2 * q + 1];
                 const int32_t c2_ = (int32_t)R1[2 * q], c3 = (int32_t)R1[2 * q + 1];
                 // stages beyond NA arrays are absent: give them the bias value (C_j = 0 after removal)
-                const int32_t c4 = NA > 2 ? (int32_t)R2[2 * q] : I8_BIAS, c5 = NA > 2 ? (int32_t)R2[2 * q + 1] : I8_BIAS;
-                const int32_t c6 = NA > 3 ? (int32_t)R3[2 * q] : I8_BIAS, c7 = NA > 3 ? (int32_t)R3[2 * q + 1] : I8_BIAS;
-                // D_j = −C_j + I8_BIAS, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j, two limbs < 2^46
-                const double dlo = limb_biased(c0, c1_, c2_, c3);
-                const double dhi = NA > 2 ? limb_biased(c4, c5, c6, c7) : 0.0;
-                const double Y = NA > 2 ? __fma_rn(dhi, 0x1p32, dlo) : dlo;    // RN(−y)
+                const int32_t c4 = NA > 2 ? (int32_t)R2[2 * q] : BIASV, c5 = NA > 2 ? (int32_t)R2[2 * q + 1] : BIASV;
+                const int32_t c6 = NA > 3 ? (int32_t)R3[2 * q] : BIASV, c7 = NA > 3 ? (int32_t)R3[2 * q + 1] : BIASV;
+                // D_j = −C_j + BIAS, C_j = K_D·b_j (K_D·1 = 0): y = Σ_j 256^j C_j (DIR: 128^j), two limbs
+                const double dlo = DIR ? limb_biased128<BIASV>(c0, c1_, c2_, c3) : limb_biased(c0, c1_, c2_, c3);
+                const double dhi = NA > 2 ? (DIR ? limb_biased128<BIASV>(c4, c5, c6, c7) : limb_biased(c4, c5, c6, c7)) : 0.0;
+                const double Y = NA > 2 ? __fma_rn(dhi, DIR ? 0x1p28 : 0x1p32, dlo) : dlo;    // RN(−y)
                 const double f = __dmul_rn(alpha, Y);            // = RN(c1s·RN(y))
                 if (MODE == MODE_DEBUG && edbg) {
                     const int i = 12 * hf + j;
-                    const int32_t Cj[8] = {c0 - I8_BIAS, c1_ - I8_BIAS, c2_ - I8_BIAS, c3 - I8_BIAS,
-                                           c4 - I8_BIAS, c5 - I8_BIAS, c6 - I8_BIAS, c7 - I8_BIAS};
+                    const int32_t Cj[8] = {c0 - BIASV, c1_ - BIASV, c2_ - BIASV, c3 - BIASV,
+                                           c4 - BIASV, c5 - BIASV, c6 - BIASV, c7 - BIASV};
                     __int128 y = 0;
 #pragma unroll
-                    for (int jj = 7; jj >= 0; --jj) y = y * 256 - (__int128)Cj[jj];
+                    for (int jj = 7; jj >= 0; --jj) y = y * (DIR ? 128 : 256) - (__int128)Cj[jj];
                     if (p.dbg_C)
 #pragma unroll
                         for (int jj = 0; jj < 8; ++jj) p.dbg_C[edj * 192 + jj * 24 + i] = -Cj[jj];
@@ -513,11 +547,11 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         uint64_t *xbar = &S.mbar[C::MT - 1 - mt];
         if (hf == 0) {
             gather16<0, PX, C::NODES>(ue, &S.up[sL][0][0], &S.up[sL1][0][0], lx, ly);
-            i8w_convert<MODE, M, 0, TA>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj, ta, xbar, xpar);
+            i8w_convert<MODE, M, 0, TA, DIR>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj, ta, xbar, xpar);
             if (MODE == MODE_DEBUG && dbg && p.dbg_s) p.dbg_s[dj] = s;
         } else {
             gather16<1, PX, C::NODES>(ue, &S.up[sL][0][0], &S.up[sL1][0][0], lx, ly);
-            i8w_convert<MODE, M, 1, TA>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj, ta, xbar, xpar);
+            i8w_convert<MODE, M, 1, TA, DIR>(p, ue, cG, s, deg, vzero, fast, Ab, rowoff, dbg, dj, ta, xbar, xpar);
         }
         xpar ^= 1u;
         if (TA) {
@@ -547,21 +581,21 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
                         const uint32_t d = S.tmem + mtu * TA_D_TILE + pa * TA_D_ARR;
 #pragma unroll
                         for (int ks = 0; ks < 3; ++ks)
-                            ptx::mma_i8_ts(d, at + 8 * ks, ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC,
+                            ptx::mma_i8_ts(d, at + 8 * ks, ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDS,
                                            ks > 0 ? 1u : 0u);
-                        ptx::mma_i8_ts(d, at + 12, ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
-                        ptx::mma_i8_ts(d, at + 20, ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
+                        ptx::mma_i8_ts(d, at + 12, ptx::smem_desc(bi0, 128, BI_PITCH), IDS, 1u);
+                        ptx::mma_i8_ts(d, at + 20, ptx::smem_desc(bi1, 128, BI_PITCH), IDS, 1u);
                     } else {
                     const uint32_t abase = a0 + pa * A1_BYTES;
                     const uint32_t d = S.tmem + mtu * 256 + pa * 64;
 #pragma unroll
                     for (int ks = 0; ks < 3; ++ks)
                         ptx::mma_i8(d, ptx::smem_desc(abase + ks * 256, 128, A1_PITCH),
-                                    ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDESC, ks > 0 ? 1u : 0u);
+                                    ptx::smem_desc(b0 + ks * 256, 128, B1_PITCH), IDS, ks > 0 ? 1u : 0u);
                     ptx::mma_i8(d, ptx::smem_desc(abase + 3 * 128, 128, A1_PITCH),
-                                ptx::smem_desc(bi0, 128, BI_PITCH), IDESC, 1u);
+                                ptx::smem_desc(bi0, 128, BI_PITCH), IDS, 1u);
                     ptx::mma_i8(d, ptx::smem_desc(abase + 5 * 128, 128, A1_PITCH),
-                                ptx::smem_desc(bi1, 128, BI_PITCH), IDESC, 1u);
+                                ptx::smem_desc(bi1, 128, BI_PITCH), IDS, 1u);
                     }
                 }
                 ptx::mma_commit(&S.mbar[mtu]);

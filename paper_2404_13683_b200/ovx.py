@@ -16,6 +16,7 @@ from . import build as _build
 
 OVX_OK, OVX_EINVAL, OVX_EUNSTABLE, OVX_ESTATE, OVX_ECUDA, OVX_ENCCL, OVX_ENOMEM = 0, 2, 3, 6, 7, 8, 9
 OVX_INT8, OVX_FP64, OVX_FP64_DENSE, OVX_VFEM, OVX_VFEM_DENSE = 0, 1, 2, 3, 4   # VFEM: NEXT-3
+OVX_INT8_DIRECT = 5   # NEXT-4: the direct N-stage FP64→INT8 conversion (Fig. 2 left)
 
 _c = ctypes
 _vp = _c.c_void_p
@@ -213,8 +214,10 @@ class Ovx:
         self._call("ovx_set_materials", len(r), _np_ptr(r), _np_ptr(k), _np_ptr(g))
 
     def set_element_materials(self, mat) -> None:
+        """Material id per element; a distributed rank > 0 passes the layer below its slab first."""
         m = _host(mat, np.uint8)
-        if m.size != self.n_elems:
+        halo = self.nx * self.ny if (self.world > 1 and self.rank > 0) else 0
+        if m.size != self.n_elems + halo:
             raise OvxError(OVX_EINVAL, "element material array size mismatch")
         self._call("ovx_set_element_materials", _np_ptr(m))
 

@@ -232,3 +232,29 @@ def test_power_iteration_critical_dt():
     lam = np.linalg.eigvalsh(K / np.sqrt(np.outer(md, md))).max()
     assert abs(dp / (2 / math.sqrt(lam)) - 1) < 1e-4
     assert dp > de
+
+
+def test_nccl_communicator_of_one():
+    """The library's NCCL plumbing on one GPU: libnccl.so.2 loads (dlopen, the copy torch uses if
+    already loaded), ovx_nccl_unique_id and ovx_create_dist (ncclCommInitRank) succeed for a world of
+    one, and the context then runs like a plain one (NCCL refuses two ranks on one device, so the
+    multi-rank exchange itself is covered by the loopback-group tests and the driver's multi-GPU runs)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2404_13683_b200 import ovx as O
+    uid = O.nccl_unique_id()
+    assert len(uid) == 128
+    s = O.Ovx.create_dist(0, 0, 1, uid)
+    m = wl.c1_cube(8, steps=10)
+    s.load_model(m, 0)
+    z = np.zeros(3 * m.n_nodes)
+    s.set_state(z, z, 0)
+    s.step(10)
+    u, _, _ = s.get_state()
+    r = O.Ovx(0)
+    r.load_model(m, 0)
+    r.set_state(z, z, 0)
+    r.step(10)
+    assert np.array_equal(u, r.get_state()[0])
+    s.close()

@@ -529,10 +529,13 @@ def test_full_size_c4_sampled(ovxmod, name, path):
     _sampled_apply_check(ovxmod, m, path, u, pts)
 
 
-def test_smem_a_variant_bit_exact(ovxmod):
-    """The alternate INT8 kernel (OVX_I8_KERNEL=smem: A operand in shared memory instead of TMEM),
-    selected once per process, in a subprocess: apply_K and a 30-step trajectory bit-exact vs the
-    oracle on the ragged multi-tile grid."""
+@pytest.mark.parametrize("variant", [{"OVX_I8_KERNEL": "smem"}, {"OVX_I8_KERNEL": "x", "OVX_I8X_LAYOUT": "word"},
+                                     {"OVX_I8_KERNEL": "x", "OVX_I8X_LAYOUT": "half"}])
+def test_alternate_int8_kernels_bit_exact(ovxmod, variant):
+    """The alternate INT8 kernels (selected once per process, so in a subprocess): step_i8w with the
+    A operand in shared memory, and step_i8x with the word (−K ⊗ I_4, no byte permutes) or half-word
+    operand layout: apply_K and a 30-step trajectory bit-exact vs the oracle's U2 mirror on the ragged
+    multi-tile grid (DESIGN.md §6.1 compares their speed)."""
     import os
     import subprocess
     import sys
@@ -556,7 +559,7 @@ r, rp, _, st = oracle.run(m.as_dict(), u, u, 0, 30, path=oracle.PATH_INT8, order
 assert st == 0 and np.array_equal(v, r) and np.array_equal(vp, rp)
 print('ok')
 """
-    env = dict(os.environ, OVX_I8_KERNEL="smem")
+    env = dict(os.environ, **variant)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
 
@@ -594,8 +597,8 @@ def _phase_fit(a, ns, th0):
     """θ minimising Σ (a_n − cos(n θ))² near θ0 (Gauss-Newton; the projection fit of SURVEY §8(d))."""
     th = th0
     for _ in range(20):
-        r = a - np.cos(ns * th)
-        J = ns * np.sin(ns * th)
+        r = a - np.cos(ns * th)               # residual of the model cos(n θ)
+        J = -ns * np.sin(ns * th)             # its derivative in θ
         th += float(J @ r) / float(J @ J)
     return th
 
@@ -615,8 +618,13 @@ def test_c2_oblique_bloch_modes(ovxmod, nu, mvec):
     k = np.array([math.pi * mv / (256 * m.ds) for mv in mvec])
     lam, U = physics.bloch_modes(m.kappa[0], m.G[0], m.rho[0], m.ds, k)
     s = _solver(ovxmod, m, 0)
-    for i in (2, 0):          # P-like (largest eigenvalue), S-like (smallest)
-        u0 = wl.standing_wave(m, mvec=mvec, U=tuple(U[:, i]))
+    # the P-like mode (largest eigenvalue) and the S-like mode with a non-zero roller-box field (for
+    # k_z = 0 a purely z-polarised mode vanishes identically: u_z ∝ sin(k_z z))
+    fields = {i: wl.standing_wave(m, mvec=mvec, U=tuple(U[:, i])) for i in range(3)}
+    s_mode = max((0, 1), key=lambda i: float(fields[i] @ fields[i]))
+    for i in (2, s_mode):
+        u0 = fields[i]
+        assert float(u0 @ u0) > 0
         th0 = math.acos(1 - lam[i] * m.dt ** 2 / 2)
         s.set_state(u0, math.cos(th0) * u0, 0)
         n0 = float(u0 @ u0)
@@ -700,3 +708,45 @@ def test_set_grid_resets_sources_and_negative_step_index_rejected(ovxmod):
     assert np.all(u == 0)                   # no stale point force from the first model
     with pytest.raises(ovxmod.OvxError):
         s.set_state(z, z, -1)
+
+
+def test_direct_n_stage_path_bit_exact(ovxmod):
+    """NEXT-4, the paper's DIRECT FP64→INT8 method (Fig. 2 left, Eqs. 11-14, a = 2^7, N = 8) on the
+    tensor cores (OVX_INT8_DIRECT): per-element records (v, the 8 signed digits per value, the
+    per-stage products C_j, y, f_e) bit-exact vs the oracle's direct variant; K u bit-exact vs its
+    U2 mirror; the results equal the hierarchical paper-digit path (same integer image, L146) and a
+    20-step trajectory equals the oracle's."""
+    m = wl.small_random(9, 5, 4, ds=0.01)
+    rng = np.random.default_rng(8)
+    u = wl.random_field(m) * 10.0 ** rng.uniform(-20, 5, size=3 * m.n_nodes)
+    u[::97] = 0.0
+    s = ovxmod.Ovx(0)
+    s.load_model(m, ovxmod.OVX_INT8_DIRECT)
+    rec = s.debug_element_ints(u, 0, m.n_elems)
+    for e in range(m.n_elems):
+        nodes = oracle.element_nodes(m.nx, m.ny, e)
+        ue = np.concatenate([u[3 * n:3 * n + 3] for n in nodes])
+        mm = m.mat[e]
+        r = oracle.element_int8(ue, m.kappa[mm], m.G[mm], m.ds, 8, oracle.DIGITS_DIRECT_FOLD)
+        assert rec["s"][e] == r["s"]
+        assert np.array_equal(rec["v"][e], r["v"])
+        assert np.array_equal(rec["d"][e][:8].astype(np.int8).astype(np.int32), r["d"])
+        assert np.array_equal(rec["C"][e].astype(np.int64), r["C"])
+        assert rec["y"][e] == r["y"]
+        assert np.array_equal(rec["fe"][e], r["fe"])
+    f = s.apply_K(u)
+    mirror = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=oracle.PATH_INT8,
+                            digits=oracle.DIGITS_DIRECT_FOLD, order=oracle.ORDER_U2)
+    paper = oracle.apply_K(m.nx, m.ny, m.nz, m.ds, m.mat, m.kappa, m.G, u, path=oracle.PATH_INT8,
+                           digits=oracle.DIGITS_PAPER | 2, order=oracle.ORDER_U2)
+    assert np.array_equal(f, mirror) and np.array_equal(mirror, paper)
+    mc = wl.c1_cube(8, steps=20)
+    z = np.zeros(3 * mc.n_nodes)
+    sd = ovxmod.Ovx(0)
+    sd.load_model(mc, ovxmod.OVX_INT8_DIRECT)
+    sd.set_state(z, z, 0)
+    sd.step(20)
+    ud, upd, _ = sd.get_state()
+    ru, rup, _, st = oracle.run(mc.as_dict(), z, z, 0, 20, path=oracle.PATH_INT8, digits=oracle.DIGITS_DIRECT_FOLD,
+                                order=oracle.ORDER_U2)
+    assert st == 0 and np.array_equal(ud, ru) and np.array_equal(upd, rup)

@@ -194,3 +194,55 @@ def test_fold_variant_matches_literal_to_fp64_precision_and_is_odd():
         assert np.abs(a["fe"] - b["fe"]).max() <= 2.0 ** -48 * sc
         n = oracle.element_int8(-u, kappa, G, ds, 8, oracle.DIGITS_BYTES_FOLD)
         assert np.array_equal(a["fe"], -n["fe"])
+
+
+def _elem_with_max(xmax_component):
+    """An element vector whose scaled image has a chosen first component (the max is 1)."""
+    ue = np.zeros(24)
+    ue[0] = 1.0
+    ue[1] = xmax_component
+    return ue
+
+
+@pytest.mark.parametrize("M", [4, 6, 8])
+def test_direct_n_stage_conversion_equals_hierarchical(M):
+    """NEXT-4, Fig. 2 left (Eqs. 11-14, a = 2^7, N = M): converting the FP64 remainder to INT8
+    at every stage gives the same integer image v = Σ_i a^{N-i} d_i as the hierarchical FP64→INT64→INT8
+    path (one conversion, then 7-bit slices), hence the same y and element force — the paper's
+    "the total computation accuracy is the same when N = M" (L146).  Random and adversarial inputs."""
+    rng = np.random.default_rng(40 + M)
+    for trial in range(300):
+        ue = rng.standard_normal(24) * 10.0 ** rng.uniform(-8, 8)
+        if trial % 5 == 0:
+            ue = np.sign(ue) * 3.0                       # every component at ±max: the clamp is active
+        if trial % 11 == 0:
+            ue[rng.integers(0, 24)] = 0.0
+        for fold in (0, 2):
+            a = oracle.element_int8(ue, 1.7, 1.1, 0.01, M, oracle.DIGITS_DIRECT | fold)
+            b = oracle.element_int8(ue, 1.7, 1.1, 0.01, M, oracle.DIGITS_PAPER | fold)
+            assert np.array_equal(a["v"], b["v"]), trial
+            assert a["y"] == b["y"] and np.array_equal(a["fe"], b["fe"]), trial
+            d = a["d"]
+            assert d.shape == (M, 48) and np.abs(d).max() <= 127
+            recon = sum((128 ** j) * d[j].astype(object) for j in range(M))   # lowest weight first
+            assert list(recon) == [int(x) for x in a["v"]]
+
+
+def test_direct_digits_worked_examples():
+    """Hand-derived digit sequences of the direct recursion d_i = INT(a r_{i-1}), r_i = a r_{i-1} − d_i:
+    x = 0.75 → (96, 0, …); x = −0.75 → (−96, 0, …); x = 1 (the max component) → 127 at every stage
+    (= 2^56 − 1, reading Q9); x = fl(1/3) → the base-128 digits of ⌊2^56·fl(1/3)⌋ (exact rationals):
+    42, 85, 42, 85, … ending in 84 because fl(1/3) < 1/3."""
+    K = dict(kappa=1.7, G=1.1, ds=0.01)
+    r = oracle.element_int8(_elem_with_max(0.75), K["kappa"], K["G"], K["ds"], 8, oracle.DIGITS_DIRECT)
+    d = r["d"][::-1]                                  # highest weight first: d_1 .. d_8
+    assert list(d[:, 1]) == [96, 0, 0, 0, 0, 0, 0, 0]
+    assert list(d[:, 0]) == [127] * 8 and int(r["v"][0]) == 2 ** 56 - 1
+    r = oracle.element_int8(_elem_with_max(1.0 / 3.0), K["kappa"], K["G"], K["ds"], 8, oracle.DIGITS_DIRECT)
+    d = r["d"][::-1]
+    from fractions import Fraction
+    V = int(Fraction(1.0 / 3.0) * 2 ** 56)        # the FP64 value of 1/3 is slightly below 1/3
+    assert list(d[:, 1]) == [(V >> (7 * (7 - i))) & 127 for i in range(8)] == [42, 85, 42, 85, 42, 85, 42, 84]
+    r = oracle.element_int8(-_elem_with_max(0.75), K["kappa"], K["G"], K["ds"], 8, oracle.DIGITS_DIRECT)
+    d = r["d"][::-1]
+    assert list(d[:, 1]) == [-96, 0, 0, 0, 0, 0, 0, 0] and list(d[:, 0]) == [-127] * 8

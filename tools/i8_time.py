@@ -14,12 +14,12 @@ m, u0 = bench._workload(256)
 s = Ovx(0)
 st = torch.cuda.current_stream()
 s.set_stream(st)
-s.load_model(m, OVX_INT8, stages=int(os.environ.get("OVX_STAGES", "8")))
+s.load_model(m, int(os.environ.get("OVX_PATH", OVX_INT8)), stages=int(os.environ.get("OVX_STAGES", "8")))
 s.set_state(u0, u0, 0)
 s.step(5)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(st); s.step(40); e1.record(st); torch.cuda.synchronize()
-env = {k: os.environ[k] for k in ("OVX_I8_KERNEL", "OVX_I8X_LAYOUT", "OVX_ZCHUNKS", "OVX_STAGES", "OVX_LIB_PATH")
+env = {k: os.environ[k] for k in ("OVX_I8_KERNEL", "OVX_I8X_LAYOUT", "OVX_ZCHUNKS", "OVX_STAGES", "OVX_LIB_PATH", "OVX_PATH")
        if k in os.environ}
 print(json.dumps({"env": env, "ms_per_step": e0.elapsed_time(e1) / 40}))
