@@ -199,8 +199,6 @@ __device__ __forceinline__ void element_force_vfem_wht(const double (&ue)[24], c
     }
 }
 
-// multiplier of the limb's high pair, read from constant memory so ptxas keeps one wide multiply-add
-__constant__ int32_t c_two16 = 65536;
 // Biased stage products (INT8 kernel): the A operand's K-padding bytes are 255 and the matching B
 // entries 127 (16 bytes per row), so every accumulator D_j = −C_j + I8_BIAS with I8_BIAS =
 // 16·255·127 = 518160 > max|C_j| = 255·1258 = 320790 (max absolute row sum of K_D): all D_j > 0.
@@ -210,10 +208,13 @@ __constant__ int32_t c_two16 = 65536;
 constexpr int32_t I8_BIAS = 16 * 255 * 127;
 constexpr double I8_LIMB_MAGIC = 0x1.8p52 + (double)I8_BIAS * 16843009.0;
 __device__ __forceinline__ double limb_biased(int32_t d0, int32_t d1, int32_t d2, int32_t d3) {
+    // L = p0 + 2^16·p1 < 2^44 assembled under the magic exponent as two 32-bit words: the low word
+    // with carry-out, the high word (p1 >> 16) + carry + 0x43380000 (no 64-bit multiply-add)
     const uint32_t p0 = (uint32_t)(d0 + 256 * d1), p1 = (uint32_t)(d2 + 256 * d3);
-    unsigned long long acc = 0x4338000000000000ull + p0;
-    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(p1), "r"(c_two16));
-    return __longlong_as_double((long long)acc) - I8_LIMB_MAGIC;
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0x43380000;" : "=r"(lo), "=r"(hi) : "r"(p0), "r"(p1 << 16),
+        "r"(p1 >> 16));
+    return __hiloint2double((int)hi, (int)lo) - I8_LIMB_MAGIC;
 }
 // The same for the direct N-stage path (DIR): stages in base 2^7, D_j = −C_j + B (B = 16·127·127,
 // s8 digits): L = p0 + 2^14·p1 (p0 = D0 + 128·D1, p1 = D2 + 128·D3 < 2^26), L < 2^41, assembled as

@@ -525,15 +525,11 @@ __global__ void __launch_bounds__(G::NT, G::CPS) step_i8w(const StepParams p) {
         // s_e from the per-node maxima of the two planes
         const unsigned long long *m0 = S.nmax[sL], *m1 = S.nmax[sL1];
         const int n0 = ly * PX + lx;
-        unsigned long long ab = m0[n0];
-        ab = max(ab, m0[n0 + 1]);
-        ab = max(ab, m0[n0 + PX]);
-        ab = max(ab, m0[n0 + PX + 1]);
-        ab = max(ab, m1[n0]);
-        ab = max(ab, m1[n0 + 1]);
-        ab = max(ab, m1[n0 + PX]);
-        ab = max(ab, m1[n0 + PX + 1]);
-        const double amax = __longlong_as_double((long long)ab);
+        // the node maxima are |u| bit patterns of finite values: as doubles, one DMNMX per pair (a
+        // balanced tree) instead of a 64-bit integer compare-and-select
+        auto dv = [](unsigned long long b) { return __longlong_as_double((long long)b); };
+        const double amax = fmax(fmax(fmax(dv(m0[n0]), dv(m0[n0 + 1])), fmax(dv(m0[n0 + PX]), dv(m0[n0 + PX + 1]))),
+                                 fmax(fmax(dv(m1[n0]), dv(m1[n0 + 1])), fmax(dv(m1[n0 + PX]), dv(m1[n0 + PX + 1]))));
         const int mcur = S.mid[sL][elem];
         const double cG = S.mc[mcur].x;
         const double s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)

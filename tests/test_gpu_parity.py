@@ -750,3 +750,41 @@ def test_direct_n_stage_path_bit_exact(ovxmod):
     ru, rup, _, st = oracle.run(mc.as_dict(), z, z, 0, 20, path=oracle.PATH_INT8, digits=oracle.DIGITS_DIRECT_FOLD,
                                 order=oracle.ORDER_U2)
     assert st == 0 and np.array_equal(ud, ru) and np.array_equal(upd, rup)
+
+
+def test_c3_scaled_1000_steps_vs_oracle(ovxmod):
+    """BASELINE config 3 (two-layer soil over bedrock, Ricker source at the top centre, 4 bottom
+    corners fixed) scaled to 64³ so that the oracle finishes: 1000 steps of the INT8 path within
+    1e-10 rel-L2 of the FP64 oracle's definition (the north-star bar), the factored FP64 path too."""
+    m = wl.c3_two_layer(64, steps=1000)
+    z = np.zeros(3 * m.n_nodes)
+    ref, _, _, st = oracle.run(m.as_dict(), z, z, 0, 1000, path=oracle.PATH_FP64)
+    assert st == 0 and np.abs(ref).max() > 0
+    for path in (0, 1):
+        s = _solver(ovxmod, m, path)
+        assert m.dt < s.critical_dt()
+        s.set_state(z, z, 0)
+        s.step(1000)
+        u, _, _ = s.get_state(with_prev=False)
+        assert np.linalg.norm(u - ref) <= 1e-10 * np.linalg.norm(ref), path
+
+
+def test_c3_full_size_10_steps_int8_vs_fp64(ovxmod):
+    """BASELINE config 3 at full size (512³, 1.35e8 elements, the bench launch): 10 steps from a
+    random field, the INT8 path within 1e-12 rel-L2 of the factored FP64 path (which is itself
+    compared with the oracle at this size node by node in test_full_size_c3_sampled)."""
+    import torch
+    m = wl.c3_two_layer(512, steps=10)
+    rng = np.random.default_rng(3)
+    u0 = torch.from_numpy(rng.standard_normal(3 * m.n_nodes) * 1e-3).cuda()
+    out = {}
+    for path in (0, 1):
+        s = _solver(ovxmod, m, path)
+        s.set_state_device(u0, u0, 0)
+        s.step(10)
+        u = torch.empty_like(u0)
+        up = torch.empty_like(u0)
+        s.get_state_device(u, up)
+        out[path] = u
+        del s
+    assert float(torch.linalg.norm(out[0] - out[1]) / torch.linalg.norm(out[1])) <= 1e-12
