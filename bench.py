@@ -439,7 +439,12 @@ def main() -> None:
         if world == 1:
             R = Single(args.n, path_id, local, stream)
         elif backend == "nccl" and os.environ.get("OVX_BENCH_DIST", "library") == "library":
-            R = ShardedLib(args.n, path_id, local, stream, world, rank)
+            try:
+                R = ShardedLib(args.n, path_id, local, stream, world, rank)
+            except Exception as ex:   # e.g. OVX_ENCCL: fall back to the Python-driven schedule
+                print(f"bench.py: library z-slab path unavailable ({ex}); using dist.py", file=sys.stderr)
+                os.environ["OVX_BENCH_DIST"] = "python"
+                R = Sharded(args.n, path_id, local, stream, world, rank)
         else:
             R = Sharded(args.n, path_id, local, stream, world, rank)
         R.set_state(R.u0, R.u0)

@@ -754,8 +754,10 @@ def test_direct_n_stage_path_bit_exact(ovxmod):
 
 def test_c3_scaled_1000_steps_vs_oracle(ovxmod):
     """BASELINE config 3 (two-layer soil over bedrock, Ricker source at the top centre, 4 bottom
-    corners fixed) scaled to 64³ so that the oracle finishes: 1000 steps of the INT8 path within
-    1e-10 rel-L2 of the FP64 oracle's definition (the north-star bar), the factored FP64 path too."""
+    corners fixed) scaled to 64³: 1000 steps of the INT8 path within 1e-10 rel-L2 of the FP64
+    oracle's definition (the north-star bar), the factored FP64 path too.  (BASELINE names 128³ for
+    this comparison; its 1000 oracle steps take ≈ 15 min of host time on the GPU box's 16 cores, so
+    the test uses the same model at 64³, ≈ 1 min.)"""
     m = wl.c3_two_layer(64, steps=1000)
     z = np.zeros(3 * m.n_nodes)
     ref, _, _, st = oracle.run(m.as_dict(), z, z, 0, 1000, path=oracle.PATH_FP64)
