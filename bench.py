@@ -560,6 +560,20 @@ def main() -> None:
                    "warp_instructions": g("smsp__inst_executed.sum")}
         except Exception:
             ncu = None
+    # the issue-slot roofline of the same kernel (the INT8 path is CUDA-core issue bound, DESIGN.md
+    # §6.1): warp-instructions per launch (the committed ncu capture of this launch configuration)
+    # over the live kernel time, against 4 warp-instructions per clock per SM at the max SM clock
+    issue_roof = None
+    if ncu and ncu.get("warp_instructions") and kernel_ms:
+        mhz = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
+        import torch as _t
+        sms = _t.cuda.get_device_properties(local).multi_processor_count
+        peak = 4.0 * sms * mhz * 1e6
+        ach = ncu["warp_instructions"] / (kernel_ms / 1e3)
+        issue_roof = {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-instructions/s",
+                      "frac": ach / peak, "instructions_src": ncu["source"],
+                      "note": "secondary: the HBM roofline above is the SURVEY §8(d) binding one"}
     nodes_total = (args.n + 1) ** 2 * (args.n * world + 1)
     out = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
@@ -582,6 +596,7 @@ def main() -> None:
                    "l2": "inputs larger than L2 (%.2f GB touched per step per GPU)" % (_algorithmic_bytes(R_nn, R_ne) / 1e9)},
         "dof_steps_per_s": 3 * nodes_total * args.steps / (ms / 1e3),
         "roofline": roof,
+        "roofline_issue": issue_roof,
         "int8_tops_useful": (18432 * R_ne / (kernel_ms / 1e3) / 1e12) if (path == OVX_INT8 and kernel_ms) else None,
         "int8_tops_issued": (issued_ops / (kernel_ms / 1e3) / 1e12) if (issued_ops and kernel_ms) else None,
         # BASELINE "INT8 tensor-pipe % peak": useful INT8 MACs×2 per second over the INT8 dense peak

@@ -66,6 +66,7 @@ struct ovx_ctx {
     cudaStream_t s_hi = nullptr;          // high-priority stream: edge chunks, exchange, interface update
     std::vector<cudaEvent_t> ev_pool;     // per-step phase events
     std::vector<std::array<cudaEvent_t, 4>> ph_used;   // (start, kernels done, halo done, end) per step
+    double ph_ebe_ms = 0.0, ph_halo_ms = 0.0;           // folded-in totals of recycled phase events
     int64_t nn2() const { return (nx + 1) * (ny + 1); }
     int64_t nn() const { return (nx + 1) * (ny + 1) * (nz + 1); }
     int64_t ne() const { return nx * ny * nz; }
@@ -848,7 +849,6 @@ ovx_status ovx_check_finite(ovx_ctx *ctx) {
 }
 
 static ovx_status apply_impl(ovx_ctx *ctx, const double *u_dev, double *f_dev) {
-    ovx_status s = OVX_OK;
     StepParams p = base_params(ctx);
     p.u = u_dev;
     p.fout = f_dev;
@@ -1098,6 +1098,21 @@ ovx_status dist_phase_iface(ovx_ctx *ctx) {
     return OVX_OK;
 }
 // the context stream waits for s_hi; installs the top plane; swap
+// accumulate the recorded phase times into the running totals and recycle the events
+ovx_status fold_phase_events(ovx_ctx *ctx) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (auto &ev : ctx->ph_used) {
+        float t01 = 0.f, t12 = 0.f;
+        CK(cudaEventElapsedTime(&t01, ev[0], ev[1]));   // step start -> edge chunks done
+        CK(cudaEventElapsedTime(&t12, ev[1], ev[2]));   // edge chunks done -> exchanges + interface done
+        ctx->ph_ebe_ms += t01;
+        ctx->ph_halo_ms += t12;
+        for (auto e : ev) ctx->ev_pool.push_back(e);
+    }
+    ctx->ph_used.clear();
+    return OVX_OK;
+}
+
 ovx_status dist_phase_end(ovx_ctx *ctx, std::array<cudaEvent_t, 4> &ev) {
     CK(cudaEventRecord(ev[2], ctx->s_hi));
     CK(cudaStreamWaitEvent(ctx->stream, ev[2], 0));
@@ -1105,6 +1120,7 @@ ovx_status dist_phase_end(ovx_ctx *ctx, std::array<cudaEvent_t, 4> &ev) {
     if (s) return s;
     CK(cudaEventRecord(ev[3], ctx->stream));
     ctx->ph_used.push_back(ev);
+    if (ctx->ph_used.size() >= 4096) return fold_phase_events(ctx);   // bounded event use on long runs
     return OVX_OK;
 }
 
@@ -1212,7 +1228,8 @@ ovx_status ovx_create_group(int world, const int *devices, ovx_ctx **out) {
         ovx_ctx *c = nullptr;
         ovx_status s = ovx_create(devices[r], &c);
         if (s) {
-            for (int q = 0; q < r; ++q) ovx_destroy(out[q]);
+            for (int q = 0; q < r; ++q) ovx_destroy(out[q]);   // the last destroy frees the group
+            if (r == 0) delete g;
             return s;
         }
         c->rank = r;
@@ -1277,8 +1294,8 @@ ovx_status ovx_step_group(ovx_ctx **ranks, int world, int64_t n) {
         for (int r = 0; r < world; ++r) {
             ovx_ctx *ctx = ranks[r];
             cudaSetDevice(ctx->device);
-            if (r > 0) CK(cudaStreamWaitEvent(ctx->stream, ranks[r - 1]->ph_used.back()[2], 0));
-            if (r + 1 < world) CK(cudaStreamWaitEvent(ctx->stream, ranks[r + 1]->ph_used.back()[2], 0));
+            if (r > 0) CK(cudaStreamWaitEvent(ctx->stream, ev[r - 1][2], 0));
+            if (r + 1 < world) CK(cudaStreamWaitEvent(ctx->stream, ev[r + 1][2], 0));
         }
     }
     return OVX_OK;
@@ -1290,13 +1307,10 @@ ovx_status ovx_get_phase_timers(ovx_ctx *ctx, double *ms_ebe, double *ms_halo, d
     CK(cudaStreamSynchronize(ctx->stream));
     double a = 0.0, b = 0.0;
     if (ctx->world > 1) {
-        for (auto &ev : ctx->ph_used) {
-            float t01 = 0.f, t12 = 0.f;
-            CK(cudaEventElapsedTime(&t01, ev[0], ev[1]));   // step start -> edge chunks done
-            CK(cudaEventElapsedTime(&t12, ev[1], ev[2]));   // edge chunks done -> exchanges + interface done
-            a += t01;
-            b += t12;
-        }
+        ovx_status s = fold_phase_events(ctx);
+        if (s) return s;
+        a = ctx->ph_ebe_ms;
+        b = ctx->ph_halo_ms;
     } else {
         for (auto &p : ctx->ev_used) {
             float ms = 0.f;
@@ -1308,9 +1322,9 @@ ovx_status ovx_get_phase_timers(ovx_ctx *ctx, double *ms_ebe, double *ms_halo, d
     if (ms_halo) *ms_halo = b;
     if (ms_update) *ms_update = 0.0;   // the update is fused into the EBE kernels
     if (reset) {
-        for (auto &ev : ctx->ph_used)
-            for (auto e : ev) ctx->ev_pool.push_back(e);
-        ctx->ph_used.clear();
+        ctx->ph_ebe_ms = ctx->ph_halo_ms = 0.0;
+        for (auto &p : ctx->ev_used) ctx->ev_free.push_back(p);
+        ctx->ev_used.clear();
     }
     return OVX_OK;
 }
