@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libovx.so")
 SOURCES = ["kernels.cu", "capi.cu", "element_setup.cpp"]
-HEADERS = ["ptx.cuh", "ovx_internal.h", "step_v1.cuh", "step_f64.cuh", "step_i8w.cuh", "step_i8x.cuh"]
+HEADERS = ["ptx.cuh", "ovx_internal.h", "step_v1.cuh", "step_f64.cuh", "step_i8w.cuh", "step_i8x.cuh", "step_i8ws.cuh"]
 
 
 def nvcc() -> str:

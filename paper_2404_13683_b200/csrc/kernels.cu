@@ -239,6 +239,7 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 
 #include "step_i8w.cuh"
 #include "step_i8x.cuh"
+#include "step_i8ws.cuh"
 
 // cudaFuncSetAttribute state is per device: remember it per device index
 inline bool attr_done(unsigned &mask) {
@@ -277,9 +278,25 @@ int i8_variant() {
         const char *e = std::getenv("OVX_I8_KERNEL");
         if (e && std::strcmp(e, "smem") == 0) return 1;
         if (e && std::strcmp(e, "x") == 0) return 2;
+        if (e && std::strcmp(e, "ws") == 0) return 3;
         return 0;
     }();
     return v;
+}
+
+template <int MODE, bool SLAB>
+cudaError_t launch_i8ws(const StepParams &p, int64_t ctas, cudaStream_t st) {
+    const int smem = (int)sizeof(SmemWS);
+    static unsigned attr = 0;
+    if (!attr_done(attr)) {
+        cudaError_t e = cudaFuncSetAttribute(step_i8ws<MODE, SLAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(step_i8ws<MODE, SLAB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+        attr_set(attr);
+    }
+    step_i8ws<MODE, SLAB><<<(unsigned)ctas, 512, smem, st>>>(p);
+    return cudaGetLastError();
 }
 
 // step_i8x operand layout (OVX_I8X_LAYOUT): "word" (default, B = −K_D ⊗ I_4) or "half" (⊗ I_2)
@@ -339,6 +356,12 @@ cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStre
         return cudaErrorInvalidValue;
     }
     const int v = i8_variant();
+    if constexpr (M == 8)
+        if (v == 3 && mode != MODE_DEBUG && !p.damped) {   // warp-specialised kernel (M = 8, undamped)
+            if (mode == MODE_STEP)
+                return p.slab_flags ? launch_i8ws<MODE_STEP, true>(p, ctas, st) : launch_i8ws<MODE_STEP, false>(p, ctas, st);
+            return p.slab_flags ? launch_i8ws<MODE_APPLY, true>(p, ctas, st) : launch_i8ws<MODE_APPLY, false>(p, ctas, st);
+        }
     if (v == 2 && mode != MODE_DEBUG)
         return p.slab_flags ? launch_i8x_mode<M, true>(mode, p, ctas, st) : launch_i8x_mode<M, false>(mode, p, ctas, st);
     return v == 1 ? launch_i8_mode_g<M, I8W, false>(mode, p, ctas, st)
@@ -479,7 +502,7 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
         const int zc = choose_zchunk(nz + 1, tx * ty, cps);
         li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
         li.threads = I8W::NT;
-        li.smem = i8_variant() == 2 ? (int)sizeof(SmemI8X)
+        li.smem = i8_variant() == 3 ? (int)sizeof(SmemWS) : i8_variant() == 2 ? (int)sizeof(SmemI8X)
                   : i8_variant() == 0 ? (int)sizeof(SmemI8<I8W, true>) : (int)sizeof(SmemI8<I8W, false>);
         return li;
     }

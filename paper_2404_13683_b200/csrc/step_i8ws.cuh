@@ -1,0 +1,444 @@
+// step_i8ws.cuh — warp-specialised INT8 time step (OVX_INT8, OVX_I8_KERNEL=ws); included by
+// kernels.cu after step_i8w.cuh (whose B-operand image, TMEM layout and limb it shares).
+//
+// Same arithmetic, tile, TMEM layout and node-sum order as step_i8w (bit-identical results), with
+// every warp in ONE role for the whole kernel instead of alternating roles each half-iteration:
+//   warps 0-3  converters of M-tile 0 (element rows 0-3; one thread per element: s_e, the 48 scaled
+//              F2I conversions, byte packing, the A operand to TMEM), warp 0 issues its MMAs;
+//   warps 4-7  converters of M-tile 1 (rows 4-7), warp 4 issues;
+//   warps 8-11 / 12-15  epilogues of M-tiles 0 / 1 (one thread per element: all 24 outputs from
+//              TMEM, exact limbs, the face sums in the order of reading U2, the update of the
+//              element's (−x,−y) node), and the plane loads (cp.async) for both roles.
+// Hand-offs are mbarriers (plane ready, MMA complete, D free, the row-3 → row-4 face-sum exchange
+// across M-tiles) and one named barrier per role group; the element scale α travels with the A
+// operand through TMEM (spare columns 496-503: per M-tile, by layer parity), so it is ordered like D.  The
+// converters run up to two layers ahead of the epilogues.  The two M-tiles share the TMEM A operand (their MMAs alternate),
+// as in step_i8w.  Undamped time steps and products only (damped steps and the debug records use
+// step_i8w).
+
+namespace ws {
+constexpr int NP = 7;                          // plane ring (the converters load 3-4 planes ahead)
+constexpr int NYS = 4;                         // face-sum exchange ring (layers)
+}  // namespace ws
+
+struct PlaneWS {
+    double up[3][I8W::NODES];                  // node values, component-major
+    unsigned long long nmax[I8W::NODES];       // max_c |u_c| per node (bit patterns)
+    uint8_t mid[I8W::NE];                      // material id of each tile element (layer of this plane)
+};
+struct SmemWS {
+    alignas(128) uint8_t B[6 * B1_PITCH];
+    alignas(128) uint8_t BI[2][6 * BI_PITCH];
+    PlaneWS pl[ws::NP];
+    double ys[ws::NYS][2][3][I8W::EY][I8W::EX];   // [layer slot][face b/t][c][row][lx]: x-pair P' of the +y corners
+    double2 mc[kMaxMat];
+    uint64_t plane_full[ws::NP];               // the 256 converter threads arrive
+    uint64_t a_free[2][5];                     // tcgen05.commit after each MMA K-step group; [m][4] = all done
+    uint64_t d_free[2];                        // the 128 epilogue threads of the M-tile arrive
+    uint64_t ys_ready[ws::NYS];                // the 32 threads of warp 11 (row 3) arrive
+    uint32_t tmem;
+};
+
+template <int MODE, bool SLAB>
+__global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
+    using C = I8W;
+    constexpr int EX = C::EX, PX = C::PX, NODES = C::NODES, NE = C::NE;
+    constexpr double ISCALE = 1.0 / (double)(1ull << 56);
+    constexpr double SCALE = (double)(1ull << 56);
+    constexpr unsigned long long AOFF = 1ull << 56;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    SmemWS &S = *reinterpret_cast<SmemWS *>(smem_raw);
+    const int t = threadIdx.x, lane = t & 31;
+    const int wu = __shfl_sync(0xffffffffu, t >> 5, 0);
+    const bool is_conv = wu < 8;
+    const int m = (wu >> 2) & 1;                 // M-tile
+    const int q = wu & 3;                        // TMEM lane quadrant = element row within the M-tile
+    const int lx = lane, ly = 4 * m + q;
+    const int elem = lx + EX * ly;
+
+    int bid = blockIdx.x;
+    const int tx = bid % p.tiles_x;
+    bid /= p.tiles_x;
+    const int ty = bid % p.tiles_y;
+    const int tz = p.tz0 + bid / p.tiles_y;
+    const int64_t X0 = (int64_t)tx * C::TX, Y0 = (int64_t)ty * C::TY;
+    const int Z0 = tz * p.zchunk;
+    const int nz = (int)p.nz;
+    const int Z1 = min(Z0 + p.zchunk, nz + 1);
+    const int64_t NX1 = p.nx + 1, NY1 = p.ny + 1;
+    const int64_t PSTRIDE = NX1 * NY1;
+    const int Lfirst = max(Z0 - 1, 0);
+    const int Lend = min(nz, Z1);                // element layers [Lfirst, Lend) are computed
+    const int Plast = min(Z1 - 1, nz);           // node planes completed by this CTA: [Z0, Plast]
+    const int64_t ex = X0 - 1 + lx, ey = Y0 - 1 + ly;
+    const bool ein = (ex >= 0 && ex < p.nx && ey >= 0 && ey < p.ny);
+    const int64_t mstride = p.nx * p.ny;
+    const bool tnode = lx >= 1 && ly >= 1;
+    const bool own = tnode && ex < NX1 && ey < NY1;
+    const int64_t ucol = own ? ex + NX1 * ey : 0;
+    auto slot = [](int z) { return (z + 3 * ws::NP) % ws::NP; };   // z >= -NP
+
+    // ---- one-time setup ----
+    for (int i = t; i < kBImgVec; i += 512) reinterpret_cast<uint4 *>(S.B)[i] = g_bimg[i];
+    if (wu == 0) ptx::tmem_alloc<512>(&S.tmem);
+    if (t == 0) {
+        for (int i = 0; i < ws::NP; ++i) ptx::mbar_init(&S.plane_full[i], 256);
+        for (int i = 0; i < 2; ++i) {
+            for (int g = 0; g < 5; ++g) ptx::mbar_init(&S.a_free[i][g], 1);
+            ptx::mbar_init(&S.d_free[i], 128);
+        }
+        for (int i = 0; i < ws::NYS; ++i) ptx::mbar_init(&S.ys_ready[i], 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = t; i < p.nmat + 1; i += 512) {
+        const int id = i < p.nmat ? i : kZeroMat;
+        S.mc[id] = make_double2(p.mc[id].cG, p.mc[id].c1);
+    }
+    // planes Lfirst .. Lfirst+2 and their materials, synchronously (every thread helps)
+    for (int j = 0; j < 3; ++j) {
+        const int iz = Lfirst + j;
+        PlaneWS &P = S.pl[slot(iz)];
+        for (int li = t; li < NODES; li += 512) {
+            const int lpx = li % PX, lpy = li / PX;
+            const int64_t gx = X0 - 1 + lpx, gy = Y0 - 1 + lpy;
+            const bool ok = gx >= 0 && gx < NX1 && gy >= 0 && gy < NY1 && iz <= nz;
+            unsigned long long mx = 0;
+            for (int c = 0; c < 3; ++c) {
+                const double v = ok ? __ldg(p.u + 3 * (PSTRIDE * iz + gx + NX1 * gy) + c) : 0.0;
+                P.up[c][li] = v;
+                const unsigned long long b = abs_bits(v);
+                mx = b > mx ? b : mx;
+            }
+            P.nmax[li] = mx;
+        }
+        if (t < NE) {
+            const int elx = t % EX, ely = t / EX;
+            const int64_t gex = X0 - 1 + elx, gey = Y0 - 1 + ely;
+            const bool ok = gex >= 0 && gex < p.nx && gey >= 0 && gey < p.ny && iz < nz;
+            P.mid[t] = (uint8_t)(ok ? (int)__ldg(p.mat + gex + p.nx * (gey + p.ny * (int64_t)iz)) : kZeroMat);
+        }
+    }
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (wu < 4) {   // K-padding chunk 6 of the TMEM A arrays: 255 bytes (bias source), written once
+#pragma unroll
+        for (int pa = 0; pa < 4; ++pa)
+            ptx::tmem_st4(S.tmem + ((uint32_t)(q * 32) << 16) + TA_A0 + pa * TA_A_ARR + 24, ~0u, ~0u, ~0u, ~0u);
+        ptx::tmem_st_wait();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = S.tmem;
+
+    if (is_conv) {
+        // ================================ converters ================================
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TA_A0;
+        const int n0 = ly * PX + lx;
+        const int ld = t;                            // loader index 0..255
+        // loader duties (converters; they run ahead of the epilogues): nodes ld, ld+256 of the 297 and
+        // element ld of each plane; plane z+3 is completed and z+4 issued after layer z's MMAs
+        const int nl = ld < NODES - 256 ? 2 : 1;
+        int64_t goff[2];
+        bool gok[2];
+        for (int j = 0; j < 2; ++j) {
+            const int li = ld + 256 * j;
+            const int lpx = li % PX, lpy = li / PX;
+            const int64_t gx = X0 - 1 + lpx, gy = Y0 - 1 + lpy;
+            gok[j] = j < nl && gx >= 0 && gx < NX1 && gy >= 0 && gy < NY1;
+            goff[j] = gok[j] ? 3 * (gx + NX1 * gy) : 0;
+        }
+        const int elx = ld % EX, ely = ld / EX;
+        const int64_t gex = X0 - 1 + elx, gey = Y0 - 1 + ely;
+        const bool mok = gex >= 0 && gex < p.nx && gey >= 0 && gey < p.ny;
+        const uint8_t *mptr = p.mat + (mok ? gex + p.nx * gey : 0);
+        int mid_next = (mok && Lfirst + 3 < nz) ? (int)__ldg(mptr + mstride * (int64_t)(Lfirst + 3)) : kZeroMat;
+        // issue the cp.async loads of plane z into its slot (zero-filled outside the grid or beyond nz)
+        auto issue_plane = [&](int z) {
+            PlaneWS &P = S.pl[slot(z)];
+            for (int j = 0; j < nl; ++j) {
+                const int li = ld + 256 * j;
+                const bool ok = gok[j] && z <= nz;
+                const double *src = p.u + (ok ? PSTRIDE * 3 * (int64_t)z + goff[j] : 0);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) ptx::cp_async8(&P.up[c][li], src + c, ok);
+            }
+            ptx::cp_async_commit();
+        };
+        // finish plane z (its cp.async group is the oldest outstanding one): node maxima, materials of
+        // layer z, arrival on the plane's mbarrier
+        auto finish_plane = [&](int z) {
+            ptx::cp_async_wait<0>();
+            PlaneWS &P = S.pl[slot(z)];
+            for (int j = 0; j < nl; ++j) {
+                const int li = ld + 256 * j;
+                unsigned long long mx = 0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const unsigned long long b = abs_bits(P.up[c][li]);
+                    mx = b > mx ? b : mx;
+                }
+                P.nmax[li] = mx;
+            }
+            P.mid[ld] = (uint8_t)mid_next;                           // layer z, loaded one iteration ago
+            mid_next = (mok && z + 1 < nz) ? (int)__ldg(mptr + mstride * (int64_t)(z + 1)) : kZeroMat;
+            ptx::mbar_arrive(&S.plane_full[slot(z)]);
+        };
+        if (Lfirst + 3 <= Lend) issue_plane(Lfirst + 3);
+        for (int L = Lfirst; L < Lend; ++L) {
+            const int k = L - Lfirst;
+            const int sL = slot(L), sL1 = slot(L + 1);
+            if (L + 1 >= Lfirst + 3)   // plane L+1 arrived asynchronously (its k-th use of the slot)
+                ptx::mbar_wait(&S.plane_full[sL1], (uint32_t)(((L + 1 - (Lfirst + 3)) / ws::NP) & 1));
+            const PlaneWS &P0 = S.pl[sL], &P1 = S.pl[sL1];
+            const unsigned long long *m0 = P0.nmax, *m1 = P1.nmax;
+            auto dv = [](unsigned long long b) { return __longlong_as_double((long long)b); };
+            const double amax = fmax(fmax(fmax(dv(m0[n0]), dv(m0[n0 + 1])), fmax(dv(m0[n0 + PX]), dv(m0[n0 + PX + 1]))),
+                                     fmax(fmax(dv(m1[n0]), dv(m1[n0 + 1])), fmax(dv(m1[n0 + PX]), dv(m1[n0 + PX + 1]))));
+            const int mcur = P0.mid[elem];
+            const double2 mcv = S.mc[mcur];
+            const double cG = mcv.x;
+            const double s = fmax(amax, __dmul_rn(cG, amax));   // max_i |RN(cG u_i)| = RN(cG max_i |u_i|)
+            const bool deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
+            const bool vzero = !ein || !(s >= 0x1p-1022);
+            const bool fast = (s <= 0x1.fffffffffffffp1023) && (vzero || s >= 0x1p-960);
+            const double alpha = deg ? 0.0 : -__dmul_rn(mcv.y, __dmul_rn(s, ISCALE));   // −RN(c1·RN(s·2^-56))
+            const double r = 1.0 / s;                                  // RN(1/s_e), reading Q7
+            const double R = vzero ? 0.0 : __dmul_rn(r, SCALE);
+            // the element's 24 node values (local node order of reading Q1; nodes 4-7 in plane L+1)
+            double ue[24];
+            {
+                constexpr int off[4] = {0, 1, PX + 1, PX};
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) ue[3 * a + c] = (a < 4 ? P0 : P1).up[c][n0 + off[a & 3]];
+            }
+            // the other M-tile's MMAs must have read the shared A operand (m 0: layer L-1 of tile 1;
+            // m 1: layer L of tile 0)
+            const bool need_free = (m == 1) || (k > 0);
+            const uint32_t fpar = (uint32_t)((m == 1 ? k : k - 1) & 1);
+            auto chunks = [&](auto fastc) {
+                constexpr bool FAST = decltype(fastc)::value;
+#pragma unroll
+                for (int ch = 0; ch < 6; ++ch) {            // chunk ch: values 8ch .. 8ch+7 (3-5: the G half)
+                    const bool gpart = ch >= 3;
+                    const int j0 = 8 * (gpart ? ch - 3 : ch);
+                    uint32_t lo[8], hi[8];
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq) {
+                        const double ub = gpart ? __dmul_rn(cG, ue[j0 + qq]) : ue[j0 + qq];
+                        long long v;
+                        if constexpr (FAST) v = __double2ll_rz(__dmul_rn(ub, R));
+                        else v = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), SCALE));
+                        lo[qq] = (uint32_t)(unsigned long long)v;
+                        hi[qq] = (uint32_t)((unsigned long long)v >> 32) + (uint32_t)(AOFF >> 32);
+                    }
+                    // the other M-tile's MMAs of the K-step group that last reads this chunk must be
+                    // complete (groups: ks0 = chunks 0-1, ks1 = 2-3, fold a = 3-4, ks2 = 4-5, fold b = 5-6)
+                    if (need_free && ch != 1) {
+                        constexpr int GRP[6] = {0, 0, 1, 2, 3, 4};
+                        ptx::mbar_wait(&S.a_free[1 - m][GRP[ch]], fpar);
+                        ptx::tc_fence_after();
+                    }
+                    if (ch == 0) {
+                        // α of this layer with the A operand: TMEM columns 496 + 4m + 2·(L&1) of this row
+                        // (the epilogue of layer L-2, the previous user, finished before these stores
+                        // could start: they wait for MMAs that waited for its D-free arrival)
+                        ptx::tmem_st2(ta - TA_A0 + 496 + 4 * m + 2 * (L & 1), (uint32_t)__double2loint(alpha),
+                                      (uint32_t)__double2hiint(alpha));
+                    }
+#pragma unroll
+                    for (int pa = 0; pa < 4; ++pa) {
+                        const uint32_t *src = pa < 2 ? lo : hi;
+                        const uint32_t sel = (pa & 1) ? 0x7632u : 0x5410u;
+                        ptx::tmem_st4(ta + pa * TA_A_ARR + 4 * ch, __byte_perm(src[0], src[1], sel),
+                                      __byte_perm(src[2], src[3], sel), __byte_perm(src[4], src[5], sel),
+                                      __byte_perm(src[6], src[7], sel));
+                    }
+                }
+            };
+            if (__all_sync(0xffffffffu, fast)) chunks(std::true_type{});
+            else chunks(std::false_type{});
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + m) : "memory");   // the 4 converter warps of this M-tile
+            if (q == 0) {
+                if (ptx::elect_one()) {
+                    if (k > 0) ptx::mbar_wait(&S.d_free[m], (uint32_t)((k - 1) & 1));   // layer L-1's D read
+                    ptx::tc_fence_after();
+                    const uint32_t b0 = ptx::smem_u32(&S.B[0]);
+                    const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
+                    // K-step groups in chunk order, all four arrays each, a commit after every group so
+                    // that the other M-tile can overwrite A chunk by chunk
+                    const uint32_t aoff[5] = {0, 8, 12, 16, 20};
+                    const uint64_t bdesc[5] = {ptx::smem_desc(b0, 128, B1_PITCH), ptx::smem_desc(b0 + 256, 128, B1_PITCH),
+                                               ptx::smem_desc(bi0, 128, BI_PITCH), ptx::smem_desc(b0 + 512, 128, B1_PITCH),
+                                               ptx::smem_desc(bi1, 128, BI_PITCH)};
+#pragma unroll
+                    for (int g = 0; g < 5; ++g) {
+#pragma unroll
+                        for (int pa = 0; pa < 4; ++pa)
+                            ptx::mma_i8_ts(tmem + m * TA_D_TILE + pa * TA_D_ARR, tmem + TA_A0 + pa * TA_A_ARR + aoff[g],
+                                           bdesc[g], IDESC, g > 0 ? 1u : 0u);
+                        ptx::mma_commit(&S.a_free[m][g]);
+                    }
+                }
+                __syncwarp();
+            }
+            // ---- loader duties: plane L+3 completed, plane L+4 issued (its slot, that of plane L-3, is
+            // no longer read: these threads' A stores waited for MMAs issued after the epilogues of
+            // layer L-2 read D, so both epilogues finished layer L-3) ----
+            if (L + 3 <= Lend) {
+                finish_plane(L + 3);
+                if (L + 4 <= Lend) issue_plane(L + 4);
+            }
+        }
+    } else {
+        // ================================ epilogues ================================
+        const uint32_t td = tmem + ((uint32_t)(q * 32) << 16) + m * TA_D_TILE;
+        const int n0 = ly * PX + lx;
+        bool has_src = false, has_rec = false;
+        if (MODE == MODE_STEP) {
+            for (int kk = 0; kk < p.nsrc; ++kk) {
+                const int64_t n = p.src_dof[kk] / 3;
+                const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+                has_src |= (ix >= X0 && ix < X0 + C::TX && iy >= Y0 && iy < Y0 + C::TY);
+            }
+            if (p.it >= 0 && p.it < p.rec_nt)
+                for (int kk = 0; kk < p.nrec; ++kk) {
+                    const int64_t n = p.rec_node[kk];
+                    const int64_t ix = n % NX1, iy = (n / NX1) % NY1;
+                    has_rec |= (ix >= X0 && ix < X0 + C::TX && iy >= Y0 && iy < Y0 + C::TY);
+                }
+        }
+
+        double T[3] = {0.0, 0.0, 0.0};               // top-face sum of the previous layer at this node
+        double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;
+        uint8_t dm = 0;
+        int64_t node_next = ucol + PSTRIDE * (int64_t)Lfirst;
+        auto prefetch_update = [&](int P) {
+            if (MODE == MODE_STEP && own && P >= Z0 && P <= Plast) {
+                const int64_t nd = ucol + PSTRIDE * (int64_t)P;
+                upv[0] = p.uo[3 * nd];
+                upv[1] = p.uo[3 * nd + 1];
+                upv[2] = p.uo[3 * nd + 2];
+                wn = __ldg(p.w + nd);
+                dm = p.dmask ? __ldg(p.dmask + nd) : (uint8_t)0;
+            }
+        };
+        (void)node_next;
+        prefetch_update(Lfirst);
+        for (int L = Lfirst; L <= Plast; ++L) {
+            const int k = L - Lfirst;
+            // ---- element forces of layer L (24 outputs) ----
+            double fb[12], ft[12];                   // bottom corners (local nodes 0-3), top (4-7): [corner][c]
+            const bool has_layer = L < Lend;
+            if (has_layer) {
+                ptx::mbar_wait_sleep(&S.a_free[m][4], (uint32_t)(k & 1));   // all MMAs of layer L
+                ptx::tc_fence_after();
+                uint32_t alo, ahi;
+                ptx::tmem_ld2(td - m * TA_D_TILE + 496 + 4 * m + 2 * (L & 1), alo, ahi);
+                ptx::tmem_ld_wait();
+                const double alpha = __hiloint2double((int)ahi, (int)alo);
+#pragma unroll
+                for (int rr = 0; rr < 6; ++rr) {     // outputs 4rr .. 4rr+3
+                    uint32_t R0[8], R1[8], R2[8], R3[8];
+                    ptx::tmem_ld8(td + 0 * TA_D_ARR + rr * 8, R0);
+                    ptx::tmem_ld8(td + 1 * TA_D_ARR + rr * 8, R1);
+                    ptx::tmem_ld8(td + 2 * TA_D_ARR + rr * 8, R2);
+                    ptx::tmem_ld8(td + 3 * TA_D_ARR + rr * 8, R3);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        const double dlo = limb_biased((int32_t)R0[2 * qq], (int32_t)R0[2 * qq + 1], (int32_t)R1[2 * qq],
+                                                       (int32_t)R1[2 * qq + 1]);
+                        const double dhi = limb_biased((int32_t)R2[2 * qq], (int32_t)R2[2 * qq + 1], (int32_t)R3[2 * qq],
+                                                       (int32_t)R3[2 * qq + 1]);
+                        const double f = __dmul_rn(alpha, __fma_rn(dhi, 0x1p32, dlo));   // RN(c1s·RN(y))
+                        const int j = 4 * rr + qq;
+                        if (j < 12) fb[j] = f;
+                        else ft[j - 12] = f;
+                    }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&S.d_free[m]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 12; ++j) fb[j] = ft[j] = 0.0;
+            }
+            // ---- node sums in the order of reading U2 ----
+            // x-pairs: P(iy) = own (-x,-y) corner + lane lx-1's (+x,-y) corner; P'(iy) of the +y corners
+            // goes to row ly+1 through shared memory
+            const int ysl = k % ws::NYS;
+            double Pb[3], Pt[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double pmb = __shfl_up_sync(0xffffffffu, fb[3 * 1 + c], 1);
+                const double ppb = __shfl_up_sync(0xffffffffu, fb[3 * 2 + c], 1);
+                const double pmt = __shfl_up_sync(0xffffffffu, ft[3 * 1 + c], 1);
+                const double ppt = __shfl_up_sync(0xffffffffu, ft[3 * 2 + c], 1);
+                Pb[c] = __dadd_rn(fb[3 * 0 + c], pmb);
+                Pt[c] = __dadd_rn(ft[3 * 0 + c], pmt);
+                S.ys[ysl][0][c][ly][lx] = __dadd_rn(fb[3 * 3 + c], ppb);
+                S.ys[ysl][1][c][ly][lx] = __dadd_rn(ft[3 * 3 + c], ppt);
+            }
+            if (m == 0 && q == 3) ptx::mbar_arrive(&S.ys_ready[ysl]);   // row 3 feeds row 4 of the other M-tile
+            asm volatile("bar.sync %0, 128;" ::"r"(3 + m) : "memory");   // the 4 epilogue warps of this M-tile
+            if (m == 1 && q == 0) ptx::mbar_wait(&S.ys_ready[ysl], (uint32_t)((k / ws::NYS) & 1));
+            if (tnode) {
+                double fbot[3], ftop[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    fbot[c] = has_layer ? __dadd_rn(Pb[c], S.ys[ysl][0][c][ly - 1][lx]) : 0.0;   // B of plane L
+                    ftop[c] = has_layer ? __dadd_rn(Pt[c], S.ys[ysl][1][c][ly - 1][lx]) : 0.0;   // T of plane L+1
+                }
+                const bool plane_done = L >= Z0;     // L <= Plast by the loop bound
+                if (own && plane_done) {
+                    const int64_t un_id = ucol + PSTRIDE * (int64_t)L;
+                    if (SLAB && (p.slab_flags & 1) && L == 0) {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) p.iface_bot_b[3 * ucol + c] = fbot[c];
+                    } else {
+                        double f[3];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) f[c] = __dadd_rn(T[c], fbot[c]);
+                        if (SLAB && (p.slab_flags & 2) && L == nz) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = f[c];
+                        } else if (MODE == MODE_STEP) {
+                            const PlaneWS &P = S.pl[slot(L)];
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) {
+                                double F = 0.0;
+                                if (has_src)
+                                    for (int kk = 0; kk < p.nsrc; ++kk)
+                                        if (p.src_dof[kk] == 3 * un_id + c) F = __dadd_rn(F, p.src_val[kk]);
+                                const double uc = P.up[c][n0];
+                                const double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
+                                double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
+                                if ((dm >> c) & 1) un = 0.0;
+                                p.uo[3 * un_id + c] = un;
+                                if (has_rec)
+                                    for (int kk = 0; kk < p.nrec; ++kk)
+                                        if (p.rec_node[kk] == un_id) p.traces[(3 * kk + c) * p.rec_nt + p.it] = un;
+                            }
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) p.fout[3 * un_id + c] = f[c];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 3; ++c) T[c] = ftop[c];
+            }
+            prefetch_update(L + 1);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (wu == 0) ptx::tmem_dealloc<512>(S.tmem);
+}
