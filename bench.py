@@ -542,7 +542,7 @@ def main() -> None:
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_src": pk["src"],
                 "bytes_per_launch": bytes_launch, "kernel_ms_per_launch": kernel_ms,
-                "kernel": {0: "step_i8w<M=8>", 1: "step_f64", 2: "step_v1<FP64_DENSE>", 3: "step_f64<VF>",
+                "kernel": {0: "step_i8ws<M=8> (warp-specialised)", 1: "step_f64", 2: "step_v1<FP64_DENSE>", 3: "step_f64<VF>",
                            4: "step_v1<FP64_DENSE> (VFEM matrices)"}[path]}
     # SURVEY §8(d)'s per-run ncu figures for the dominant kernel, from the committed capture of the
     # same command (profiles/; ncu numbers are never taken inside this timed run)

@@ -269,17 +269,18 @@ cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// INT8 kernel variant (OVX_I8_KERNEL): "tmem" (default) step_i8w with the A operand in TMEM;
-// "smem" step_i8w with A in shared memory; "x" step_i8x (time steps and products; word or half-word
-// operand layout, OVX_I8X_LAYOUT; the debug records always come from step_i8w).
-// has the measurements (the three are bit-identical).
+// INT8 kernel variant (OVX_I8_KERNEL): "ws" (default) step_i8ws, warp-specialised (undamped time
+// steps and products, M = 8; damped steps, M = 4 / 6 and the debug records use step_i8w); "tmem"
+// step_i8w with the A operand in TMEM (the round-1 kernel); "smem" step_i8w with A in shared memory;
+// "x" step_i8x (word or half-word operand layout, OVX_I8X_LAYOUT).  All bit-identical; DESIGN.md
+// §6.1 has the measurements.
 int i8_variant() {
     static const int v = [] {
         const char *e = std::getenv("OVX_I8_KERNEL");
         if (e && std::strcmp(e, "smem") == 0) return 1;
         if (e && std::strcmp(e, "x") == 0) return 2;
-        if (e && std::strcmp(e, "ws") == 0) return 3;
-        return 0;
+        if (e && std::strcmp(e, "tmem") == 0) return 0;
+        return 3;
     }();
     return v;
 }
