@@ -1,6 +1,9 @@
 // ptx.cuh — thin inline-PTX wrappers for sm_100a (tcgen05 / mbarrier / proxy fences).
 #pragma once
 #include <cstdint>
+#ifdef OVX_WATCHDOG
+#include <cstdio>
+#endif
 
 namespace ovx {
 namespace ptx {
@@ -13,6 +16,26 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+#ifdef OVX_WATCHDOG
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __noinline__ void mbar_report(uint64_t *bar, uint32_t parity, int line) {
+    printf("WATCHDOG block %d thread %d line %d bar_off %u parity %u state %llx\n", blockIdx.x, threadIdx.x, line,
+           smem_u32(bar), parity, (unsigned long long)*bar);
+    __trap();
+}
+__device__ __forceinline__ void mbar_wait_wd(uint64_t *bar, uint32_t parity, int line) {
+    uint32_t n = 0;
+    while (!mbar_try(bar, parity))
+        if (++n == (1u << 26)) mbar_report(bar, parity, line);
+}
+#define mbar_wait(b, p) mbar_wait_wd(b, p, __LINE__)
+#define mbar_wait_backoff(b, p) mbar_wait_wd(b, p, __LINE__)
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -22,6 +45,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#endif
 // Same, with a suspend-time hint: the warp sleeps in hardware until the phase completes (or the
 // hint expires) instead of spinning through issue slots.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
@@ -33,6 +57,30 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
         "r"(parity), "r"(0x989680u)
         : "memory");
 }
+
+// One non-blocking probe of the phase; true once it has completed.
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+#ifndef OVX_WATCHDOG
+// Wait with a sleeping back-off between probes (for waiters off the critical path: they give their
+// issue slots to the other warps of the SM sub-partition instead of spinning).
+#ifdef OVX_BACKOFF_SPIN
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
+#else
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
+    while (!mbar_test(bar, parity)) __nanosleep(64);
+}
+#endif
+#endif
 
 // Arrive on an mbarrier (release semantics at CTA scope).
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {

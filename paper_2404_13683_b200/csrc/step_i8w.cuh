@@ -24,7 +24,7 @@
 // Per-warp phase timeline (profiling builds only: -DOVX_TRACE, tools/trace_i8.py): clock64 stamps
 // of one CTA (block OVX_TRACE) over TRH half-iterations, TRN points each.
 #ifdef OVX_TRACE
-#define TRN 12
+#define TRN 16
 #define TRH 16
 __device__ unsigned long long g_tr[TRH * 16 * TRN];
 #define TR(pt) do { if (blockIdx.x == OVX_TRACE && lane == 1 && trh >= 0 && trh < TRH) \

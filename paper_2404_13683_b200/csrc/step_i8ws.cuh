@@ -16,6 +16,17 @@
 // as in step_i8w.  Undamped time steps and products only (damped steps and the debug records use
 // step_i8w).
 
+#ifdef OVX_TRACE   // per-warp clock64 stamps of one CTA (tools/trace_ws.py): layers TRK0 .. TRK0+TRH-1
+#define TRK0 20
+#define TRW(pt) do { if (blockIdx.x == OVX_TRACE && lane == 0 && k >= TRK0 && k < TRK0 + TRH) \
+                         g_tr[((k - TRK0) * 16 + wu) * TRN + (pt)] = clock64(); } while (0)
+#define TRI(pt) do { if (blockIdx.x == OVX_TRACE && k >= TRK0 && k < TRK0 + TRH) \
+                         g_tr[((k - TRK0) * 16 + wu) * TRN + (pt)] = clock64(); } while (0)
+#else
+#define TRW(pt) do { } while (0)
+#define TRI(pt) do { } while (0)
+#endif
+
 namespace ws {
 constexpr int NP = 7;                          // plane ring (the converters load 3-4 planes ahead)
 constexpr int NYS = 4;                         // face-sum exchange ring (layers)
@@ -189,9 +200,11 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
         if (Lfirst + 3 <= Lend) issue_plane(Lfirst + 3);
         for (int L = Lfirst; L < Lend; ++L) {
             const int k = L - Lfirst;
+            TRW(0);
             const int sL = slot(L), sL1 = slot(L + 1);
             if (L + 1 >= Lfirst + 3)   // plane L+1 arrived asynchronously (its k-th use of the slot)
                 ptx::mbar_wait(&S.plane_full[sL1], (uint32_t)(((L + 1 - (Lfirst + 3)) / ws::NP) & 1));
+            TRW(1);
             const PlaneWS &P0 = S.pl[sL], &P1 = S.pl[sL1];
             const unsigned long long *m0 = P0.nmax, *m1 = P1.nmax;
             auto dv = [](unsigned long long b) { return __longlong_as_double((long long)b); };
@@ -207,6 +220,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             const double alpha = deg ? 0.0 : -__dmul_rn(mcv.y, __dmul_rn(s, ISCALE));   // −RN(c1·RN(s·2^-56))
             const double r = 1.0 / s;                                  // RN(1/s_e), reading Q7
             const double R = vzero ? 0.0 : __dmul_rn(r, SCALE);
+            TRW(11);
             // the element's 24 node values (local node order of reading Q1; nodes 4-7 in plane L+1)
             double ue[24];
             {
@@ -260,14 +274,18 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                     }
                 }
             };
+            TRW(2);
             if (__all_sync(0xffffffffu, fast)) chunks(std::true_type{});
             else chunks(std::false_type{});
             ptx::tmem_st_wait();
+            TRW(3);
             ptx::tc_fence_before();
             asm volatile("bar.sync %0, 128;" ::"r"(1 + m) : "memory");   // the 4 converter warps of this M-tile
+            TRW(4);
             if (q == 0) {
                 if (ptx::elect_one()) {
                     if (k > 0) ptx::mbar_wait(&S.d_free[m], (uint32_t)((k - 1) & 1));   // layer L-1's D read
+                    TRI(5);
                     ptx::tc_fence_after();
                     const uint32_t b0 = ptx::smem_u32(&S.B[0]);
                     const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
@@ -285,6 +303,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                                            bdesc[g], IDESC, g > 0 ? 1u : 0u);
                         ptx::mma_commit(&S.a_free[m][g]);
                     }
+                    TRI(6);
                 }
                 __syncwarp();
             }
@@ -293,8 +312,10 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             // layer L-2 read D, so both epilogues finished layer L-3) ----
             if (L + 3 <= Lend) {
                 finish_plane(L + 3);
+                TRW(10);
                 if (L + 4 <= Lend) issue_plane(L + 4);
             }
+            TRW(9);
         }
     } else {
         // ================================ epilogues ================================
@@ -333,11 +354,13 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
         prefetch_update(Lfirst);
         for (int L = Lfirst; L <= Plast; ++L) {
             const int k = L - Lfirst;
+            TRW(0);
             // ---- element forces of layer L (24 outputs) ----
             double fb[12], ft[12];                   // bottom corners (local nodes 0-3), top (4-7): [corner][c]
             const bool has_layer = L < Lend;
             if (has_layer) {
                 ptx::mbar_wait_sleep(&S.a_free[m][4], (uint32_t)(k & 1));   // all MMAs of layer L
+                TRW(1);
                 ptx::tc_fence_after();
                 uint32_t alo, ahi;
                 ptx::tmem_ld2(td - m * TA_D_TILE + 496 + 4 * m + 2 * (L & 1), alo, ahi);
@@ -365,6 +388,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&S.d_free[m]);
+                TRW(2);
             } else {
 #pragma unroll
                 for (int j = 0; j < 12; ++j) fb[j] = ft[j] = 0.0;
@@ -388,6 +412,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             if (m == 0 && q == 3) ptx::mbar_arrive(&S.ys_ready[ysl]);   // row 3 feeds row 4 of the other M-tile
             asm volatile("bar.sync %0, 128;" ::"r"(3 + m) : "memory");   // the 4 epilogue warps of this M-tile
             if (m == 1 && q == 0) ptx::mbar_wait(&S.ys_ready[ysl], (uint32_t)((k / ws::NYS) & 1));
+            TRW(6);
             if (tnode) {
                 double fbot[3], ftop[3];
 #pragma unroll
@@ -434,6 +459,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c) T[c] = ftop[c];
             }
+            TRW(7);
             prefetch_update(L + 1);
         }
     }

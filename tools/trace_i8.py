@@ -19,10 +19,10 @@ s.load_model(m, OVX_INT8)
 s.set_state(u0, u0, 0)
 s.step(5)
 torch.cuda.synchronize()
-tr = np.zeros(16 * 16 * 12, dtype=np.uint64)
+tr = np.zeros(16 * 16 * 16, dtype=np.uint64)
 L = O.lib()
 L.ovx_trace_read(tr.ctypes.data_as(ctypes.c_void_p))
-tr = tr.reshape(16, 16, 12).astype(np.int64)
+tr = tr.reshape(16, 16, 16).astype(np.int64)
 t0 = tr[tr > 0].min()
 np.save("gpurun_out/trace_i8.npy", tr)
 for hh in range(16):
