@@ -285,19 +285,34 @@ int i8_variant() {
     return v;
 }
 
-template <int MODE, bool SLAB>
-cudaError_t launch_i8ws(const StepParams &p, int64_t ctas, cudaStream_t st) {
-    const int smem = (int)sizeof(SmemWS);
+// node planes of step_i8ws (OVX_I8_PLANES): "cp" (default) per-thread cp.async, "bulk" the bulk-copy
+// (TMA) engine, one copy per node row
+bool i8_bulk_planes() {
+    static const bool v = [] {
+        const char *e = std::getenv("OVX_I8_PLANES");
+        return e && std::strcmp(e, "bulk") == 0;
+    }();
+    return v;
+}
+
+template <int MODE, bool SLAB, bool BULK>
+cudaError_t launch_i8ws_b(const StepParams &p, int64_t ctas, cudaStream_t st) {
+    const int smem = (int)sizeof(SmemWST<BULK>);
     static unsigned attr = 0;
     if (!attr_done(attr)) {
-        cudaError_t e = cudaFuncSetAttribute(step_i8ws<MODE, SLAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e =
+            cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(step_i8ws<MODE, SLAB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        e = cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         attr_set(attr);
     }
-    step_i8ws<MODE, SLAB><<<(unsigned)ctas, 512, smem, st>>>(p);
+    step_i8ws<MODE, SLAB, BULK><<<(unsigned)ctas, 512, smem, st>>>(p);
     return cudaGetLastError();
+}
+template <int MODE, bool SLAB>
+cudaError_t launch_i8ws(const StepParams &p, int64_t ctas, cudaStream_t st) {
+    return i8_bulk_planes() ? launch_i8ws_b<MODE, SLAB, true>(p, ctas, st) : launch_i8ws_b<MODE, SLAB, false>(p, ctas, st);
 }
 
 // step_i8x operand layout (OVX_I8X_LAYOUT): "word" (default, B = −K_D ⊗ I_4) or "half" (⊗ I_2)
@@ -503,7 +518,7 @@ LaunchInfo step_launch_info(int path, int64_t nx, int64_t ny, int64_t nz) {
         const int zc = choose_zchunk(nz + 1, tx * ty, cps);
         li.ctas = tx * ty * ((nz + 1 + zc - 1) / zc);
         li.threads = I8W::NT;
-        li.smem = i8_variant() == 3 ? (int)sizeof(SmemWS) : i8_variant() == 2 ? (int)sizeof(SmemI8X)
+        li.smem = i8_variant() == 3 ? (i8_bulk_planes() ? (int)sizeof(SmemWST<true>) : (int)sizeof(SmemWS)) : i8_variant() == 2 ? (int)sizeof(SmemI8X)
                   : i8_variant() == 0 ? (int)sizeof(SmemI8<I8W, true>) : (int)sizeof(SmemI8<I8W, false>);
         return li;
     }

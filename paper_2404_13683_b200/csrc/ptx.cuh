@@ -87,6 +87,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// ---- bulk copies (the TMA engine, non-tensor form): global -> shared, completion counted in bytes
+// on an mbarrier.  Addresses and size: multiples of 16 B.
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem_dst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // ---- cp.async (global -> shared without a register round trip) --------------
 // 8 bytes; valid == false zero-fills the destination (src-size 0, the source is not read)
 __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc, bool valid) {
@@ -97,6 +109,11 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc, bool
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// Arrive on an mbarrier once all prior cp.async of this thread have landed (no pending-count
+// increment: the barrier's expected count includes these arrivals).
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 // One lane of a converged warp (elect.sync): keeps the tcgen05 issue code warp-uniform.
 __device__ __forceinline__ bool elect_one() {

@@ -32,33 +32,49 @@ constexpr int NP = 7;                          // plane ring (the converters loa
 constexpr int NYS = 4;                         // face-sum exchange ring (layers)
 }  // namespace ws
 
-struct PlaneWS {
+// node plane held in shared memory: component-major (cp.async loads, the default) or, with BULK
+// (OVX_I8_PLANES=bulk), the global node-major rows as the bulk-copy engine delivers them: row r of the
+// tile at byte 816·r + 8·s_r (s_r = the row's 16-byte phase in global memory, which alternates with the
+// plane parity when (nx+1)(ny+1) is odd), node x at +24·x, component c at +8·c
+template <bool BULK>
+struct PlaneT {
     double up[3][I8W::NODES];                  // node values, component-major
     unsigned long long nmax[I8W::NODES];       // max_c |u_c| per node (bit patterns)
     uint8_t mid[I8W::NE];                      // material id of each tile element (layer of this plane)
 };
-struct SmemWS {
+template <>
+struct PlaneT<true> {
+    alignas(16) double raw[I8W::PY][102];      // 9 rows × 816 B
+    unsigned long long nmax[I8W::NODES];
+    uint8_t mid[I8W::NE];
+};
+using PlaneWS = PlaneT<false>;
+template <bool BULK = false>
+struct SmemWST {
     alignas(128) uint8_t B[6 * B1_PITCH];
     alignas(128) uint8_t BI[2][6 * BI_PITCH];
-    PlaneWS pl[ws::NP];
+    PlaneT<BULK> pl[ws::NP];
     double ys[ws::NYS][2][3][I8W::EY][I8W::EX];   // [layer slot][face b/t][c][row][lx]: x-pair P' of the +y corners
     double2 mc[kMaxMat];
     uint64_t plane_full[ws::NP];               // the 256 converter threads arrive
     uint64_t a_free[2][5];                     // tcgen05.commit after each MMA K-step group; [m][4] = all done
     uint64_t d_free[2];                        // the 128 epilogue threads of the M-tile arrive
     uint64_t ys_ready[ws::NYS];                // the 32 threads of warp 11 (row 3) arrive
+    uint64_t plane_tx[ws::NP];                 // BULK: the 9 row copies of the plane landed (9 arrivals + bytes)
     uint32_t tmem;
 };
+using SmemWS = SmemWST<false>;
 
-template <int MODE, bool SLAB>
+template <int MODE, bool SLAB, bool BULK = false>
 __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
     using C = I8W;
-    constexpr int EX = C::EX, PX = C::PX, NODES = C::NODES, NE = C::NE;
+    constexpr int EX = C::EX, PX = C::PX, PY = C::PY, NODES = C::NODES, NE = C::NE;
     constexpr double ISCALE = 1.0 / (double)(1ull << 56);
     constexpr double SCALE = (double)(1ull << 56);
     constexpr unsigned long long AOFF = 1ull << 56;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    SmemWS &S = *reinterpret_cast<SmemWS *>(smem_raw);
+    SmemWST<BULK> &S = *reinterpret_cast<SmemWST<BULK> *>(smem_raw);
+    using Plane = PlaneT<BULK>;
     const int t = threadIdx.x, lane = t & 31;
     const int wu = __shfl_sync(0xffffffffu, t >> 5, 0);
     const bool is_conv = wu < 8;
@@ -88,12 +104,26 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
     const bool own = tnode && ex < NX1 && ey < NY1;
     const int64_t ucol = own ? ex + NX1 * ey : 0;
     auto slot = [](int z) { return (z + 3 * ws::NP) % ws::NP; };   // z >= -NP
+    // BULK: the row phase s = parity of the global node index of the row's x = -1 node in plane z
+    const int gx0 = (int)(X0 - 1);
+    auto rowpar = [&](int r) { return (int)((gx0 + NX1 * (Y0 - 1 + r)) & 1); };
+    const int pspar = (int)(PSTRIDE & 1);
+    auto rowp = [&](const Plane &P, int r, int par_r, int z) -> const double * {   // node 0 of row r of plane z
+        if constexpr (BULK)
+            return reinterpret_cast<const double *>(reinterpret_cast<const char *>(P.raw) + 816 * r +
+                                                    8 * ((par_r ^ (pspar & z)) & 1));
+        else
+            return nullptr;
+    };
 
     // ---- one-time setup ----
     for (int i = t; i < kBImgVec; i += 512) reinterpret_cast<uint4 *>(S.B)[i] = g_bimg[i];
     if (wu == 0) ptx::tmem_alloc<512>(&S.tmem);
     if (t == 0) {
-        for (int i = 0; i < ws::NP; ++i) ptx::mbar_init(&S.plane_full[i], 256);
+        for (int i = 0; i < ws::NP; ++i) {
+            ptx::mbar_init(&S.plane_full[i], 256);
+            ptx::mbar_init(&S.plane_tx[i], PY);
+        }
         for (int i = 0; i < 2; ++i) {
             for (int g = 0; g < 5; ++g) ptx::mbar_init(&S.a_free[i][g], 1);
             ptx::mbar_init(&S.d_free[i], 128);
@@ -108,7 +138,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
     // planes Lfirst .. Lfirst+2 and their materials, synchronously (every thread helps)
     for (int j = 0; j < 3; ++j) {
         const int iz = Lfirst + j;
-        PlaneWS &P = S.pl[slot(iz)];
+        Plane &P = S.pl[slot(iz)];
         for (int li = t; li < NODES; li += 512) {
             const int lpx = li % PX, lpy = li / PX;
             const int64_t gx = X0 - 1 + lpx, gy = Y0 - 1 + lpy;
@@ -116,7 +146,10 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             unsigned long long mx = 0;
             for (int c = 0; c < 3; ++c) {
                 const double v = ok ? __ldg(p.u + 3 * (PSTRIDE * iz + gx + NX1 * gy) + c) : 0.0;
-                P.up[c][li] = v;
+                if constexpr (BULK)
+                    const_cast<double *>(rowp(P, lpy, rowpar(lpy), iz))[3 * lpx + c] = v;
+                else
+                    P.up[c][li] = v;
                 const unsigned long long b = abs_bits(v);
                 mx = b > mx ? b : mx;
             }
@@ -148,6 +181,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
         // ================================ converters ================================
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TA_A0;
         const int n0 = ly * PX + lx;
+        const int rp_ly = rowpar(ly), rp_ly1 = rowpar(ly + 1);
         const int ld = t;                            // loader index 0..255
         // loader duties (converters; they run ahead of the epilogues): nodes ld, ld+256 of the 297 and
         // element ld of each plane; plane z+3 is completed and z+4 issued after layer z's MMAs
@@ -166,32 +200,91 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
         const bool mok = gex >= 0 && gex < p.nx && gey >= 0 && gey < p.ny;
         const uint8_t *mptr = p.mat + (mok ? gex + p.nx * gey : 0);
         int mid_next = (mok && Lfirst + 3 < nz) ? (int)__ldg(mptr + mstride * (int64_t)(Lfirst + 3)) : kZeroMat;
-        // issue the cp.async loads of plane z into its slot (zero-filled outside the grid or beyond nz)
+        // BULK: node coordinates of this thread's nodes and the tile's valid node columns [lox, hix)
+        int lpx_[2], lpy_[2], par_[2];
+        for (int j = 0; j < 2; ++j) {
+            const int li = ld + 256 * j;
+            lpy_[j] = li / PX;
+            lpx_[j] = li - lpy_[j] * PX;
+            par_[j] = rowpar(lpy_[j]);
+        }
+        const int lox = gx0 < 0 ? -gx0 : 0;
+        const int hix = (int)min((int64_t)PX, NX1 - gx0);
+        // issue the loads of plane z into its slot (zero-filled outside the grid or beyond nz)
         auto issue_plane = [&](int z) {
-            PlaneWS &P = S.pl[slot(z)];
-            for (int j = 0; j < nl; ++j) {
-                const int li = ld + 256 * j;
-                const bool ok = gok[j] && z <= nz;
-                const double *src = p.u + (ok ? PSTRIDE * 3 * (int64_t)z + goff[j] : 0);
+            Plane &P = S.pl[slot(z)];
+            if constexpr (BULK) {
+                // warp 1, lanes 0..8: one node row each — an 8-byte head and tail by plain loads where
+                // the row's first / last valid node is not 16-byte aligned, the rest by one bulk copy
+                if (wu == 1 && lane < PY) {
+                    const int r = lane;
+                    const int64_t gy = Y0 - 1 + r;
+                    uint32_t bytes = 0;
+                    char *dst = nullptr;
+                    const char *src = nullptr;
+                    if (gy >= 0 && gy < NY1 && z <= nz && hix > lox) {
+                        const int64_t nfirst = PSTRIDE * (int64_t)z + NX1 * gy + gx0 + lox;
+                        src = reinterpret_cast<const char *>(p.u + 3 * nfirst);
+                        dst = const_cast<char *>(reinterpret_cast<const char *>(rowp(P, r, rowpar(r), z) + 3 * lox));
+                        const uint32_t len = 24u * (uint32_t)(hix - lox);
+                        const uint32_t head = (reinterpret_cast<uintptr_t>(src) & 15) ? 8u : 0u;
+                        bytes = (len - head) & ~15u;
+                        const uint32_t tail = len - head - bytes;
+                        if (head) *reinterpret_cast<double *>(dst) = __ldg(reinterpret_cast<const double *>(src));
+                        if (tail)
+                            *reinterpret_cast<double *>(dst + head + bytes) =
+                                __ldg(reinterpret_cast<const double *>(src + head + bytes));
+                        src += head;
+                        dst += head;
+                    }
+                    ptx::fence_proxy_async_smem();   // the slot's earlier generic reads before the async writes
+                    ptx::mbar_arrive_expect_tx(&S.plane_tx[slot(z)], bytes);
+                    if (bytes) ptx::bulk_g2s(dst, src, bytes, &S.plane_tx[slot(z)]);
+                }
+            } else {
+                for (int j = 0; j < nl; ++j) {
+                    const int li = ld + 256 * j;
+                    const bool ok = gok[j] && z <= nz;
+                    const double *src = p.u + (ok ? PSTRIDE * 3 * (int64_t)z + goff[j] : 0);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) ptx::cp_async8(&P.up[c][li], src + c, ok);
+                    for (int c = 0; c < 3; ++c) ptx::cp_async8(&P.up[c][li], src + c, ok);
+                }
+                ptx::cp_async_commit();
             }
-            ptx::cp_async_commit();
         };
         // finish plane z (its cp.async group is the oldest outstanding one): node maxima, materials of
         // layer z, arrival on the plane's mbarrier
         auto finish_plane = [&](int z) {
-            ptx::cp_async_wait<0>();
-            PlaneWS &P = S.pl[slot(z)];
-            for (int j = 0; j < nl; ++j) {
-                const int li = ld + 256 * j;
-                unsigned long long mx = 0;
+            Plane &P = S.pl[slot(z)];
+            if constexpr (BULK) {
+                ptx::mbar_wait(&S.plane_tx[slot(z)], (uint32_t)(((z - (Lfirst + 3)) / ws::NP) & 1));
+                for (int j = 0; j < nl; ++j) {
+                    const int li = ld + 256 * j;
+                    double *q = const_cast<double *>(rowp(P, lpy_[j], par_[j], z)) + 3 * lpx_[j];
+                    unsigned long long mx = 0;
+                    if (gok[j] && z <= nz) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const unsigned long long b = abs_bits(P.up[c][li]);
-                    mx = b > mx ? b : mx;
+                        for (int c = 0; c < 3; ++c) {
+                            const unsigned long long b = abs_bits(q[c]);
+                            mx = b > mx ? b : mx;
+                        }
+                    } else {   // outside the grid: the copies left this node's slot untouched
+                        q[0] = q[1] = q[2] = 0.0;
+                    }
+                    P.nmax[li] = mx;
                 }
-                P.nmax[li] = mx;
+            } else {
+                ptx::cp_async_wait<0>();
+                for (int j = 0; j < nl; ++j) {
+                    const int li = ld + 256 * j;
+                    unsigned long long mx = 0;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const unsigned long long b = abs_bits(P.up[c][li]);
+                        mx = b > mx ? b : mx;
+                    }
+                    P.nmax[li] = mx;
+                }
             }
             P.mid[ld] = (uint8_t)mid_next;                           // layer z, loaded one iteration ago
             mid_next = (mok && z + 1 < nz) ? (int)__ldg(mptr + mstride * (int64_t)(z + 1)) : kZeroMat;
@@ -205,7 +298,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             if (L + 1 >= Lfirst + 3)   // plane L+1 arrived asynchronously (its k-th use of the slot)
                 ptx::mbar_wait(&S.plane_full[sL1], (uint32_t)(((L + 1 - (Lfirst + 3)) / ws::NP) & 1));
             TRW(1);
-            const PlaneWS &P0 = S.pl[sL], &P1 = S.pl[sL1];
+            const Plane &P0 = S.pl[sL], &P1 = S.pl[sL1];
             const unsigned long long *m0 = P0.nmax, *m1 = P1.nmax;
             auto dv = [](unsigned long long b) { return __longlong_as_double((long long)b); };
             const double amax = fmax(fmax(fmax(dv(m0[n0]), dv(m0[n0 + 1])), fmax(dv(m0[n0 + PX]), dv(m0[n0 + PX + 1]))),
@@ -225,10 +318,20 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             double ue[24];
             {
                 constexpr int off[4] = {0, 1, PX + 1, PX};
+                if constexpr (BULK) {
+                    const double *r00 = rowp(P0, ly, rp_ly, L) + 3 * lx, *r01 = rowp(P0, ly + 1, rp_ly1, L) + 3 * lx;
+                    const double *r10 = rowp(P1, ly, rp_ly, L + 1) + 3 * lx, *r11 = rowp(P1, ly + 1, rp_ly1, L + 1) + 3 * lx;
+                    const double *rb[8] = {r00, r00 + 3, r01 + 3, r01, r10, r10 + 3, r11 + 3, r11};
 #pragma unroll
-                for (int a = 0; a < 8; ++a)
+                    for (int a = 0; a < 8; ++a)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) ue[3 * a + c] = (a < 4 ? P0 : P1).up[c][n0 + off[a & 3]];
+                        for (int c = 0; c < 3; ++c) ue[3 * a + c] = rb[a][c];
+                } else {
+#pragma unroll
+                    for (int a = 0; a < 8; ++a)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) ue[3 * a + c] = (a < 4 ? P0 : P1).up[c][n0 + off[a & 3]];
+                }
             }
             // the other M-tile's MMAs must have read the shared A operand (m 0: layer L-1 of tile 1;
             // m 1: layer L of tile 0)
@@ -320,6 +423,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
     } else {
         // ================================ epilogues ================================
         const uint32_t td = tmem + ((uint32_t)(q * 32) << 16) + m * TA_D_TILE;
+        const int rp_ly = rowpar(ly);
         const int n0 = ly * PX + lx;
         bool has_src = false, has_rec = false;
         if (MODE == MODE_STEP) {
@@ -434,14 +538,16 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) p.iface_top_A[3 * ucol + c] = f[c];
                         } else if (MODE == MODE_STEP) {
-                            const PlaneWS &P = S.pl[slot(L)];
+                            const Plane &P = S.pl[slot(L)];
 #pragma unroll
                             for (int c = 0; c < 3; ++c) {
                                 double F = 0.0;
                                 if (has_src)
                                     for (int kk = 0; kk < p.nsrc; ++kk)
                                         if (p.src_dof[kk] == 3 * un_id + c) F = __dadd_rn(F, p.src_val[kk]);
-                                const double uc = P.up[c][n0];
+                                double uc;
+                                if constexpr (BULK) uc = rowp(P, ly, rp_ly, L)[3 * lx + c];
+                                else uc = P.up[c][n0];
                                 const double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
                                 double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
                                 if ((dm >> c) & 1) un = 0.0;

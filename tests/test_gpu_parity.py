@@ -531,12 +531,14 @@ def test_full_size_c4_sampled(ovxmod, name, path):
 
 @pytest.mark.parametrize("variant", [{"OVX_I8_KERNEL": "tmem"}, {"OVX_I8_KERNEL": "smem"},
                                      {"OVX_I8_KERNEL": "x", "OVX_I8X_LAYOUT": "word"},
-                                     {"OVX_I8_KERNEL": "x", "OVX_I8X_LAYOUT": "half"}])
+                                     {"OVX_I8_KERNEL": "x", "OVX_I8X_LAYOUT": "half"},
+                                     {"OVX_I8_PLANES": "bulk"}])
 def test_alternate_int8_kernels_bit_exact(ovxmod, variant):
     """The alternate INT8 kernels (selected once per process, so in a subprocess): step_i8w (the
     round-1 kernel: roles alternating per half-iteration) with the A operand in TMEM or in shared
-    memory, and step_i8x with the word (−K ⊗ I_4, no byte permutes) or half-word operand layout (the
-    default is the warp-specialised step_i8ws): apply_K and a 30-step trajectory bit-exact vs the oracle's U2 mirror on the ragged
+    memory, step_i8x with the word (−K ⊗ I_4, no byte permutes) or half-word operand layout, and the
+    default warp-specialised step_i8ws with its node planes delivered by the bulk-copy (TMA) engine
+    instead of cp.async: apply_K and a 30-step trajectory bit-exact vs the oracle's U2 mirror on the ragged
     multi-tile grid (DESIGN.md §6.1 compares their speed)."""
     import os
     import subprocess
