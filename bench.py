@@ -547,7 +547,7 @@ def main() -> None:
     # SURVEY §8(d)'s per-run ncu figures for the dominant kernel, from the committed capture of the
     # same command (profiles/; ncu numbers are never taken inside this timed run)
     ncu = None
-    prof = {0: "r2_int8_final", 1: "r2_fp64_final"}.get(path)
+    prof = {0: "r2_int8_ws_final", 1: "r2_fp64_final"}.get(path)
     if world == 1 and prof and os.path.exists(os.path.join(ROOT, "profiles", prof + ".json")):
         try:
             l0 = json.load(open(os.path.join(ROOT, "profiles", prof + ".json")))["launches"][0]

@@ -25,20 +25,25 @@ CATS = OrderedDict([
     ("v + 2^56 offset (high word)", [r"AOFF >> 32", r"\+ \(uint32_t\)AOFF"]),
     ("byte packing (PRMT) into the A words", [r"__byte_perm"]),
     ("A operand to TMEM (tcgen05.st)", [r"tmem_st4", r"tmem_st8", r"tcgen05\.st"]),
-    ("gather of u_e from shared planes", [r"ue\[j\] =", r"gather16"]),
+    ("gather of u_e from shared planes", [r"ue\[j\] =", r"gather16", r"ue\[3 \* a", r"rb\[a\]"]),
     ("s_e = max|ū| (node maxima, 64-bit max)", [r"ullmax", r"max\(ab", r"ab = ", r"amax", r"fmax\(amax", r"qmax"]),
     ("degenerate / fast-path tests", [r"const bool deg", r"const bool vzero", r"const bool fast", r"__all_sync"]),
-    ("reciprocal RN(1/s)", [r"1\.0 / s", r"__dmul_rn\(r, SCALE\)"]),
+    ("reciprocal RN(1/s)", [r"1\.0 / s", r"__drcp_rn", r"__dmul_rn\(r, SCALE\)"]),
     ("MMA issue, commit, M-tile barrier", [r"mma_i8", r"mma_commit", r"bar\.sync", r"elect_one", r"smem_desc"]),
     ("MMA completion waits (mbarrier)", [r"mbar_wait", r"try_wait"]),
     ("accumulators from TMEM (tcgen05.ld)", [r"tmem_ld", r"tcgen05\.ld", r"tcgen05\.wait"]),
-    ("exact two-limb recombination", [r"limb", r"p0 = ", r"mad\.wide", r"acc\)", r"I8_LIMB_MAGIC", r"add\.cc"]),
+    ("exact two-limb recombination", [r"limb", r"p0 = ", r"mad\.wide", r"acc\)", r"I8_LIMB_MAGIC", r"add\.cc", r"p1 >> 16"]),
     ("RN(y) and the Eq. 9 scalar (DFMA, DMUL)", [r"__fma_rn\(dhi", r"__dmul_rn\(alpha", r"const double alpha"]),
-    ("node sums: x-pairs (shuffle), y-pairs (smem)", [r"__shfl_up_sync", r"shfl", r"ysum", r"plo\[c\]"]),
+    ("node sums: x-pairs (shuffle), y-pairs (smem)", [r"__shfl_up_sync", r"shfl", r"ysum", r"plo\[c\]", r"S\.ys\[",
+                                                      r"Pb\[c\]", r"Pt\[c\]", r"fbot\[c\]", r"ftop\[c\]", r"ys_ready"]),
     ("post-phase: face sums, T + B, update, store", [r"tfv", r"ucv", r"face\[", r"__fma_rn\(wn", r"un = ", r"dst\[c\]",
-                                                    r"\(DAMP \? p\.un : p\.uo\)", r"p\.src_dof", r"2\.0, uc", r"dm >> c"]),
+                                                    r"\(DAMP \? p\.un : p\.uo\)", r"p\.src_dof", r"2\.0, uc", r"dm >> c",
+                                                    r"uc = ", r"p\.uo\[3 \* un_id", r"__dadd_rn\(T\[c\]", r"T\[c\] = ftop",
+                                                    r"p\.rec_node", r"p\.fout"]),
     ("plane / operand prefetch and park (global loads, smem stores)", [r"__ldg", r"load_in", r"pfv", r"S\.up\[",
-                                                                     r"nmax", r"upv_n", r"wn_n", r"mfar", r"S\.mid"]),
+                                                                     r"nmax", r"upv_n", r"wn_n", r"mfar", r"S\.mid",
+                                                                     r"cp_async", r"P\.up\[", r"P\.mid", r"mid_next",
+                                                                     r"abs_bits", r"mx = b > mx", r"upv\[", r"p\.uo\[3 \* nd"]),
 ])
 
 
@@ -116,3 +121,9 @@ print(f"warp-instructions (smsp__inst_executed.sum): {tot:.4g}  ->  thread-instr
 print(f"{'category':66s} {'/elem':>7s} {'share':>6s}")
 for name, n in by.most_common():
     print(f"{name:66s} {32 * n / ELEMS:7.0f} {100 * n / tot:5.1f}%")
+# the largest lines left in "other" (transparency for the catch-all category)
+oth = sorted(((n, k) for k, n in counts.items()
+              if cat_of(line_src.get(k, ""), k) == "loop control, indexing, role selection (other)"), reverse=True)[:12]
+print("\nlargest 'other' lines (thread-instructions per element):")
+for n, k in oth:
+    print(f"  {k[0]}:{k[1]:<5d} {32 * n * scale / ELEMS:6.0f}  {line_src.get(k, '')[:70]}")
