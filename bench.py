@@ -448,7 +448,16 @@ def main() -> None:
         else:
             R = Sharded(args.n, path_id, local, stream, world, rank)
         R.set_state(R.u0, R.u0)
-        R.step(warmup)
+        try:
+            R.step(warmup)
+        except Exception as ex:   # the library's NCCL schedule failed at run time: the Python-driven one
+            if not isinstance(R, ShardedLib):
+                raise
+            print(f"bench.py: library z-slab step failed ({ex}); using dist.py", file=sys.stderr)
+            os.environ["OVX_BENCH_DIST"] = "python"
+            R = Sharded(args.n, path_id, local, stream, world, rank)
+            R.set_state(R.u0, R.u0)
+            R.step(warmup)
         barrier()
         R.s.get_timers(reset=True)
         sampler = ClockSampler(local) if sample_clocks else None
