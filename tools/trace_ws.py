@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 from paper_2404_13683_b200 import build as B
-B.LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "abl", "libovx_trace.so")
+B.LIB = os.environ.get("OVX_TRACE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "abl", "libovx_trace.so")
 B._stale = lambda: False
 import bench
 from paper_2404_13683_b200 import Ovx, OVX_INT8
