@@ -269,8 +269,8 @@ cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// INT8 kernel variant (OVX_I8_KERNEL): "ws" (default) step_i8ws, warp-specialised (undamped time
-// steps and products, M = 8; damped steps, M = 4 / 6 and the debug records use step_i8w); "tmem"
+// INT8 kernel variant (OVX_I8_KERNEL): "ws" (default) step_i8ws, warp-specialised (time steps,
+// damped or not, and products, M = 8; M = 4 / 6, the direct path and the debug records use step_i8w); "tmem"
 // step_i8w with the A operand in TMEM (the round-1 kernel); "smem" step_i8w with A in shared memory;
 // "x" step_i8x (word or half-word operand layout, OVX_I8X_LAYOUT).  All bit-identical; DESIGN.md
 // §6.1 has the measurements.
@@ -295,23 +295,25 @@ bool i8_bulk_planes() {
     return v;
 }
 
-template <int MODE, bool SLAB, bool BULK>
+template <int MODE, bool SLAB, bool BULK, bool DAMP = false>
 cudaError_t launch_i8ws_b(const StepParams &p, int64_t ctas, cudaStream_t st) {
     const int smem = (int)sizeof(SmemWST<BULK>);
     static unsigned attr = 0;
     if (!attr_done(attr)) {
         cudaError_t e =
-            cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK, DAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        e = cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK, DAMP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         attr_set(attr);
     }
-    step_i8ws<MODE, SLAB, BULK><<<(unsigned)ctas, 512, smem, st>>>(p);
+    step_i8ws<MODE, SLAB, BULK, DAMP><<<(unsigned)ctas, 512, smem, st>>>(p);
     return cudaGetLastError();
 }
 template <int MODE, bool SLAB>
 cudaError_t launch_i8ws(const StepParams &p, int64_t ctas, cudaStream_t st) {
+    if constexpr (MODE == MODE_STEP)
+        if (p.damped) return launch_i8ws_b<MODE, SLAB, false, true>(p, ctas, st);
     return i8_bulk_planes() ? launch_i8ws_b<MODE, SLAB, true>(p, ctas, st) : launch_i8ws_b<MODE, SLAB, false>(p, ctas, st);
 }
 
@@ -373,7 +375,7 @@ cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStre
     }
     const int v = i8_variant();
     if constexpr (M == 8)
-        if (v == 3 && mode != MODE_DEBUG && !p.damped) {   // warp-specialised kernel (M = 8, undamped)
+        if (v == 3 && mode != MODE_DEBUG && (!p.damped || mode == MODE_STEP)) {   // warp-specialised kernel (M = 8)
             if (mode == MODE_STEP)
                 return p.slab_flags ? launch_i8ws<MODE_STEP, true>(p, ctas, st) : launch_i8ws<MODE_STEP, false>(p, ctas, st);
             return p.slab_flags ? launch_i8ws<MODE_APPLY, true>(p, ctas, st) : launch_i8ws<MODE_APPLY, false>(p, ctas, st);

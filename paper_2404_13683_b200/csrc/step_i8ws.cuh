@@ -61,12 +61,17 @@ struct SmemWST {
     uint64_t d_free[2];                        // the 128 epilogue threads of the M-tile arrive
     uint64_t ys_ready[ws::NYS];                // the 32 threads of warp 11 (row 3) arrive
     uint64_t plane_tx[ws::NP];                 // BULK: the 9 row copies of the plane landed (9 arrivals + bytes)
+    double upst[2][3][I8W::NODES];             // DAMP: u_prev of the planes in flight (by plane parity)
     uint32_t tmem;
 };
 using SmemWS = SmemWST<false>;
 
-template <int MODE, bool SLAB, bool BULK = false>
+// DAMP (MODE_STEP, cp.async planes): Rayleigh damping, reading R1 — the planes hold the EBE input
+// ũ = u + cb·(u − u_prev) (u_prev staged next to the plane and folded in when the plane completes),
+// the update reads u and u_prev of its node from global memory and writes u^{it+1} to p.un.
+template <int MODE, bool SLAB, bool BULK = false, bool DAMP = false>
 __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
+    static_assert(!DAMP || (MODE == MODE_STEP && !BULK), "damped: time steps with cp.async planes");
     using C = I8W;
     constexpr int EX = C::EX, PX = C::PX, PY = C::PY, NODES = C::NODES, NE = C::NE;
     constexpr double ISCALE = 1.0 / (double)(1ull << 56);
@@ -145,7 +150,11 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             const bool ok = gx >= 0 && gx < NX1 && gy >= 0 && gy < NY1 && iz <= nz;
             unsigned long long mx = 0;
             for (int c = 0; c < 3; ++c) {
-                const double v = ok ? __ldg(p.u + 3 * (PSTRIDE * iz + gx + NX1 * gy) + c) : 0.0;
+                double v = ok ? __ldg(p.u + 3 * (PSTRIDE * iz + gx + NX1 * gy) + c) : 0.0;
+                if constexpr (DAMP) {   // ũ = u + cb·(u − u_prev), reading R1
+                    const double pp = ok ? __ldg(p.uo + 3 * (PSTRIDE * iz + gx + NX1 * gy) + c) : 0.0;
+                    v = __dadd_rn(v, __dmul_rn(p.cb, __dsub_rn(v, pp)));
+                }
                 if constexpr (BULK)
                     const_cast<double *>(rowp(P, lpy, rowpar(lpy), iz))[3 * lpx + c] = v;
                 else
@@ -248,6 +257,11 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                     const double *src = p.u + (ok ? PSTRIDE * 3 * (int64_t)z + goff[j] : 0);
 #pragma unroll
                     for (int c = 0; c < 3; ++c) ptx::cp_async8(&P.up[c][li], src + c, ok);
+                    if constexpr (DAMP) {
+                        const double *srp = p.uo + (ok ? PSTRIDE * 3 * (int64_t)z + goff[j] : 0);
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) ptx::cp_async8(&S.upst[z & 1][c][li], srp + c, ok);
+                    }
                 }
                 ptx::cp_async_commit();
             }
@@ -280,7 +294,12 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                     unsigned long long mx = 0;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        const unsigned long long b = abs_bits(P.up[c][li]);
+                        double v = P.up[c][li];
+                        if constexpr (DAMP) {   // ũ = u + cb·(u − u_prev), reading R1
+                            v = __dadd_rn(v, __dmul_rn(p.cb, __dsub_rn(v, S.upst[z & 1][c][li])));
+                            P.up[c][li] = v;
+                        }
+                        const unsigned long long b = abs_bits(v);
                         mx = b > mx ? b : mx;
                     }
                     P.nmax[li] = mx;
@@ -442,6 +461,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
 
         double T[3] = {0.0, 0.0, 0.0};               // top-face sum of the previous layer at this node
         double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;
+        double uv[3] = {0.0, 0.0, 0.0};              // DAMP: u of the owned node (the plane holds ũ)
         uint8_t dm = 0;
         int64_t node_next = ucol + PSTRIDE * (int64_t)Lfirst;
         auto prefetch_update = [&](int P) {
@@ -450,6 +470,10 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                 upv[0] = p.uo[3 * nd];
                 upv[1] = p.uo[3 * nd + 1];
                 upv[2] = p.uo[3 * nd + 2];
+                if constexpr (DAMP) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) uv[c] = __ldg(p.u + 3 * nd + c);
+                }
                 wn = __ldg(p.w + nd);
                 dm = p.dmask ? __ldg(p.dmask + nd) : (uint8_t)0;
             }
@@ -548,10 +572,12 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                                 double uc;
                                 if constexpr (BULK) uc = rowp(P, ly, rp_ly, L)[3 * lx + c];
                                 else uc = P.up[c][n0];
-                                const double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
+                                if constexpr (DAMP) uc = uv[c];
+                                double b = __dsub_rn(__dmul_rn(2.0, uc), upv[c]);
+                                if constexpr (DAMP) b = __dsub_rn(b, __dmul_rn(p.ca, __dsub_rn(uc, upv[c])));
                                 double un = __fma_rn(wn, __dsub_rn(F, f[c]), b);
                                 if ((dm >> c) & 1) un = 0.0;
-                                p.uo[3 * un_id + c] = un;
+                                (DAMP ? p.un : p.uo)[3 * un_id + c] = un;
                                 if (has_rec)
                                     for (int kk = 0; kk < p.nrec; ++kk)
                                         if (p.rec_node[kk] == un_id) p.traces[(3 * kk + c) * p.rec_nt + p.it] = un;
