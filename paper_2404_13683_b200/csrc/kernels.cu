@@ -270,7 +270,8 @@ cudaError_t launch_i8w(const StepParams &p, int64_t ctas, cudaStream_t st) {
 }
 
 // INT8 kernel variant (OVX_I8_KERNEL): "ws" (default) step_i8ws, warp-specialised (time steps,
-// damped or not, and products, M = 8; M = 4 / 6, the direct path and the debug records use step_i8w); "tmem"
+// damped or not, and products; M = 4 / 6 undamped single contexts; the direct path, the debug records
+// and M = 4 / 6 damped or on z-slabs use step_i8w); "tmem"
 // step_i8w with the A operand in TMEM (the round-1 kernel); "smem" step_i8w with A in shared memory;
 // "x" step_i8x (word or half-word operand layout, OVX_I8X_LAYOUT).  All bit-identical; DESIGN.md
 // §6.1 has the measurements.
@@ -295,19 +296,19 @@ bool i8_bulk_planes() {
     return v;
 }
 
-template <int MODE, bool SLAB, bool BULK, bool DAMP = false>
+template <int MODE, bool SLAB, bool BULK, bool DAMP = false, int M = 8>
 cudaError_t launch_i8ws_b(const StepParams &p, int64_t ctas, cudaStream_t st) {
     const int smem = (int)sizeof(SmemWST<BULK>);
     static unsigned attr = 0;
     if (!attr_done(attr)) {
         cudaError_t e =
-            cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK, DAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK, DAMP, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK, DAMP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        e = cudaFuncSetAttribute(step_i8ws<MODE, SLAB, BULK, DAMP, M>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         attr_set(attr);
     }
-    step_i8ws<MODE, SLAB, BULK, DAMP><<<(unsigned)ctas, 512, smem, st>>>(p);
+    step_i8ws<MODE, SLAB, BULK, DAMP, M><<<(unsigned)ctas, 512, smem, st>>>(p);
     return cudaGetLastError();
 }
 template <int MODE, bool SLAB>
@@ -374,12 +375,17 @@ cudaError_t launch_i8_mode(int mode, const StepParams &p, int64_t ctas, cudaStre
         return cudaErrorInvalidValue;
     }
     const int v = i8_variant();
-    if constexpr (M == 8)
+    if constexpr (M == 8) {
         if (v == 3 && mode != MODE_DEBUG && (!p.damped || mode == MODE_STEP)) {   // warp-specialised kernel (M = 8)
             if (mode == MODE_STEP)
                 return p.slab_flags ? launch_i8ws<MODE_STEP, true>(p, ctas, st) : launch_i8ws<MODE_STEP, false>(p, ctas, st);
             return p.slab_flags ? launch_i8ws<MODE_APPLY, true>(p, ctas, st) : launch_i8ws<MODE_APPLY, false>(p, ctas, st);
         }
+    } else {   // M = 4 / 6 on the warp-specialised kernel: single contexts, undamped
+        if (v == 3 && mode != MODE_DEBUG && !p.damped && !p.slab_flags)
+            return mode == MODE_STEP ? launch_i8ws_b<MODE_STEP, false, false, false, M>(p, ctas, st)
+                                     : launch_i8ws_b<MODE_APPLY, false, false, false, M>(p, ctas, st);
+    }
     if (v == 2 && mode != MODE_DEBUG)
         return p.slab_flags ? launch_i8x_mode<M, true>(mode, p, ctas, st) : launch_i8x_mode<M, false>(mode, p, ctas, st);
     return v == 1 ? launch_i8_mode_g<M, I8W, false>(mode, p, ctas, st)

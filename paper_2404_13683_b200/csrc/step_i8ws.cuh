@@ -69,14 +69,17 @@ using SmemWS = SmemWST<false>;
 // DAMP (MODE_STEP, cp.async planes): Rayleigh damping, reading R1 — the planes hold the EBE input
 // ũ = u + cb·(u − u_prev) (u_prev staged next to the plane and folded in when the plane completes),
 // the update reads u and u_prev of its node from global memory and writes u^{it+1} to p.un.
-template <int MODE, bool SLAB, bool BULK = false, bool DAMP = false>
+// M (NEXT-4): INT8 stages, a = 2^{7M}; the byte slices of v + 2^{7M} fill NA = 2 (M = 4), 3 (M = 6) or
+// 4 (M = 8) half-word arrays (fewer MMAs and limbs for fewer stages).
+template <int MODE, bool SLAB, bool BULK = false, bool DAMP = false, int M = 8>
 __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
+    constexpr int NA = ((7 * M + 1 + 7) / 8 + 1) / 2;
     static_assert(!DAMP || (MODE == MODE_STEP && !BULK), "damped: time steps with cp.async planes");
     using C = I8W;
     constexpr int EX = C::EX, PX = C::PX, PY = C::PY, NODES = C::NODES, NE = C::NE;
-    constexpr double ISCALE = 1.0 / (double)(1ull << 56);
-    constexpr double SCALE = (double)(1ull << 56);
-    constexpr unsigned long long AOFF = 1ull << 56;
+    constexpr double ISCALE = 1.0 / (double)(1ull << (7 * M));   // exact powers of two
+    constexpr double SCALE = (double)(1ull << (7 * M));
+    constexpr unsigned long long AOFF = 1ull << (7 * M);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     SmemWST<BULK> &S = *reinterpret_cast<SmemWST<BULK> *>(smem_raw);
     using Plane = PlaneT<BULK>;
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             const bool deg = !ein || !(s >= 0x1p-1022) || !(s <= 0x1.fffffffffffffp1023);
             const bool vzero = !ein || !(s >= 0x1p-1022);
             const bool fast = (s <= 0x1.fffffffffffffp1023) && (vzero || s >= 0x1p-960);
-            const double alpha = deg ? 0.0 : -__dmul_rn(mcv.y, __dmul_rn(s, ISCALE));   // −RN(c1·RN(s·2^-56))
+            const double alpha = deg ? 0.0 : -__dmul_rn(mcv.y, __dmul_rn(s, ISCALE));   // −RN(c1·RN(s·2^-7M))
             const double r = 1.0 / s;                                  // RN(1/s_e), reading Q7
             const double R = vzero ? 0.0 : __dmul_rn(r, SCALE);
             TRW(11);
@@ -369,8 +372,13 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                         long long v;
                         if constexpr (FAST) v = __double2ll_rz(__dmul_rn(ub, R));
                         else v = deg ? 0ll : __double2ll_rz(__dmul_rn(__dmul_rn(ub, r), SCALE));
-                        lo[qq] = (uint32_t)(unsigned long long)v;
-                        hi[qq] = (uint32_t)((unsigned long long)v >> 32) + (uint32_t)(AOFF >> 32);
+                        if constexpr (7 * M >= 32) {   // v + 2^{7M}: the offset only touches the high word
+                            lo[qq] = (uint32_t)(unsigned long long)v;
+                            hi[qq] = (uint32_t)((unsigned long long)v >> 32) + (uint32_t)(AOFF >> 32);
+                        } else {                       // v + 2^{7M} < 2^32
+                            lo[qq] = (uint32_t)(unsigned long long)v + (uint32_t)AOFF;
+                            hi[qq] = 0;
+                        }
                     }
                     // the other M-tile's MMAs of the K-step group that last reads this chunk must be
                     // complete (groups: ks0 = chunks 0-1, ks1 = 2-3, fold a = 3-4, ks2 = 4-5, fold b = 5-6)
@@ -387,7 +395,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                                       (uint32_t)__double2hiint(alpha));
                     }
 #pragma unroll
-                    for (int pa = 0; pa < 4; ++pa) {
+                    for (int pa = 0; pa < NA; ++pa) {
                         const uint32_t *src = pa < 2 ? lo : hi;
                         const uint32_t sel = (pa & 1) ? 0x7632u : 0x5410u;
                         ptx::tmem_st4(ta + pa * TA_A_ARR + 4 * ch, __byte_perm(src[0], src[1], sel),
@@ -420,7 +428,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
 #pragma unroll
                     for (int g = 0; g < 5; ++g) {
 #pragma unroll
-                        for (int pa = 0; pa < 4; ++pa)
+                        for (int pa = 0; pa < NA; ++pa)
                             ptx::mma_i8_ts(tmem + m * TA_D_TILE + pa * TA_D_ARR, tmem + TA_A0 + pa * TA_A_ARR + aoff[g],
                                            bdesc[g], IDESC, g > 0 ? 1u : 0u);
                         ptx::mma_commit(&S.a_free[m][g]);
@@ -499,16 +507,21 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                     uint32_t R0[8], R1[8], R2[8], R3[8];
                     ptx::tmem_ld8(td + 0 * TA_D_ARR + rr * 8, R0);
                     ptx::tmem_ld8(td + 1 * TA_D_ARR + rr * 8, R1);
-                    ptx::tmem_ld8(td + 2 * TA_D_ARR + rr * 8, R2);
-                    ptx::tmem_ld8(td + 3 * TA_D_ARR + rr * 8, R3);
+                    if (NA > 2) ptx::tmem_ld8(td + 2 * TA_D_ARR + rr * 8, R2);
+                    if (NA > 3) ptx::tmem_ld8(td + 3 * TA_D_ARR + rr * 8, R3);
                     ptx::tmem_ld_wait();
 #pragma unroll
                     for (int qq = 0; qq < 4; ++qq) {
                         const double dlo = limb_biased((int32_t)R0[2 * qq], (int32_t)R0[2 * qq + 1], (int32_t)R1[2 * qq],
                                                        (int32_t)R1[2 * qq + 1]);
-                        const double dhi = limb_biased((int32_t)R2[2 * qq], (int32_t)R2[2 * qq + 1], (int32_t)R3[2 * qq],
-                                                       (int32_t)R3[2 * qq + 1]);
-                        const double f = __dmul_rn(alpha, __fma_rn(dhi, 0x1p32, dlo));   // RN(c1s·RN(y))
+                        double y = dlo;
+                        if constexpr (NA > 2) {   // stages beyond NA arrays are absent: the bias value (C_j = 0)
+                            const double dhi =
+                                limb_biased((int32_t)R2[2 * qq], (int32_t)R2[2 * qq + 1],
+                                            NA > 3 ? (int32_t)R3[2 * qq] : I8_BIAS, NA > 3 ? (int32_t)R3[2 * qq + 1] : I8_BIAS);
+                            y = __fma_rn(dhi, 0x1p32, dlo);
+                        }
+                        const double f = __dmul_rn(alpha, y);   // RN(c1s·RN(y))
                         const int j = 4 * rr + qq;
                         if (j < 12) fb[j] = f;
                         else ft[j - 12] = f;
