@@ -28,7 +28,7 @@
 #endif
 
 namespace ws {
-constexpr int NP = 7;                          // plane ring (the converters load 3-4 planes ahead)
+constexpr int NP = 8;                          // plane ring (the converters load 3-4 planes ahead; a power of two)
 constexpr int NYS = 4;                         // face-sum exchange ring (layers)
 }  // namespace ws
 
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
     const bool tnode = lx >= 1 && ly >= 1;
     const bool own = tnode && ex < NX1 && ey < NY1;
     const int64_t ucol = own ? ex + NX1 * ey : 0;
-    auto slot = [](int z) { return (z + 3 * ws::NP) % ws::NP; };   // z >= -NP
+    auto slot = [](int z) { return z & (ws::NP - 1); };   // z >= 0
     // BULK: the row phase s = parity of the global node index of the row's x = -1 node in plane z
     const int gx0 = (int)(X0 - 1);
     auto rowpar = [&](int r) { return (int)((gx0 + NX1 * (Y0 - 1 + r)) & 1); };
@@ -254,7 +254,9 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                     if (bytes) ptx::bulk_g2s(dst, src, bytes, &S.plane_tx[slot(z)]);
                 }
             } else {
-                for (int j = 0; j < nl; ++j) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (j >= nl) break;
                     const int li = ld + 256 * j;
                     const bool ok = gok[j] && z <= nz;
                     const double *src = p.u + (ok ? PSTRIDE * 3 * (int64_t)z + goff[j] : 0);
@@ -292,7 +294,9 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                 }
             } else {
                 ptx::cp_async_wait<0>();
-                for (int j = 0; j < nl; ++j) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (j >= nl) break;
                     const int li = ld + 256 * j;
                     unsigned long long mx = 0;
 #pragma unroll
@@ -323,8 +327,11 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             const Plane &P0 = S.pl[sL], &P1 = S.pl[sL1];
             const unsigned long long *m0 = P0.nmax, *m1 = P1.nmax;
             auto dv = [](unsigned long long b) { return __longlong_as_double((long long)b); };
-            const double amax = fmax(fmax(fmax(dv(m0[n0]), dv(m0[n0 + 1])), fmax(dv(m0[n0 + PX]), dv(m0[n0 + PX + 1]))),
-                                     fmax(fmax(dv(m1[n0]), dv(m1[n0 + 1])), fmax(dv(m1[n0 + PX]), dv(m1[n0 + PX + 1]))));
+            // max of the magnitude bit patterns (monotone for non-negative doubles; a NaN sorts above +inf
+            // and makes the element degenerate, as in step_i8w)
+            auto umax = [](unsigned long long x, unsigned long long y) { return x > y ? x : y; };
+            const double amax = dv(umax(umax(umax(m0[n0], m0[n0 + 1]), umax(m0[n0 + PX], m0[n0 + PX + 1])),
+                                        umax(umax(m1[n0], m1[n0 + 1]), umax(m1[n0 + PX], m1[n0 + PX + 1]))));
             const int mcur = P0.mid[elem];
             const double2 mcv = S.mc[mcur];
             const double cG = mcv.x;
