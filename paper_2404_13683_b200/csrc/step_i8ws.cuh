@@ -211,7 +211,8 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
         const int64_t gex = X0 - 1 + elx, gey = Y0 - 1 + ely;
         const bool mok = gex >= 0 && gex < p.nx && gey >= 0 && gey < p.ny;
         const uint8_t *mptr = p.mat + (mok ? gex + p.nx * gey : 0);
-        int mid_next = (mok && Lfirst + 3 < nz) ? (int)__ldg(mptr + mstride * (int64_t)(Lfirst + 3)) : kZeroMat;
+        const uint8_t *mrow = mptr + mstride * (int64_t)(Lfirst + 3);   // element ld in layer z+1 (running)
+        int mid_next = (mok && Lfirst + 3 < nz) ? (int)__ldg(mrow) : kZeroMat;
         // BULK: node coordinates of this thread's nodes and the tile's valid node columns [lox, hix)
         int lpx_[2], lpy_[2], par_[2];
         for (int j = 0; j < 2; ++j) {
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
         const int lox = gx0 < 0 ? -gx0 : 0;
         const int hix = (int)min((int64_t)PX, NX1 - gx0);
         // issue the loads of plane z into its slot (zero-filled outside the grid or beyond nz)
+        int64_t zoff = PSTRIDE * 3 * (int64_t)(Lfirst + 3);   // 3·PSTRIDE·z of the next plane to issue
         auto issue_plane = [&](int z) {
             Plane &P = S.pl[slot(z)];
             if constexpr (BULK) {
@@ -259,17 +261,18 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                     if (j >= nl) break;
                     const int li = ld + 256 * j;
                     const bool ok = gok[j] && z <= nz;
-                    const double *src = p.u + (ok ? PSTRIDE * 3 * (int64_t)z + goff[j] : 0);
+                    const double *src = p.u + (ok ? zoff + goff[j] : 0);
 #pragma unroll
                     for (int c = 0; c < 3; ++c) ptx::cp_async8(&P.up[c][li], src + c, ok);
                     if constexpr (DAMP) {
-                        const double *srp = p.uo + (ok ? PSTRIDE * 3 * (int64_t)z + goff[j] : 0);
+                        const double *srp = p.uo + (ok ? zoff + goff[j] : 0);
 #pragma unroll
                         for (int c = 0; c < 3; ++c) ptx::cp_async8(&S.upst[z & 1][c][li], srp + c, ok);
                     }
                 }
                 ptx::cp_async_commit();
             }
+            zoff += 3 * PSTRIDE;
         };
         // finish plane z (its cp.async group is the oldest outstanding one): node maxima, materials of
         // layer z, arrival on the plane's mbarrier
@@ -313,7 +316,8 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                 }
             }
             P.mid[ld] = (uint8_t)mid_next;                           // layer z, loaded one iteration ago
-            mid_next = (mok && z + 1 < nz) ? (int)__ldg(mptr + mstride * (int64_t)(z + 1)) : kZeroMat;
+            mrow += mstride;
+            mid_next = (mok && z + 1 < nz) ? (int)__ldg(mrow) : kZeroMat;
             ptx::mbar_arrive(&S.plane_full[slot(z)]);
         };
         if (Lfirst + 3 <= Lend) issue_plane(Lfirst + 3);
@@ -478,10 +482,10 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
         double upv[3] = {0.0, 0.0, 0.0}, wn = 0.0;
         double uv[3] = {0.0, 0.0, 0.0};              // DAMP: u of the owned node (the plane holds ũ)
         uint8_t dm = 0;
-        int64_t node_next = ucol + PSTRIDE * (int64_t)Lfirst;
+        int64_t nd_next = ucol + PSTRIDE * (int64_t)Lfirst;   // node of plane P of prefetch_update (running)
         auto prefetch_update = [&](int P) {
             if (MODE == MODE_STEP && own && P >= Z0 && P <= Plast) {
-                const int64_t nd = ucol + PSTRIDE * (int64_t)P;
+                const int64_t nd = nd_next;
                 upv[0] = p.uo[3 * nd];
                 upv[1] = p.uo[3 * nd + 1];
                 upv[2] = p.uo[3 * nd + 2];
@@ -492,8 +496,10 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                 wn = __ldg(p.w + nd);
                 dm = p.dmask ? __ldg(p.dmask + nd) : (uint8_t)0;
             }
+            nd_next += PSTRIDE;
         };
-        (void)node_next;
+        int64_t un_cur = ucol + PSTRIDE * (int64_t)Lfirst;   // node of plane L (running)
+
         prefetch_update(Lfirst);
         for (int L = Lfirst; L <= Plast; ++L) {
             const int k = L - Lfirst;
@@ -570,7 +576,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                 }
                 const bool plane_done = L >= Z0;     // L <= Plast by the loop bound
                 if (own && plane_done) {
-                    const int64_t un_id = ucol + PSTRIDE * (int64_t)L;
+                    const int64_t un_id = un_cur;
                     if (SLAB && (p.slab_flags & 1) && L == 0) {
 #pragma unroll
                         for (int c = 0; c < 3; ++c) p.iface_bot_b[3 * ucol + c] = fbot[c];
@@ -612,6 +618,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                 for (int c = 0; c < 3; ++c) T[c] = ftop[c];
             }
             TRW(7);
+            un_cur += PSTRIDE;
             prefetch_update(L + 1);
         }
     }
