@@ -561,11 +561,13 @@ def main() -> None:
         try:
             l0 = json.load(open(os.path.join(ROOT, "profiles", prof + ".json")))["launches"][0]
             g = lambda k: l0.get(k, [None])[0]
-            ncu = {"source": f"profiles/{prof}.md", "kernel_ms": g("gpu__time_duration.sum"),
+            _scale = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "ms": 1.0, "us": 1e-3, "ns": 1e-6}
+            gu = lambda k: l0[k][0] * _scale[l0[k][1]]   # ncu picks the unit per value: GB / ms
+            ncu = {"source": f"profiles/{prof}.md", "kernel_ms": gu("gpu__time_duration.sum"),
                    "issue_active_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                    "tensor_pipe_active_pct": g("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
                    "fp64_pipe_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
-                   "dram_gbytes_per_launch": (g("dram__bytes_read.sum") + g("dram__bytes_write.sum")) / 1e3,
+                   "dram_gbytes_per_launch": gu("dram__bytes_read.sum") + gu("dram__bytes_write.sum"),
                    "warp_instructions": g("smsp__inst_executed.sum")}
         except Exception:
             ncu = None
