@@ -57,7 +57,7 @@ struct SmemWST {
     double ys[ws::NYS][2][3][I8W::EY][I8W::EX];   // [layer slot][face b/t][c][row][lx]: x-pair P' of the +y corners
     double2 mc[kMaxMat];
     uint64_t plane_full[ws::NP];               // the 256 converter threads arrive
-    uint64_t a_free[2][5];                     // tcgen05.commit after each MMA K-step group; [m][4] = all done
+    uint64_t mma_done[2];                      // tcgen05.commit after the M-tile's 20 MMAs of a layer
     uint64_t d_free[2];                        // the 128 epilogue threads of the M-tile arrive
     uint64_t ys_ready[ws::NYS];                // the 32 threads of warp 11 (row 3) arrive
     uint64_t plane_tx[ws::NP];                 // BULK: the 9 row copies of the plane landed (9 arrivals + bytes)
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             ptx::mbar_init(&S.plane_tx[i], PY);
         }
         for (int i = 0; i < 2; ++i) {
-            for (int g = 0; g < 5; ++g) ptx::mbar_init(&S.a_free[i][g], 1);
+            ptx::mbar_init(&S.mma_done[i], 1);
             ptx::mbar_init(&S.d_free[i], 128);
         }
         for (int i = 0; i < ws::NYS; ++i) ptx::mbar_init(&S.ys_ready[i], 32);
@@ -391,11 +391,10 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                             hi[qq] = 0;
                         }
                     }
-                    // the other M-tile's MMAs of the K-step group that last reads this chunk must be
-                    // complete (groups: ks0 = chunks 0-1, ks1 = 2-3, fold a = 3-4, ks2 = 4-5, fold b = 5-6)
-                    if (need_free && ch != 1) {
-                        constexpr int GRP[6] = {0, 0, 1, 2, 3, 4};
-                        ptx::mbar_wait(&S.a_free[1 - m][GRP[ch]], fpar);
+                    // the other M-tile's MMAs must have read the shared A: one wait for all of them before
+                    // the first store (measured: one wait beats chunk-granular release)
+                    if (need_free && ch == 0) {
+                        ptx::mbar_wait(&S.mma_done[1 - m], fpar);
                         ptx::tc_fence_after();
                     }
                     if (ch == 0) {
@@ -430,8 +429,8 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                     ptx::tc_fence_after();
                     const uint32_t b0 = ptx::smem_u32(&S.B[0]);
                     const uint32_t bi0 = ptx::smem_u32(&S.BI[0][0]), bi1 = ptx::smem_u32(&S.BI[1][0]);
-                    // K-step groups in chunk order, all four arrays each, a commit after every group so
-                    // that the other M-tile can overwrite A chunk by chunk
+                    // K-step groups (ks0 = chunks 0-1, ks1 = 2-3, fold a = 3-4, ks2 = 4-5, fold b = 5-6),
+                    // all arrays each
                     const uint32_t aoff[5] = {0, 8, 12, 16, 20};
                     const uint64_t bdesc[5] = {ptx::smem_desc(b0, 128, B1_PITCH), ptx::smem_desc(b0 + 256, 128, B1_PITCH),
                                                ptx::smem_desc(bi0, 128, BI_PITCH), ptx::smem_desc(b0 + 512, 128, B1_PITCH),
@@ -442,8 +441,8 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
                         for (int pa = 0; pa < NA; ++pa)
                             ptx::mma_i8_ts(tmem + m * TA_D_TILE + pa * TA_D_ARR, tmem + TA_A0 + pa * TA_A_ARR + aoff[g],
                                            bdesc[g], IDESC, g > 0 ? 1u : 0u);
-                        ptx::mma_commit(&S.a_free[m][g]);
                     }
+                    ptx::mma_commit(&S.mma_done[m]);   // one commit for the layer's 20 MMAs
                     TRI(6);
                 }
                 __syncwarp();
@@ -508,7 +507,7 @@ __global__ void __launch_bounds__(512, 1) step_i8ws(const StepParams p) {
             double fb[12], ft[12];                   // bottom corners (local nodes 0-3), top (4-7): [corner][c]
             const bool has_layer = L < Lend;
             if (has_layer) {
-                ptx::mbar_wait_sleep(&S.a_free[m][4], (uint32_t)(k & 1));   // all MMAs of layer L
+                ptx::mbar_wait_sleep(&S.mma_done[m], (uint32_t)(k & 1));   // all MMAs of layer L
                 TRW(1);
                 ptx::tc_fence_after();
                 uint32_t alo, ahi;
