@@ -1,20 +1,23 @@
-// step_i8ws.cuh — warp-specialised INT8 time step (OVX_INT8, OVX_I8_KERNEL=ws); included by
+// step_i8ws.cuh — warp-specialised INT8 time step (OVX_INT8, the default kernel); included by
 // kernels.cu after step_i8w.cuh (whose B-operand image, TMEM layout and limb it shares).
 //
 // Same arithmetic, tile, TMEM layout and node-sum order as step_i8w (bit-identical results), with
 // every warp in ONE role for the whole kernel instead of alternating roles each half-iteration:
 //   warps 0-3  converters of M-tile 0 (element rows 0-3; one thread per element: s_e, the 48 scaled
-//              F2I conversions, byte packing, the A operand to TMEM), warp 0 issues its MMAs;
+//              F2I conversions, byte packing, the A operand to TMEM) and loaders of the node planes
+//              (cp.async, with warps 4-7), warp 0 issues the M-tile's MMAs;
 //   warps 4-7  converters of M-tile 1 (rows 4-7), warp 4 issues;
 //   warps 8-11 / 12-15  epilogues of M-tiles 0 / 1 (one thread per element: all 24 outputs from
 //              TMEM, exact limbs, the face sums in the order of reading U2, the update of the
-//              element's (−x,−y) node), and the plane loads (cp.async) for both roles.
-// Hand-offs are mbarriers (plane ready, MMA complete, D free, the row-3 → row-4 face-sum exchange
-// across M-tiles) and one named barrier per role group; the element scale α travels with the A
-// operand through TMEM (spare columns 496-503: per M-tile, by layer parity), so it is ordered like D.  The
-// converters run up to two layers ahead of the epilogues.  The two M-tiles share the TMEM A operand (their MMAs alternate),
-// as in step_i8w.  Undamped time steps and products only (damped steps and the debug records use
-// step_i8w).
+//              element's (−x,−y) node).
+// Hand-offs are mbarriers (plane ready, MMAs complete — one commit per M-tile and layer, waited for
+// once by the other M-tile's converters before their first store into the shared A operand and by
+// the epilogues —, D free, the row-3 → row-4 face-sum exchange across M-tiles) and one named barrier
+// per role group; the element scale α travels with the A operand through TMEM (spare columns
+// 496-503: per M-tile, by layer parity), so it is ordered like D.  The converters run up to two
+// layers ahead of the epilogues.  The two M-tiles share the TMEM A operand (their MMAs alternate), as
+// in step_i8w.  Time steps (DAMP: Rayleigh damping), products, M = 4 / 6 / 8 stages; the debug
+// records and the direct N-stage path use step_i8w.  DESIGN.md §6 / §6.1 has the measurements.
 
 #ifdef OVX_TRACE   // per-warp clock64 stamps of one CTA (tools/trace_ws.py): layers TRK0 .. TRK0+TRH-1
 #define TRK0 20
